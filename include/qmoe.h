@@ -1,0 +1,167 @@
+/*
+ * qmoe.h — C ABI of libqmoe.so, the B200 (sm_100a) expert-level preemptive MoE path.
+ *
+ * Every entry point:
+ *   - takes raw DEVICE pointers plus sizes and a cudaStream_t (passed as void*),
+ *   - enqueues asynchronously on that stream, never allocates (workspace is caller-provided),
+ *   - never synchronises the host (no hidden cudaDeviceSynchronize / D2H copies),
+ *   - returns an int status (QMOE_OK == 0).  The Python host maps the codes onto the
+ *     reference's exception classes (core.py:20-37 in the reference):
+ *       QMOE_ERR_INVALID   -> ValueError
+ *       QMOE_ERR_STATE     -> StateCorruptionError
+ *       QMOE_ERR_PARTIAL   -> PartialTokenError
+ *       QMOE_ERR_CAPACITY  -> CacheCapacityError
+ *       QMOE_ERR_CUDA / QMOE_ERR_UNSUPPORTED -> RuntimeError
+ *
+ * The reference (moesim, pure Python/numpy) has no native boundary: these functions replace
+ * the numeric calls the engine makes into its model plugin.  Each declaration cites the
+ * reference call site it replaces (paths relative to /root/reference/pkg/src/moesim/).
+ *
+ * Layouts (all row-major, contiguous):
+ *   X        [T, d]            token hidden states of one batch, member-major then token order
+ *                              (engine.py:204-209 walks members -> tokens in this order)
+ *   W_router [E, d]            gate weight (model.py:99 w_router[l]; HF gate.weight)
+ *   ids      [T, k] int32      routed experts per token, ascending id (model.py:129)
+ *   w        [T, k]            routing weights, same order as ids
+ *   cursor   [T] int32         per-token resume cursor: slot (t,j) is pending iff ids[t,j] >= cursor[t]
+ *                              (Checkpoint.pending_experts, core.py:101, compressed: experts drain
+ *                              in ascending id so pending == routed ∩ {e >= cursor})
+ *   perm     [R] int32         slot index s = t*k + j of the r-th entry in (expert, slot) order
+ *   offsets  [E+1] int32       expert e owns perm rows [offsets[e], offsets[e+1])
+ *   Xp       [R, d]            X rows gathered in perm order (Xp[r] = X[perm[r] / k])
+ *   Y        [T*k, d]          expert outputs in SLOT order (Checkpoint.completed_expert_outputs)
+ */
+#ifndef QMOE_H_
+#define QMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define QMOE_API __attribute__((visibility("default")))
+#else
+#define QMOE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------------------------- */
+#define QMOE_OK 0
+#define QMOE_ERR_INVALID 1
+#define QMOE_ERR_STATE 2
+#define QMOE_ERR_PARTIAL 3
+#define QMOE_ERR_CAPACITY 4
+#define QMOE_ERR_CUDA 5
+#define QMOE_ERR_UNSUPPORTED 6
+
+/* ---- element types --------------------------------------------------------------------- */
+#define QMOE_F64 0  /* reference precision (model.py:7-9 computes in fp64) */
+#define QMOE_F32 1
+#define QMOE_BF16 2 /* production precision: bf16 operands, fp32 accumulation */
+
+/* ---- router weight modes --------------------------------------------------------------- */
+#define QMOE_ROUTE_TOPK_SOFTMAX 0 /* softmax over the k picked logits (model.py:122-134; == HF Mixtral) */
+#define QMOE_ROUTE_SOFTMAX_TOPK 1 /* softmax over all E, keep top-k probs, no renorm (HF Qwen2-MoE,
+                                     norm_topk_prob=False; no reference counterpart) */
+
+/* ---- expert variants ------------------------------------------------------------------- */
+#define QMOE_EXPERT_TANH_AFFINE 0 /* y = tanh(A_e x + b_e)          (model.py:141-145)        */
+#define QMOE_EXPERT_SWIGLU 1      /* y = W2_e (SiLU(W1_e x) * W3_e x) (HF MixtralExperts)      */
+
+QMOE_API int qmoe_version(void);
+QMOE_API const char* qmoe_status_string(int status);
+/* Text of the last error raised on the calling thread (CUDA error string or validation msg). */
+QMOE_API const char* qmoe_last_error(void);
+
+/*
+ * Router (replaces MoEModel.route / route_many, model.py:115-134, called from
+ * InferenceEngine._router_stage, engine.py:303-310).
+ * logits = W_router · x per token, accumulated in fp32 (fp64 when dtype == QMOE_F64);
+ * top-k by (logit desc, id asc) — lower id wins ties (model.py:71-75) — ids written ascending.
+ * w_out has dtype F64 when dtype == QMOE_F64, else F32.  logits_out (optional, same float type
+ * as w_out) receives the raw [T, E] logits.  Requires 1 <= k <= E <= 64, k <= 8.
+ */
+QMOE_API int qmoe_router(const void* x, const void* w_router, int T, int d, int E, int k, int dtype,
+                int route_mode, int32_t* ids_out, void* w_out, void* logits_out, void* stream);
+
+/*
+ * Permute (replaces _enqueue_expert_work + ExpertQueues.enqueue/drain, engine.py:312-328,
+ * model.py:195-214, and the per-expert gather engine.py:207-209).
+ * Stable counting sort of the pending slots s = t*k + j by expert id: entries of one expert
+ * keep flat (member, token, j) order — exactly the FIFO order of the reference's (expert, layer)
+ * queue.  Writes perm, offsets[E+1] (offsets[E] = R), and, when x/xp are given, the gathered
+ * rows Xp (row_bytes = d * element size).  cursor may be NULL (all slots pending).
+ * workspace: qmoe_permute_workspace_bytes(T, k, E) bytes of device memory.
+ */
+QMOE_API size_t qmoe_permute_workspace_bytes(int T, int k, int E);
+QMOE_API int qmoe_permute(const int32_t* ids, const int32_t* cursor, int T, int k, int E,
+                 int32_t* perm_out, int32_t* offsets_out, void* workspace, size_t workspace_bytes,
+                 const void* x, void* xp, size_t row_bytes, void* stream);
+
+/*
+ * Grouped expert FFN over experts [e_begin, e_end) (replaces the drain loop body
+ * engine.py:205-215 → MoEModel.expert_forward_many, model.py:141-145).
+ * Reads Xp rows [offsets[e], offsets[e+1]) for each expert, writes Y[perm[r]] (slot order).
+ *   TANH_AFFINE: w1 = A [E, d, d] ([out, in]), w2 = b [E, d]; F ignored.
+ *   SWIGLU     : w1 = gate_up [E, 2F, d] (rows [0,F) gate, [F,2F) up), w2 = down [E, d, F];
+ *                act_ws = [R, F] scratch of the input dtype.
+ * dtype QMOE_BF16 runs on tcgen05/TMEM tensor cores (TMA-fed); F32/F64 run the SIMT path used
+ * for bit-faithful parity builds.
+ * preempt_flag (optional, device-visible, e.g. mapped host memory): polled at every expert
+ * boundary; once non-zero, no tile of a later expert is started.  cursor_out (optional, device
+ * int32[1]) receives the first expert NOT completed (== e_end when the launch ran to completion).
+ * xp_rows = allocated rows of Xp / act_ws (>= offsets[E]; bounds the TMA tensor maps).
+ * workspace: qmoe_expert_ffn_workspace_bytes() bytes of device memory (tile claim counters).
+ */
+QMOE_API size_t qmoe_expert_ffn_workspace_bytes(void);
+QMOE_API int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int32_t* offsets,
+                    const int32_t* perm, int E, int d, int F, const void* w1, const void* w2,
+                    int e_begin, int e_end, int xp_rows, void* act_ws, void* y,
+                    const volatile int32_t* preempt_flag, int32_t* cursor_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/*
+ * Combine (replaces InferenceEngine._finish_layer, engine.py:330-365, and MoEModel.combine,
+ * model.py:147-164): out[t] = residual[t] + sum_j w[t,j] * Y[t*k+j], j in ascending expert id
+ * (the order ids are stored in).  residual may be NULL (HF MoE-block semantics: the residual is
+ * added by the caller).  F64 mode rounds each product and each sum separately, matching the
+ * reference's `acc = acc + w*y` bit for bit given identical inputs.
+ * The caller must have checked that no slot is pending (PartialTokenError, engine.py:344-348).
+ */
+QMOE_API int qmoe_combine(int dtype, const void* y, const void* w, const void* residual, int T, int k, int d,
+                 void* out, void* stream);
+
+/*
+ * Row gather (restore of preempted state, engine.py:151-164 + _init_state engine.py:242-250):
+ * dst[i] = src[idx[i]] for i < rows.  Used to rebuild a merged resume batch's device state from
+ * per-sequence checkpoint rows without a host round trip.
+ */
+QMOE_API int qmoe_gather_rows(const void* src, const int32_t* idx, int rows, size_t row_bytes, void* dst,
+                     void* stream);
+
+/*
+ * Cursor advance after a (possibly partial) expert launch: for every token, the next pending
+ * expert becomes max(cursor[t], stop_expert) (pending = routed ∩ {e >= cursor}).  stop_expert is
+ * read from device memory (the grouped GEMM's cursor_out) so no host sync is needed.
+ */
+QMOE_API int qmoe_cursor_advance(int32_t* cursor, int T, const int32_t* stop_expert_dev, void* stream);
+
+/*
+ * Paged KV ownership (replaces UnifiedDynamicCache storage, model.py:231-329).
+ * pool: [n_pages, page_size, row_elems] of the given dtype; slot_mapping[i] = page*page_size +
+ * offset for the i-th new row; append copies rows[i] into that slot.  The page allocator and the
+ * byte ledger (reference units, entry = 2*d*8 bytes, model.py:277) live on the host.
+ */
+QMOE_API int qmoe_kv_append(void* pool, const int32_t* slot_mapping, const void* rows, int n_rows,
+                   size_t row_bytes, void* stream);
+/* dst[i] = pool[slot_mapping[i]] (one sequence's entries, ascending entry order). */
+QMOE_API int qmoe_kv_gather(const void* pool, const int32_t* slot_mapping, int n_rows, size_t row_bytes,
+                   void* dst, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QMOE_H_ */

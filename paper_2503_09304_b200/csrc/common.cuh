@@ -1,0 +1,80 @@
+// Shared helpers for libqmoe: status plumbing, element-type traits, small device utilities.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/qmoe.h"
+
+namespace qmoe {
+
+// Thread-local text of the last failure; surfaced by qmoe_last_error().
+void set_error(const char* fmt, ...);
+
+inline int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return QMOE_ERR_CUDA;
+  }
+  return QMOE_OK;
+}
+
+#define QMOE_REQUIRE(cond, ...)            \
+  do {                                     \
+    if (!(cond)) {                         \
+      ::qmoe::set_error(__VA_ARGS__);      \
+      return QMOE_ERR_INVALID;             \
+    }                                      \
+  } while (0)
+
+#define QMOE_CUDA_TRY(expr)                                                       \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      ::qmoe::set_error("%s failed: %s", #expr, cudaGetErrorString(_e));          \
+      return QMOE_ERR_CUDA;                                                       \
+    }                                                                             \
+  } while (0)
+
+inline size_t dtype_bytes(int dtype) {
+  switch (dtype) {
+    case QMOE_F64: return 8;
+    case QMOE_F32: return 4;
+    case QMOE_BF16: return 2;
+    default: return 0;
+  }
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- element conversion ---------------------------------------------------------------
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Accumulator-precision load: bf16/f32 inputs accumulate in f32, f64 in f64.
+template <typename T> struct AccOf { using type = float; };
+template <> struct AccOf<double> { using type = double; };
+
+template <typename T, typename A> __device__ __forceinline__ A load_as(const T* p) {
+  return static_cast<A>(to_f32<T>(*p));
+}
+template <> __device__ __forceinline__ double load_as<double, double>(const double* p) { return *p; }
+
+template <typename T, typename A> __device__ __forceinline__ void store_from(T* p, A v) {
+  *p = from_f32<T>(static_cast<float>(v));
+}
+template <> __device__ __forceinline__ void store_from<double, double>(double* p, double v) { *p = v; }
+
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+}  // namespace qmoe

@@ -1,0 +1,69 @@
+// qmoe_expert_ffn entry point: validation, workspace reset/finalize, SIMT vs tcgen05 dispatch.
+#include "expert_common.cuh"
+
+namespace qmoe {
+namespace {
+
+__global__ void ffn_finalize_kernel(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out) {
+  int c = INT_MAX - ws->stop_inv;
+  if (c > e_end) c = e_end;
+  if (limit != nullptr && *limit < c) c = *limit;
+  ws->stop = c;
+  if (cursor_out != nullptr) *cursor_out = c;
+}
+
+}  // namespace
+
+int ffn_ws_reset(FfnWorkspace* ws, cudaStream_t s) {
+  QMOE_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(FfnWorkspace) * kFfnWorkspaceSlots, s));
+  return QMOE_OK;
+}
+
+int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out, cudaStream_t s) {
+  ffn_finalize_kernel<<<1, 1, 0, s>>>(ws, limit, e_end, cursor_out);
+  return check_launch("qmoe_expert_ffn(finalize)");
+}
+
+}  // namespace qmoe
+
+extern "C" size_t qmoe_expert_ffn_workspace_bytes(void) {
+  return sizeof(qmoe::FfnWorkspace) * qmoe::kFfnWorkspaceSlots;
+}
+
+extern "C" int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int32_t* offsets,
+                               const int32_t* perm, int E, int d, int F, const void* w1, const void* w2,
+                               int e_begin, int e_end, int xp_rows, void* act_ws, void* y,
+                               const volatile int32_t* preempt_flag, int32_t* cursor_out, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(variant == QMOE_EXPERT_TANH_AFFINE || variant == QMOE_EXPERT_SWIGLU,
+               "qmoe_expert_ffn: unknown variant %d", variant);
+  QMOE_REQUIRE(E >= 1 && E <= 64 && d >= 1, "qmoe_expert_ffn: bad sizes E=%d d=%d", E, d);
+  QMOE_REQUIRE(variant == QMOE_EXPERT_TANH_AFFINE || F >= 1, "qmoe_expert_ffn: SwiGLU needs F >= 1");
+  QMOE_REQUIRE(0 <= e_begin && e_begin <= e_end && e_end <= E, "qmoe_expert_ffn: bad expert range [%d, %d)",
+               e_begin, e_end);
+  QMOE_REQUIRE(workspace != nullptr && workspace_bytes >= qmoe_expert_ffn_workspace_bytes(),
+               "qmoe_expert_ffn: workspace too small");
+  QMOE_REQUIRE(offsets && w1 && y && (xp_rows == 0 || (xp && perm)), "qmoe_expert_ffn: null pointer");
+  QMOE_REQUIRE(variant != QMOE_EXPERT_SWIGLU || act_ws != nullptr, "qmoe_expert_ffn: SwiGLU needs act_ws");
+  QMOE_REQUIRE(variant != QMOE_EXPERT_TANH_AFFINE || w2 != nullptr, "qmoe_expert_ffn: tanh expert needs bias");
+  FfnWorkspace* ws = reinterpret_cast<FfnWorkspace*>(workspace);
+  cudaStream_t s = as_stream(stream);
+  if (xp_rows == 0 || e_begin == e_end) {
+    int st = ffn_ws_reset(ws, s);
+    if (st) return st;
+    return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
+  }
+  switch (dtype) {
+    case QMOE_F64:
+    case QMOE_F32:
+      return expert_ffn_simt(variant, dtype, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y,
+                             preempt_flag, cursor_out, ws, s);
+    case QMOE_BF16:
+      return expert_ffn_tc(variant, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, preempt_flag,
+                           cursor_out, ws, xp_rows, s);
+    default:
+      set_error("qmoe_expert_ffn: unknown dtype %d", dtype);
+      return QMOE_ERR_INVALID;
+  }
+}

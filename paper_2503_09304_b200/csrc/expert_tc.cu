@@ -1,0 +1,352 @@
+// Grouped expert FFN on 5th-gen tensor cores (tcgen05 + TMEM), TMA-fed, persistent and
+// warp-specialised — the production bf16 path of qmoe_expert_ffn.
+//
+// Replaces the reference's per-expert drain (engine.py:204-215 → model.py:141-145) and, for the
+// north-star SwiGLU expert, HF MixtralExperts.forward (gate_up → SiLU(g)*u → down).
+//
+// One CTA per SM, 256 threads:
+//   warp 0  TMA producer: claims tiles (expert-major, device preempt flag checked at each claim),
+//           streams A (gathered token rows) and B (expert weights) 128x64 / BNx64 bf16 tiles into
+//           a kStages-deep 128B-swizzled smem ring (mbarrier complete_tx).
+//   warp 1  MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16)
+//           into a double-buffered fp32 TMEM accumulator (2 x BN columns of 512).
+//   warp 2  TMEM allocator.
+//   warps 4-7 epilogue: tcgen05.ld 32 lanes x 32 columns, fused SiLU(g)*u / bias+tanh / plain,
+//           bf16 pack, 16-byte stores to act rows (expert order) or Y slot rows (perm scatter).
+// The TMEM double buffer lets the epilogue of tile i overlap the MMAs of tile i+1.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "expert_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace qmoe {
+namespace {
+
+constexpr int BM = 128, BK = 64;
+constexpr int kStages = 4;
+constexpr int kAccStages = 2;
+constexpr int kTileRing = 4;
+constexpr int kThreads = 256;
+constexpr int kEpiWarp0 = 4;
+
+enum { EPI_TANH = 0, EPI_SWIGLU = 1, EPI_DOWN = 2 };
+
+struct TcParams {
+  int N;         // output columns of this GEMM (act columns F for the SwiGLU gate_up pass)
+  int K;         // reduction length
+  int b_rows;    // rows of the B operand per expert (N, or 2F for gate_up)
+  int e_begin, e_end;
+  const int32_t* offsets;
+  const int32_t* perm;
+  const int32_t* e_limit;
+  const __nv_bfloat16* bias;  // [E, N] for the tanh expert
+  __nv_bfloat16* out;
+  int out_ld;
+  const volatile int32_t* flag;
+  FfnWorkspace* ws;
+};
+
+template <int BN>
+constexpr int stage_bytes() { return BM * BK * 2 + BN * BK * 2; }
+template <int BN>
+constexpr int smem_bytes() { return kStages * stage_bytes<BN>() + 1024; }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar[kAccStages], tempty_bar[kAccStages];
+  __shared__ __align__(8) uint64_t ring_full[kTileRing], ring_empty[kTileRing];
+  __shared__ int ring_tile[kTileRing];
+  __shared__ uint32_t tmem_base_smem;
+  __shared__ TileMap map;
+
+  constexpr int BN_OUT = (EPI == EPI_SWIGLU) ? BN / 2 : BN;  // output columns per tile
+  constexpr int kStageBytes = stage_bytes<BN>();
+  constexpr int kABytes = BM * BK * 2;
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(BM, BN);
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles_n = (p.N + BN_OUT - 1) / BN_OUT;
+  const int nkb = (p.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    build_tile_map(map, p.offsets, p.e_begin, p.e_end, p.e_limit, BM, n_tiles_n);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < kAccStages; ++a) {
+      ptx::mbar_init(&tfull_bar[a], 1);
+      ptx::mbar_init(&tempty_bar[a], 4);
+    }
+    for (int i = 0; i < kTileRing; ++i) {
+      ptx::mbar_init(&ring_full[i], 1);
+      ptx::mbar_init(&ring_empty[i], 1 + 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<2 * BN>(&tmem_base_smem);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = tmem_base_smem;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmA);
+      ptx::tma_prefetch_desc(&tmB);
+      int stage = 0, slot = 0;
+      uint32_t phase = 0, rphase = 0;
+      while (true) {
+        const int tile = ffn_claim(map, p.ws, p.flag);
+        ptx::mbar_wait(&ring_empty[slot], rphase ^ 1);
+        ring_tile[slot] = tile;
+        ptx::mbar_arrive(&ring_full[slot]);
+        if (++slot == kTileRing) { slot = 0; rphase ^= 1; }
+        if (tile < 0) break;
+        int e, m0, n0;
+        map.locate(tile, BM, n_tiles_n, BN_OUT, e, m0, n0);
+        // B rows of this tile: two halves of BN/2 rows each.  gate_up: gate rows [n0, n0+BN/2),
+        // up rows F + [n0, n0+BN/2) so accumulator columns [0,BN/2) = gate, [BN/2,BN) = up.
+        const int brow0 = e * p.b_rows + n0;
+        const int brow1 = (EPI == EPI_SWIGLU) ? e * p.b_rows + p.N + n0 : brow0 + BN / 2;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          uint8_t* sb = sa + kABytes;
+          ptx::mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
+          ptx::tma_load_2d(&tmA, &full_bar[stage], sa, kb * BK, m0, ptx::kEvictNormal);
+          ptx::tma_load_2d(&tmB, &full_bar[stage], sb, kb * BK, brow0, ptx::kEvictNormal);
+          ptx::tma_load_2d(&tmB, &full_bar[stage], sb + (BN / 2) * 128, kb * BK, brow1, ptx::kEvictNormal);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0, slot = 0, acc = 0;
+      uint32_t phase = 0, rphase = 0, aphase = 0;
+      while (true) {
+        ptx::mbar_wait(&ring_full[slot], rphase);
+        const int tile = ring_tile[slot];
+        ptx::mbar_arrive(&ring_empty[slot]);
+        if (++slot == kTileRing) { slot = 0; rphase ^= 1; }
+        if (tile < 0) break;
+        ptx::mbar_wait(&tempty_bar[acc], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem + stage * kStageBytes);
+          const uint32_t b_addr = a_addr + kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            ptx::tc_mma_bf16(d_tmem, ptx::sw128_kmajor_desc(a_addr + k * 32), ptx::sw128_kmajor_desc(b_addr + k * 32),
+                             kIdesc, (kb | k) != 0);
+          }
+          ptx::tc_commit(&empty_bar[stage]);  // smem slot free once these MMAs retire
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        ptx::tc_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        if (++acc == kAccStages) { acc = 0; aphase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------------------------ epilogue
+    const int ew = warp - kEpiWarp0;  // TMEM lanes [32*ew, 32*ew+32)
+    int slot = 0, acc = 0;
+    uint32_t rphase = 0, aphase = 0;
+    while (true) {
+      ptx::mbar_wait(&ring_full[slot], rphase);
+      const int tile = ring_tile[slot];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&ring_empty[slot]);
+      if (++slot == kTileRing) { slot = 0; rphase ^= 1; }
+      if (tile < 0) break;
+      int e, m0, n0;
+      map.locate(tile, BM, n_tiles_n, BN_OUT, e, m0, n0);
+      const int row = m0 + ew * 32 + lane;
+      const bool valid = row < p.offsets[e + 1];
+      __nv_bfloat16* dst_row = nullptr;
+      if (valid) {
+        const size_t orow = (EPI == EPI_SWIGLU) ? (size_t)row : (size_t)p.perm[row];
+        dst_row = p.out + orow * p.out_ld;
+      }
+      ptx::mbar_wait(&tfull_bar[acc], aphase);
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN_OUT; c += 32) {
+        uint32_t v[32];
+        ptx::tmem_ld32(t_row + c, v);
+        uint32_t packed[16];
+        if constexpr (EPI == EPI_SWIGLU) {
+          uint32_t u[32];
+          ptx::tmem_ld32(t_row + BN / 2 + c, u);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float g0 = __uint_as_float(v[2 * i]), g1 = __uint_as_float(v[2 * i + 1]);
+            const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+            packed[i] = pack_bf16(g0 / (1.f + __expf(-g0)) * u0, g1 / (1.f + __expf(-g1)) * u1);
+          }
+        } else if constexpr (EPI == EPI_TANH) {
+          ptx::tmem_ld_wait();
+          const __nv_bfloat16* b = p.bias + (size_t)e * p.N + n0 + c;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float x0 = __uint_as_float(v[2 * i]) + __bfloat162float(b[2 * i]);
+            const float x1 = __uint_as_float(v[2 * i + 1]) + __bfloat162float(b[2 * i + 1]);
+            packed[i] = pack_bf16(tanhf(x0), tanhf(x1));
+          }
+        } else {
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        }
+        if (valid && n0 + c < p.N) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst_row + n0 + c);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            d4[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+      if (++acc == kAccStages) { acc = 0; aphase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<2 * BN>(tmem_base);
+  }
+}
+
+// ---- host side --------------------------------------------------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+int g_num_sms = 0;
+std::once_flag g_once;
+int g_init_status = QMOE_OK;
+
+int init_driver() {
+  std::call_once(g_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr) {
+      set_error("qmoe_expert_ffn: cuTensorMapEncodeTiled unavailable");
+      g_init_status = QMOE_ERR_CUDA;
+      return;
+    }
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10) {
+      set_error("qmoe_expert_ffn: tcgen05 path needs sm_100 (found sm_%d%d)", major, minor);
+      g_init_status = QMOE_ERR_UNSUPPORTED;
+    }
+  });
+  return g_init_status;
+}
+
+// 2D bf16 row-major [rows, cols] -> tensor map with box {64 cols, box_rows}, 128B swizzle.
+int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu", (int)r, (unsigned long long)rows,
+              (unsigned long long)cols);
+    return QMOE_ERR_CUDA;
+  }
+  return QMOE_OK;
+}
+
+template <int BN, int EPI>
+int launch_tc(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_bytes<BN>()));
+    attr_set = true;
+  }
+  ffn_tc_kernel<BN, EPI><<<g_num_sms, kThreads, smem_bytes<BN>(), s>>>(a, b, p);
+  return check_launch("qmoe_expert_ffn(tcgen05)");
+}
+
+}  // namespace
+
+int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
+                  const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
+                  const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
+                  cudaStream_t s) {
+  int st = init_driver();
+  if (st) return st;
+  QMOE_REQUIRE(d % 64 == 0, "qmoe_expert_ffn(bf16): d must be a multiple of 64 (d=%d)", d);
+  QMOE_REQUIRE(variant != QMOE_EXPERT_SWIGLU || F % 64 == 0, "qmoe_expert_ffn(bf16): F must be a multiple of 64");
+  QMOE_REQUIRE(((uintptr_t)xp | (uintptr_t)w1 | (uintptr_t)y | (uintptr_t)(act_ws ? act_ws : y)) % 16 == 0,
+               "qmoe_expert_ffn(bf16): buffers must be 16-byte aligned");
+  constexpr int BN = 256;
+  if ((st = ffn_ws_reset(ws, s))) return st;
+  TcParams p{};
+  p.e_begin = e_begin;
+  p.e_end = e_end;
+  p.offsets = offsets;
+  p.perm = perm;
+  p.flag = flag;
+  CUtensorMap ta, tb;
+  if (variant == QMOE_EXPERT_TANH_AFFINE) {
+    if ((st = make_map(&ta, xp, xp_rows, d, BM)) || (st = make_map(&tb, w1, (uint64_t)E * d, d, BN / 2))) return st;
+    p.N = d; p.K = d; p.b_rows = d;
+    p.bias = (const __nv_bfloat16*)w2;
+    p.out = (__nv_bfloat16*)y; p.out_ld = d;
+    p.ws = ws;
+    if ((st = launch_tc<BN, EPI_TANH>(ta, tb, p, s))) return st;
+    return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
+  }
+  // gate_up: act[r, :F] = SiLU(x W1^T) * (x W3^T), expert order rows
+  if ((st = make_map(&ta, xp, xp_rows, d, BM)) || (st = make_map(&tb, w1, (uint64_t)E * 2 * F, d, BN / 2))) return st;
+  p.N = F; p.K = d; p.b_rows = 2 * F;
+  p.out = (__nv_bfloat16*)act_ws; p.out_ld = F;
+  p.ws = ws + 0;
+  if ((st = launch_tc<BN, EPI_SWIGLU>(ta, tb, p, s))) return st;
+  if ((st = ffn_finalize(ws + 0, nullptr, e_end, nullptr, s))) return st;
+  // down: Y[perm[r], :d] = act[r] W2^T, only experts whose gate_up completed
+  CUtensorMap ta2, tb2;
+  if ((st = make_map(&ta2, act_ws, xp_rows, F, BM)) || (st = make_map(&tb2, w2, (uint64_t)E * d, F, BN / 2))) return st;
+  TcParams p2 = p;
+  p2.N = d; p2.K = F; p2.b_rows = d;
+  p2.out = (__nv_bfloat16*)y; p2.out_ld = d;
+  p2.e_limit = &ws[0].stop;
+  p2.ws = ws + 1;
+  if ((st = launch_tc<BN, EPI_DOWN>(ta2, tb2, p2, s))) return st;
+  return ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s);
+}
+
+}  // namespace qmoe

@@ -1,0 +1,213 @@
+"""Torch-facing wrappers over the libqmoe C ABI.
+
+torch is plumbing here: it owns device memory and the current stream; every computation below
+is one of the library's sm_100a kernels.  Each wrapper validates devices/dtypes/shapes, passes
+raw pointers plus ``torch.cuda.current_stream()`` and maps status codes onto the reference's
+exception classes.  Nothing here synchronises the host.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+DTYPE_CODE = {torch.float64: _lib.QMOE_F64, torch.float32: _lib.QMOE_F32, torch.bfloat16: _lib.QMOE_BF16}
+
+ROUTE_TOPK_SOFTMAX = _lib.QMOE_ROUTE_TOPK_SOFTMAX
+ROUTE_SOFTMAX_TOPK = _lib.QMOE_ROUTE_SOFTMAX_TOPK
+EXPERT_TANH_AFFINE = _lib.QMOE_EXPERT_TANH_AFFINE
+EXPERT_SWIGLU = _lib.QMOE_EXPERT_SWIGLU
+
+_workspaces: dict[tuple[int, int, str], torch.Tensor] = {}
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, name: str, dtype: Optional[torch.dtype] = None) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (libqmoe has no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def _code(t: torch.Tensor) -> int:
+    try:
+        return DTYPE_CODE[t.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported dtype {t.dtype}") from None
+
+
+def acc_dtype(dtype: torch.dtype) -> torch.dtype:
+    """Routing-weight dtype produced by the router for a given activation dtype."""
+    return torch.float64 if dtype == torch.float64 else torch.float32
+
+
+def workspace(nbytes: int, tag: str, device: torch.device) -> torch.Tensor:
+    """Stream-ordered scratch, grown on demand and reused (one buffer per device/stream/tag)."""
+    key = (device.index or 0, _stream(), tag)
+    buf = _workspaces.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _workspaces[key] = buf
+    return buf
+
+
+def router(x: torch.Tensor, w_router: torch.Tensor, k: int, mode: int = ROUTE_TOPK_SOFTMAX,
+           want_logits: bool = False):
+    """ids [T,k] int32 (ascending), weights [T,k] (f64 for f64 inputs else f32), optional logits."""
+    _need(x, "x")
+    _need(w_router, "w_router", x.dtype)
+    T, d = x.shape
+    E = w_router.shape[0]
+    if w_router.shape[1] != d:
+        raise ValueError("w_router must be [E, d]")
+    ids = torch.empty((T, k), dtype=torch.int32, device=x.device)
+    w = torch.empty((T, k), dtype=acc_dtype(x.dtype), device=x.device)
+    logits = torch.empty((T, E), dtype=w.dtype, device=x.device) if want_logits else None
+    lib = _lib.load()
+    check(lib.qmoe_router(_ptr(x), _ptr(w_router), T, d, E, k, _code(x), mode, _ptr(ids), _ptr(w), _ptr(logits),
+                          _stream()), "qmoe_router")
+    return (ids, w, logits) if want_logits else (ids, w)
+
+
+def permute(ids: torch.Tensor, num_experts: int, cursor: Optional[torch.Tensor] = None,
+            x: Optional[torch.Tensor] = None):
+    """Stable expert-major order of the pending slots.
+
+    Returns (perm [T*k] int32 — only the first offsets[E] entries are meaningful,
+    offsets [E+1] int32, xp [T*k, d] gathered rows or None)."""
+    _need(ids, "ids", torch.int32)
+    T, k = ids.shape
+    if cursor is not None:
+        _need(cursor, "cursor", torch.int32)
+        if cursor.shape != (T,):
+            raise ValueError("cursor must be [T]")
+    perm = torch.empty(T * k, dtype=torch.int32, device=ids.device)
+    offsets = torch.empty(num_experts + 1, dtype=torch.int32, device=ids.device)
+    xp = None
+    row_bytes = 0
+    if x is not None:
+        _need(x, "x")
+        if x.shape[0] != T:
+            raise ValueError("x must have one row per token")
+        xp = torch.empty((T * k, x.shape[1]), dtype=x.dtype, device=x.device)
+        row_bytes = x.shape[1] * x.element_size()
+    lib = _lib.load()
+    nbytes = lib.qmoe_permute_workspace_bytes(T, k, num_experts)
+    ws = workspace(nbytes, "permute", ids.device)
+    check(lib.qmoe_permute(_ptr(ids), _ptr(cursor), T, k, num_experts, _ptr(perm), _ptr(offsets), _ptr(ws), nbytes,
+                           _ptr(x), _ptr(xp), row_bytes, _stream()), "qmoe_permute")
+    return perm, offsets, xp
+
+
+def expert_ffn(variant: int, xp: torch.Tensor, offsets: torch.Tensor, perm: torch.Tensor, w1: torch.Tensor,
+               w2: torch.Tensor, y: torch.Tensor, e_begin: int = 0, e_end: Optional[int] = None,
+               act_ws: Optional[torch.Tensor] = None, preempt_flag: Optional[torch.Tensor] = None,
+               cursor_out: Optional[torch.Tensor] = None) -> None:
+    """Run experts [e_begin, e_end) over their rows of xp; results land in y[perm[r]] (slot order).
+
+    TANH_AFFINE: w1 = A [E, d, d], w2 = b [E, d].  SWIGLU: w1 = gate_up [E, 2F, d], w2 = down [E, d, F],
+    act_ws = [rows, F] scratch.  preempt_flag: int32 device-visible flag polled at expert boundaries;
+    cursor_out: int32 [1] device tensor receiving the first expert not completed."""
+    for name, t in (("xp", xp), ("w1", w1), ("w2", w2), ("y", y)):
+        _need(t, name, xp.dtype)
+    _need(offsets, "offsets", torch.int32)
+    _need(perm, "perm", torch.int32)
+    E = w1.shape[0]
+    d = xp.shape[1]
+    if variant == EXPERT_SWIGLU:
+        F = w1.shape[1] // 2
+        if w1.shape != (E, 2 * F, d) or w2.shape != (E, d, F):
+            raise ValueError("SwiGLU weights must be gate_up [E, 2F, d] and down [E, d, F]")
+        if act_ws is None:
+            act_ws = torch.empty((xp.shape[0], F), dtype=xp.dtype, device=xp.device)
+        _need(act_ws, "act_ws", xp.dtype)
+        if act_ws.shape[0] < xp.shape[0] or act_ws.shape[1] != F:
+            raise ValueError("act_ws must be [rows >= xp rows, F]")
+    else:
+        F = 0
+        if w1.shape != (E, d, d) or w2.shape != (E, d):
+            raise ValueError("tanh expert weights must be A [E, d, d] and b [E, d]")
+    if offsets.shape != (E + 1,):
+        raise ValueError("offsets must be [E+1]")
+    if e_end is None:
+        e_end = E
+    if preempt_flag is not None and preempt_flag.dtype != torch.int32:
+        raise ValueError("preempt_flag must be int32")
+    lib = _lib.load()
+    nbytes = lib.qmoe_expert_ffn_workspace_bytes()
+    ws = workspace(nbytes, "ffn", xp.device)
+    check(lib.qmoe_expert_ffn(variant, _code(xp), _ptr(xp), _ptr(offsets), _ptr(perm), E, d, F, _ptr(w1), _ptr(w2),
+                              e_begin, e_end, xp.shape[0], _ptr(act_ws), _ptr(y), _ptr(preempt_flag),
+                              _ptr(cursor_out), _ptr(ws), nbytes, _stream()), "qmoe_expert_ffn")
+
+
+def combine(y: torch.Tensor, w: torch.Tensor, residual: Optional[torch.Tensor], out: Optional[torch.Tensor] = None):
+    """out[t] = residual[t] + sum_j w[t,j] * y[t*k+j]  (j ascending expert id)."""
+    T, k = w.shape
+    d = y.shape[1]
+    _need(y, "y")
+    _need(w, "w", acc_dtype(y.dtype))
+    if y.shape[0] != T * k:
+        raise ValueError("y must hold T*k slot rows")
+    if residual is not None:
+        _need(residual, "residual", y.dtype)
+    if out is None:
+        out = torch.empty((T, d), dtype=y.dtype, device=y.device)
+    lib = _lib.load()
+    check(lib.qmoe_combine(_code(y), _ptr(y), _ptr(w), _ptr(residual), T, k, d, _ptr(out), _stream()),
+          "qmoe_combine")
+    return out
+
+
+def gather_rows(src: torch.Tensor, idx: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """out[i] = src[idx[i]] (device row gather used to rebuild resumed batches)."""
+    _need(src, "src")
+    _need(idx, "idx", torch.int32)
+    rows = idx.shape[0]
+    if out is None:
+        out = torch.empty((rows,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else 1
+    lib = _lib.load()
+    check(lib.qmoe_gather_rows(_ptr(src), _ptr(idx), rows, row_bytes, _ptr(out), _stream()), "qmoe_gather_rows")
+    return out
+
+
+def cursor_advance(cursor: torch.Tensor, stop_dev: torch.Tensor) -> None:
+    _need(cursor, "cursor", torch.int32)
+    _need(stop_dev, "stop", torch.int32)
+    lib = _lib.load()
+    check(lib.qmoe_cursor_advance(_ptr(cursor), cursor.shape[0], _ptr(stop_dev), _stream()), "qmoe_cursor_advance")
+
+
+def kv_append(pool: torch.Tensor, slot_mapping: torch.Tensor, rows: torch.Tensor) -> None:
+    _need(pool, "pool")
+    _need(rows, "rows", pool.dtype)
+    _need(slot_mapping, "slot_mapping", torch.int32)
+    n = rows.shape[0]
+    row_bytes = rows[0].numel() * rows.element_size() if n else 1
+    lib = _lib.load()
+    check(lib.qmoe_kv_append(_ptr(pool), _ptr(slot_mapping), _ptr(rows), n, row_bytes, _stream()), "qmoe_kv_append")
+
+
+def kv_gather(pool: torch.Tensor, slot_mapping: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    _need(pool, "pool")
+    _need(out, "out", pool.dtype)
+    _need(slot_mapping, "slot_mapping", torch.int32)
+    n = slot_mapping.shape[0]
+    row_bytes = out[0].numel() * out.element_size() if n else 1
+    lib = _lib.load()
+    check(lib.qmoe_kv_gather(_ptr(pool), _ptr(slot_mapping), n, row_bytes, _ptr(out), _stream()), "qmoe_kv_gather")
+    return out
