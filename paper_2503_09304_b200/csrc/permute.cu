@@ -15,7 +15,7 @@
 namespace qmoe {
 namespace {
 
-constexpr int kChunk = 4096;      // slots per CTA
+constexpr int kChunk = 2048;      // slots per CTA
 constexpr int kPass = 512;        // slots ranked per pass (one per thread)
 constexpr int kThreads = kPass;
 constexpr int kWarpsPer = kThreads / 32;
@@ -62,9 +62,20 @@ __device__ __forceinline__ void copy_row(const uint8_t* __restrict__ src, uint8_
   }
 }
 
+// Wide row gather for multi-chunk launches: Xp[r] = X[perm[r] / k], one warp per row.
+__global__ void __launch_bounds__(256) perm_gather_kernel(const int32_t* __restrict__ perm,
+                                                          const int32_t* __restrict__ offsets, int E, int k,
+                                                          int max_rows, const uint8_t* __restrict__ x,
+                                                          uint8_t* __restrict__ xp, size_t row_bytes) {
+  const int R = offsets[E];
+  const int lane = lane_id();
+  for (int r = blockIdx.x * 8 + warp_id(); r < R && r < max_rows; r += gridDim.x * 8)
+    copy_row(x + (size_t)(perm[r] / k) * row_bytes, xp + (size_t)r * row_bytes, row_bytes, lane);
+}
+
 __global__ void __launch_bounds__(kThreads)
 perm_scatter_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ cursor, int S, int k,
-                    int E, int nblk, const int32_t* __restrict__ hist, int32_t* __restrict__ perm,
+                    int E, int nblk, int32_t* __restrict__ hist, int32_t* __restrict__ perm,
                     int32_t* __restrict__ offsets, const uint8_t* __restrict__ x, uint8_t* __restrict__ xp,
                     size_t row_bytes) {
   __shared__ int base[kMaxE];
@@ -74,6 +85,19 @@ perm_scatter_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__
   __shared__ int s_src[kPass];
   const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
 
+  // Single-chunk launches (decode-sized batches) count in-kernel: one launch does everything.
+  if (nblk == 1) {
+    __shared__ int h1[kMaxE];
+    for (int e = tid; e < E; e += kThreads) h1[e] = 0;
+    __syncthreads();
+    for (int s = tid; s < S; s += kThreads) {
+      const int e = slot_expert(ids, cursor, s, k, E);
+      if (e >= 0) atomicAdd(&h1[e], 1);
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += kThreads) hist[e] = h1[e];
+    __syncthreads();
+  }
   // Exclusive base of this chunk for every expert: expert start + counts of earlier chunks.
   if (warp == 0) {
     int tot_e[2] = {0, 0}, pre_e[2] = {0, 0};
@@ -188,10 +212,23 @@ extern "C" int qmoe_permute(const int32_t* ids, const int32_t* cursor, int T, in
   QMOE_REQUIRE(ids && perm_out && workspace, "qmoe_permute: null pointer");
   const int nblk = (int)((S + kChunk - 1) / kChunk);
   int32_t* hist = reinterpret_cast<int32_t*>(workspace);
-  perm_count_kernel<<<nblk, 256, 0, s>>>(ids, cursor, (int)S, k, E, hist);
-  int st = check_launch("qmoe_permute(count)");
-  if (st) return st;
+  int st;
+  if (nblk > 1) {  // multi-chunk: per-chunk histograms first
+    perm_count_kernel<<<nblk, 256, 0, s>>>(ids, cursor, (int)S, k, E, hist);
+    if ((st = check_launch("qmoe_permute(count)"))) return st;
+  }
+  // one CTA: count + rank + scatter + gather fused; many CTAs: gather runs wide afterwards
+  const bool inline_gather = S <= 32;  // decode-sized: one launch; otherwise gather wide
   perm_scatter_kernel<<<nblk, kThreads, 0, s>>>(ids, cursor, (int)S, k, E, nblk, hist, perm_out, offsets_out,
-                                                (const uint8_t*)x, (uint8_t*)xp, row_bytes);
-  return check_launch("qmoe_permute(scatter)");
+                                                (const uint8_t*)x, inline_gather ? (uint8_t*)xp : nullptr,
+                                                row_bytes);
+  if ((st = check_launch("qmoe_permute(scatter)"))) return st;
+  if (xp != nullptr && !inline_gather) {
+    const int rows = (int)S;
+    const int grid = rows / 8 < 148 * 16 ? (rows + 7) / 8 : 148 * 16;
+    perm_gather_kernel<<<grid, 256, 0, s>>>(perm_out, offsets_out, E, k, rows, (const uint8_t*)x, (uint8_t*)xp,
+                                            row_bytes);
+    if ((st = check_launch("qmoe_permute(gather)"))) return st;
+  }
+  return QMOE_OK;
 }

@@ -2,7 +2,7 @@
 //
 // Replaces MoEModel.route / route_many (reference model.py:115-134) and select_top_k /
 // softmax_over (model.py:71-80).  HBM-bound on X: each token row is read once; W_router (E x d)
-// stays L1/L2-resident and is reused across the TPW tokens a warp owns (register blocking).
+// stays L1/L2-resident and is reused across the TPC tokens a CTA owns (register blocking).
 #include "common.cuh"
 
 namespace qmoe {
@@ -44,93 +44,95 @@ template <typename A> __device__ __forceinline__ A warp_sum(A v) {
 __device__ __forceinline__ float exp_acc(float v) { return expf(v); }
 __device__ __forceinline__ double exp_acc(double v) { return exp(v); }
 
+// One CTA owns TPC tokens; its kWarps warps split the hidden dimension (so a decode batch still
+// spreads over many CTAs), every lane keeps TPC x kExpChunk partial dot products in registers,
+// and all loads of one step (TPC token vectors + kExpChunk weight vectors) are issued before any
+// FMA so they are in flight together.  Partials are reduced across lanes (shuffles) and warps
+// (shared memory); then one thread per token does the top-k selection.
 // VEC: true -> 16-byte vector loads (requires d % Vec<T>::N == 0 and aligned rows).
-template <typename T, int TPW, bool VEC>
+template <typename T, int TPC, bool VEC>
 __global__ void __launch_bounds__(kWarps * 32)
 router_kernel(const T* __restrict__ x, const T* __restrict__ wr, int ntok, int d, int E, int k,
               int mode, int32_t* __restrict__ ids_out, typename AccOf<T>::type* __restrict__ w_out,
               typename AccOf<T>::type* __restrict__ logits_out) {
   using A = typename AccOf<T>::type;
-  __shared__ A s_logit[kWarps][TPW][kMaxE];
+  __shared__ A s_part[kWarps][TPC][kExpChunk];
+  __shared__ A s_logit[TPC][kMaxE];
   const int warp = warp_id(), lane = lane_id();
-  const int tok0 = (blockIdx.x * kWarps + warp) * TPW;
+  const int tok0 = blockIdx.x * TPC;
+  constexpr int N = VEC ? Vec<T>::N : 1;
+  // d range of this warp, in units of N elements
+  const int nvec = d / N;
+  const int per_warp = (nvec + kWarps - 1) / kWarps;
+  const int v0 = warp * per_warp, v1 = min(nvec, v0 + per_warp);
 
   for (int ec = 0; ec < E; ec += kExpChunk) {
-    A acc[TPW][kExpChunk];
+    A acc[TPC][kExpChunk];
 #pragma unroll
-    for (int t = 0; t < TPW; ++t)
+    for (int t = 0; t < TPC; ++t)
 #pragma unroll
       for (int j = 0; j < kExpChunk; ++j) acc[t][j] = A(0);
+    const T* wrow[kExpChunk];
+#pragma unroll
+    for (int j = 0; j < kExpChunk; ++j) wrow[j] = wr + (size_t)min(ec + j, E - 1) * d;  // clamp: no branch
+    const T* xrow[TPC];
+#pragma unroll
+    for (int t = 0; t < TPC; ++t) xrow[t] = x + (size_t)min(tok0 + t, ntok - 1) * d;
 
-    if constexpr (VEC) {
-      constexpr int N = Vec<T>::N;
-      using U = typename Vec<T>::U;
-      for (int i = lane * N; i < d; i += 32 * N) {
-        A xv[TPW][N];
+    for (int v = v0 + lane; v < v1; v += 32) {
+      A xv[TPC][N], wv[kExpChunk][N];
+      if constexpr (VEC) {
+        using U = typename Vec<T>::U;
+        U xu[TPC], wu[kExpChunk];
 #pragma unroll
-        for (int t = 0; t < TPW; ++t) {
-          const int tok = tok0 + t;
-          if (tok < ntok) {
-            U u = *reinterpret_cast<const U*>(x + (size_t)tok * d + i);
-            unpack<T, A>(u, xv[t]);
-          } else {
+        for (int t = 0; t < TPC; ++t) xu[t] = *reinterpret_cast<const U*>(xrow[t] + (size_t)v * N);
 #pragma unroll
-            for (int q = 0; q < N; ++q) xv[t][q] = A(0);
-          }
-        }
+        for (int j = 0; j < kExpChunk; ++j) wu[j] = __ldg(reinterpret_cast<const U*>(wrow[j] + (size_t)v * N));
 #pragma unroll
-        for (int j = 0; j < kExpChunk; ++j) {
-          const int e = ec + j;
-          if (e < E) {
-            A wv[N];
-            U u = __ldg(reinterpret_cast<const U*>(wr + (size_t)e * d + i));
-            unpack<T, A>(u, wv);
+        for (int t = 0; t < TPC; ++t) unpack<T, A>(xu[t], xv[t]);
 #pragma unroll
-            for (int t = 0; t < TPW; ++t)
+        for (int j = 0; j < kExpChunk; ++j) unpack<T, A>(wu[j], wv[j]);
+      } else {
 #pragma unroll
-              for (int q = 0; q < N; ++q) acc[t][j] += xv[t][q] * wv[q];
-          }
-        }
+        for (int t = 0; t < TPC; ++t) xv[t][0] = load_as<T, A>(xrow[t] + v);
+#pragma unroll
+        for (int j = 0; j < kExpChunk; ++j) wv[j][0] = load_as<T, A>(wrow[j] + v);
       }
-    } else {
-      for (int i = lane; i < d; i += 32) {
-        A xv[TPW];
 #pragma unroll
-        for (int t = 0; t < TPW; ++t) {
-          const int tok = tok0 + t;
-          xv[t] = tok < ntok ? load_as<T, A>(x + (size_t)tok * d + i) : A(0);
-        }
+      for (int t = 0; t < TPC; ++t)
 #pragma unroll
-        for (int j = 0; j < kExpChunk; ++j) {
-          const int e = ec + j;
-          if (e < E) {
-            const A wv = load_as<T, A>(wr + (size_t)e * d + i);
+        for (int j = 0; j < kExpChunk; ++j)
 #pragma unroll
-            for (int t = 0; t < TPW; ++t) acc[t][j] += xv[t] * wv;
-          }
-        }
-      }
+          for (int q = 0; q < N; ++q) acc[t][j] += xv[t][q] * wv[j][q];
     }
 #pragma unroll
-    for (int t = 0; t < TPW; ++t)
+    for (int t = 0; t < TPC; ++t)
 #pragma unroll
       for (int j = 0; j < kExpChunk; ++j) {
-        const A s = warp_sum(acc[t][j]);
-        if (lane == 0 && ec + j < E) s_logit[warp][t][ec + j] = s;
+        const A sum = warp_sum(acc[t][j]);
+        if (lane == 0) s_part[warp][t][j] = sum;
       }
+    __syncthreads();
+    if (threadIdx.x < TPC * kExpChunk) {
+      const int t = threadIdx.x / kExpChunk, j = threadIdx.x % kExpChunk;
+      A sum = A(0);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) sum += s_part[w][t][j];
+      if (ec + j < E) s_logit[t][ec + j] = sum;
+    }
+    __syncthreads();
   }
-  __syncwarp();
 
-  // Selection: lane t owns token tok0 + t.
-  if (lane < TPW) {
-    const int tok = tok0 + lane;
+  // Selection: thread t owns token tok0 + t.
+  if (threadIdx.x < TPC) {
+    const int tok = tok0 + threadIdx.x;
     if (tok < ntok) {
-      const A* lg = s_logit[warp][lane];
+      const A* lg = s_logit[threadIdx.x];
       if (logits_out != nullptr)
         for (int e = 0; e < E; ++e) logits_out[(size_t)tok * E + e] = lg[e];
       A score[kMaxE];  // value the top-k ranks on
-      A m_all = lg[0];
       if (mode == QMOE_ROUTE_SOFTMAX_TOPK) {
+        A m_all = lg[0];
         for (int e = 1; e < E; ++e) m_all = lg[e] > m_all ? lg[e] : m_all;
         A tot = A(0);
         for (int e = 0; e < E; ++e) {
@@ -179,19 +181,18 @@ router_kernel(const T* __restrict__ x, const T* __restrict__ wr, int ntok, int d
   }
 }
 
-template <typename T, int TPW>
+template <typename T, int TPC>
 int launch_router(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids,
                   void* w, void* logits, cudaStream_t s) {
   using A = typename AccOf<T>::type;
-  const int per_cta = kWarps * TPW;
-  dim3 grid((T_ + per_cta - 1) / per_cta);
+  dim3 grid((T_ + TPC - 1) / TPC);
   const bool vec = (d % Vec<T>::N == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(wr) % 16 == 0);
   if (vec)
-    router_kernel<T, TPW, true><<<grid, kWarps * 32, 0, s>>>(
+    router_kernel<T, TPC, true><<<grid, kWarps * 32, 0, s>>>(
         (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits);
   else
-    router_kernel<T, TPW, false><<<grid, kWarps * 32, 0, s>>>(
+    router_kernel<T, TPC, false><<<grid, kWarps * 32, 0, s>>>(
         (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits);
   return check_launch("qmoe_router");
 }
@@ -211,9 +212,9 @@ extern "C" int qmoe_router(const void* x, const void* w_router, int T, int d, in
   if (T == 0) return QMOE_OK;
   QMOE_REQUIRE(x && w_router && ids_out && w_out, "qmoe_router: null pointer");
   cudaStream_t s = as_stream(stream);
-  // Few tokens (decode): one token per warp maximises the CTA count; many tokens: 4 per warp
-  // so every W_router load feeds 4 dot products.
-  const bool small = T < 148 * kWarps * 4;
+  // Few tokens (decode): one token per CTA maximises the CTA count; many tokens: 4 per CTA so
+  // every W_router load feeds 4 dot products.
+  const bool small = T < 148 * 8;
   switch (dtype) {
     case QMOE_BF16:
       return small ? launch_router<__nv_bfloat16, 1>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s)

@@ -1,0 +1,44 @@
+"""Quick per-kernel timing of one Mixtral-shaped MoE layer (dev probe, not the bench)."""
+import sys, torch
+sys.path.insert(0, ".")
+from paper_2503_09304_b200 import kernels as K
+
+d, F, E, k = 4096, 14336, 8, 2
+g = torch.Generator(device="cuda").manual_seed(0)
+wr = (torch.randn((E, d), device="cuda", generator=g) / 64).bfloat16()
+gu = (torch.randn((E, 2 * F, d), device="cuda", generator=g) / 64).bfloat16()
+dn = (torch.randn((E, d, F), device="cuda", generator=g) / 120).bfloat16()
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+def timeit(fn, iters=10):
+    """Device time of fn: captured in a CUDA graph so host launch overhead is excluded."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3): fn()
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        fn()
+    ts = []
+    for _ in range(iters):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); graph.replay(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+    ts.sort(); return ts[len(ts) // 2]
+
+for T in [int(t) for t in sys.argv[1:]] or [32, 256, 1024, 4096, 8192, 16384]:
+    x = torch.randn((T, d), device="cuda", generator=g).bfloat16()
+    ids, w = K.router(x, wr, k)
+    perm, offsets, xp = K.permute(ids, E, x=x)
+    y = torch.empty((T * k, d), dtype=torch.bfloat16, device="cuda")
+    act = torch.empty((T * k, F), dtype=torch.bfloat16, device="cuda")
+    t_r = timeit(lambda: K.router(x, wr, k))
+    t_p = timeit(lambda: K.permute(ids, E, x=x))
+    t_f = timeit(lambda: K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act))
+    t_c = timeit(lambda: K.combine(y, w, x))
+    flops = 6.0 * T * k * d * F
+    hit = int((offsets[1:] > offsets[:-1]).sum())
+    wbytes = hit * 3 * d * F * 2
+    print(f"T={T:6d} router {t_r*1e3:8.1f}us permute {t_p*1e3:8.1f}us ffn {t_f*1e3:9.1f}us "
+          f"({flops/t_f/1e9:7.1f} TFLOP/s, weights {wbytes/t_f/1e6:7.1f} GB/s) combine {t_c*1e3:7.1f}us", flush=True)
