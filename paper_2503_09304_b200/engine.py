@@ -1,0 +1,330 @@
+"""Inference engine: drives a batch through ATTENTION -> ROUTER -> EXPERTS per layer, reports
+to the scheduler after attention, after the router and after each non-empty expert, honours
+PREEMPT_AT_NEXT_BOUNDARY at those boundaries, and checkpoints/restores batch state on the device.
+
+Same public surface as the reference engine (reference engine.py:31-226): VirtualClock,
+CostModel, Completed, Preempted, InferenceEngine.execute / restore / next_batch_id,
+max_stage_cost.  What changes is where state lives and how the expert stage runs:
+
+* Batch state (expert input, residual, routing ids/weights, expert outputs in slot order, and a
+  per-token expert cursor) is a handful of device tensors.  A checkpoint is a set of row views
+  of them — preemption copies nothing (reference engine.py:401-423 copies every array).
+* The expert stage is: one permute launch (stable expert-major queue order over the pending
+  slots), one 4*(E+1)-byte D2H of the queue offsets, the report loop on the host (the virtual
+  timestamps of all expert boundaries follow from the queue lengths: engine.py:215), and ONE
+  grouped expert launch for experts [0, stop) where stop is the boundary the scheduler chose.
+  On preemption the per-token cursors advance to `stop` on the device.
+* Restore rebuilds a merged resume batch in the new member order by concatenating checkpoint
+  rows (zero-copy when the resumed members are one contiguous run of a single preempted batch).
+
+Device plugin interface (model.py implements it; tests may substitute a replay double):
+  config.{num_layers, hidden_dim, num_experts, top_k}
+  embed_batch(tokens) -> h[T,d]
+  attention_batch(layer, h, members, cache) -> (x, residual)
+  route_batch(layer, x) -> (ids[T,k], w[T,k])
+  new_expert_state(T) -> (y[T*k,d], cursor[T])
+  permute(ids, cursor, x) -> (perm, offsets, xp, counts: list[int])
+  run_experts(layer, xp, offsets, perm, y, e_begin, e_end) -> stop (device int32[1])
+  advance_cursor(cursor, stop)
+  combine_batch(layer, y, w, residual, x) -> h_next[T,d]
+  emit_batch(h, rows) -> list[int]
+  cat_rows(list of tensors) -> tensor
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Union
+
+from .core import (Batch, Checkpoint, EngineReport, MemberProgress, Phase, SchedulerDirective, Sequence,
+                   SimulationError, Stage, StateCorruptionError, batch_form)
+from .model import MemberRows
+
+PREEMPT = SchedulerDirective.PREEMPT_AT_NEXT_BOUNDARY
+
+
+class VirtualClock:
+    """Monotone virtual milliseconds (reference engine.py:31-45)."""
+
+    virtual = True
+
+    def __init__(self, start: float = 0.0):
+        self.now = float(start)
+
+    def advance(self, delta_ms: float) -> None:
+        if delta_ms < 0:
+            raise SimulationError(f"clock cannot move backwards (delta {delta_ms})")
+        self.now += delta_ms
+
+    def advance_to(self, timestamp: float) -> None:
+        if timestamp < self.now:
+            raise SimulationError(f"clock cannot jump back to {timestamp} from {self.now}")
+        self.now = timestamp
+
+
+class WallClock:
+    """Real milliseconds since construction.  Charges are ignored (time passes by itself);
+    advance_to sleeps until the target so idle periods last as long as in a real server."""
+
+    virtual = False
+
+    def __init__(self):
+        self._t0 = time.perf_counter()
+
+    @property
+    def now(self) -> float:
+        return (time.perf_counter() - self._t0) * 1000.0
+
+    def advance(self, delta_ms: float) -> None:
+        if delta_ms < 0:
+            raise SimulationError(f"clock cannot move backwards (delta {delta_ms})")
+
+    def advance_to(self, timestamp: float) -> None:
+        wait = timestamp - self.now
+        if wait > 0:
+            time.sleep(wait / 1000.0)
+
+
+@dataclass(frozen=True)
+class CostModel:
+    """Linear virtual-time charges per stage in ms (reference engine.py:48-88)."""
+
+    attn_base: float = 1.2
+    attn_per_token: float = 0.001
+    attn_per_cached: float = 0.0003
+    router_cost: float = 0.8
+    expert_base: float = 0.85
+    expert_per_entry: float = 0.0005
+    checkpoint_cost: float = 2.0
+    restore_cost: float = 2.0
+
+    def validate(self) -> None:
+        for name, value in self.__dict__.items():
+            if value < 0:
+                raise ValueError(f"cost parameter {name} must be >= 0, got {value}")
+
+    def attention_cost(self, tokens: int, cached_entries: int) -> float:
+        return self.attn_base + self.attn_per_token * tokens + self.attn_per_cached * cached_entries
+
+    def expert_cost(self, entries: int) -> float:
+        return self.expert_base + self.expert_per_entry * entries
+
+    def stage_cost(self, stage: Stage, *, tokens: int = 0, cached_entries: int = 0, expert_entries: int = 0) -> float:
+        if stage is Stage.ATTENTION:
+            return self.attention_cost(tokens, cached_entries)
+        if stage is Stage.ROUTER:
+            return self.router_cost
+        if stage is Stage.EXPERTS:
+            return 0.0 if expert_entries == 0 else self.expert_cost(expert_entries)
+        return 0.0
+
+    def scaled(self, factor: float) -> "CostModel":
+        return CostModel(**{k: v * factor for k, v in self.__dict__.items()})
+
+
+@dataclass
+class Completed:
+    tokens: dict[int, int]
+
+
+@dataclass
+class Preempted:
+    checkpoints: dict[int, Checkpoint]
+
+
+IterationOutcome = Union[Completed, Preempted]
+ReportCallback = Callable[[EngineReport], SchedulerDirective]
+
+
+@dataclass
+class _State:
+    """Device state of one in-flight batch; rows are member-major, token order within a member."""
+
+    seqs: list[Sequence]
+    members: list[MemberRows]
+    T: int
+    h: object = None         # hidden entering the attention stage
+    x: object = None         # expert input (attention-stage output)
+    res: object = None       # residual for the combine
+    ids: object = None
+    w: object = None
+    y: object = None
+    cursor: object = None
+
+
+class InferenceEngine:
+    """Single-host-thread engine; all tensor work is enqueued on the current CUDA stream."""
+
+    def __init__(self, model, cache, clock, cost_model: CostModel = CostModel(), max_batch_size: int = 32,
+                 log: Optional[list] = None):
+        cost_model.validate()
+        self.model = model
+        self.cache = cache
+        self.clock = clock
+        self.cost = cost_model
+        self.max_batch_size = max_batch_size
+        self.max_stage_cost = 0.0
+        self.log = log  # decision log: per-expert queue contents ("Q" events) when not None
+        self._batch_counter = 0
+        self.stats = {"iterations": 0, "preemptions": 0, "expert_launches": 0, "zero_copy_restores": 0,
+                      "copy_restores": 0}
+
+    def next_batch_id(self) -> int:
+        self._batch_counter += 1
+        return self._batch_counter
+
+    def restore(self, sequences: list[Sequence]) -> Batch:
+        """Rebuild a batch from checkpoints at one position; charges restore_cost per member."""
+        if not sequences:
+            raise ValueError("nothing to restore")
+        positions = set()
+        for seq in sequences:
+            if seq.checkpoint is None:
+                raise ValueError(f"sequence {seq.id} has no checkpoint to restore")
+            positions.add(seq.checkpoint.position)
+        if len(positions) != 1:
+            raise ValueError(f"checkpoints at mixed positions {sorted(positions)}; group them first")
+        batch = batch_form(sequences, sequences[0].phase, self.max_batch_size, self.next_batch_id())
+        self.clock.advance(self.cost.restore_cost * len(sequences))
+        return batch
+
+    # ------------------------------------------------------------------------------------------
+    def execute(self, batch: Batch, sequences: list[Sequence], on_report: ReportCallback) -> IterationOutcome:
+        if [s.id for s in sequences] != batch.members:
+            raise SimulationError("sequence list does not match batch members")
+        st = self._init_state(sequences)
+        m = self.model
+        L, E = m.config.num_layers, m.config.num_experts
+        layer, stage = batch.layer_cursor, batch.stage_cursor
+        if stage not in (Stage.ATTENTION, Stage.ROUTER, Stage.EXPERTS):
+            raise SimulationError(f"batch cursor at non-executable stage {stage}")
+        self.stats["iterations"] += 1
+
+        while layer < L:
+            if stage is Stage.ATTENTION:
+                st.x, st.res = m.attention_batch(layer, st.h, st.members, self.cache)
+                st.h = None
+                scanned = sum(self.cache.count(s.cache_handle, layer) for s in st.seqs)
+                self._charge(self.cost.attention_cost(st.T, scanned))
+                if on_report(self._report(batch, Stage.ATTENTION, layer, st)) is PREEMPT:
+                    return self._preempt(st, layer, Stage.ROUTER)
+                stage = Stage.ROUTER
+
+            if stage is Stage.ROUTER:
+                st.ids, st.w = m.route_batch(layer, st.x)
+                st.y, st.cursor = m.new_expert_state(st.T)
+                self._charge(self.cost.router_cost)
+                if on_report(self._report(batch, Stage.ROUTER, layer, st)) is PREEMPT:
+                    return self._preempt(st, layer, Stage.EXPERTS)
+                stage = Stage.EXPERTS
+
+            # EXPERTS: queue build for the pending slots, boundary decisions, one grouped launch.
+            perm, offsets, xp, counts = m.permute(st.ids, st.cursor, st.x)
+            slots = None
+            if self.log is not None and sum(counts):
+                slots = perm[: sum(counts)].tolist()
+            stop, preempted, start = E, False, 0
+            for e in range(E):
+                n = counts[e]
+                if n == 0:
+                    continue
+                if slots is not None:
+                    self._log_queue(st, layer, e, slots[start:start + n])
+                start += n
+                self._charge(self.cost.expert_cost(n))
+                if on_report(self._report(batch, Stage.EXPERTS, layer, st, expert_id=e)) is PREEMPT:
+                    stop, preempted = e + 1, True
+                    break
+            stop_dev = None
+            if sum(counts):
+                stop_dev = m.run_experts(layer, xp, offsets, perm, st.y, 0, stop)
+                self.stats["expert_launches"] += 1
+            if preempted:
+                m.advance_cursor(st.cursor, stop_dev)
+                return self._preempt(st, layer, Stage.EXPERTS)
+            st.h = m.combine_batch(layer, st.y, st.w, st.res, st.x)
+            st.x = st.res = st.ids = st.w = st.y = st.cursor = None
+            layer += 1
+            stage = Stage.ATTENTION
+
+        rows = [mr.row0 + mr.n - 1 for mr in st.members]
+        tokens = m.emit_batch(st.h, rows)
+        return Completed({s.id: int(t) for s, t in zip(st.seqs, tokens)})
+
+    # ------------------------------------------------------------------------------------------
+    def _init_state(self, sequences: list[Sequence]) -> _State:
+        members, row = [], 0
+        inputs = []
+        for seq in sequences:
+            if seq.cache_handle is None or not self.cache.has_handle(seq.cache_handle):
+                raise StateCorruptionError(f"sequence {seq.id} has no registered cache handle")
+            toks = seq.iteration_input()
+            if seq.checkpoint is not None and seq.checkpoint.num_tokens != len(toks):
+                raise StateCorruptionError(f"sequence {seq.id}: checkpoint does not match iteration input")
+            inputs.append(toks)
+            members.append(MemberRows(seq, row, len(toks)))
+            row += len(toks)
+        st = _State(list(sequences), members, row)
+        ckpts = [s.checkpoint for s in sequences]
+        if ckpts[0] is None:
+            st.h = self.model.embed_batch([t for toks in inputs for t in toks])
+            return st
+        st.x, st.res = self._gather(ckpts, "hidden"), self._gather(ckpts, "residual")
+        if ckpts[0].ids is not None:
+            st.ids, st.w = self._gather(ckpts, "ids"), self._gather(ckpts, "weights")
+            st.y, st.cursor = self._gather(ckpts, "y"), self._gather(ckpts, "cursor")
+        self.stats["zero_copy_restores" if self._contiguous(ckpts) else "copy_restores"] += 1
+        for s in sequences:
+            s.checkpoint = None  # checkpoints live only while preempted
+        return st
+
+    @staticmethod
+    def _contiguous(ckpts: list[Checkpoint]) -> bool:
+        o = [getattr(c, "origin", None) for c in ckpts]
+        if any(x is None for x in o) or any(x[0] is not o[0][0] for x in o):
+            return False
+        return all(o[i][2] == o[i + 1][1] for i in range(len(o) - 1))
+
+    def _gather(self, ckpts: list[Checkpoint], name: str):
+        if self._contiguous(ckpts):
+            st, r0, r1 = ckpts[0].origin[0], ckpts[0].origin[1], ckpts[-1].origin[2]
+            k = self.model.config.top_k
+            full = getattr(st, {"hidden": "x", "residual": "res", "weights": "w"}.get(name, name))
+            return full[r0 * k:r1 * k] if name == "y" else full[r0:r1]
+        return self.model.cat_rows([getattr(c, name) for c in ckpts])
+
+    def _charge(self, cost_ms: float) -> None:
+        self.clock.advance(cost_ms)
+        if cost_ms > self.max_stage_cost:
+            self.max_stage_cost = cost_ms
+
+    def _report(self, batch: Batch, stage: Stage, layer: int, st: _State,
+                expert_id: Optional[int] = None) -> EngineReport:
+        progress = tuple(MemberProgress(s.id, s.priority, s.phase, len(s.generated)) for s in st.seqs)
+        return EngineReport(batch.batch_id, stage, layer, self.clock.now, progress, expert_id)
+
+    def _log_queue(self, st: _State, layer: int, expert: int, slots: list[int]) -> None:
+        k = self.model.config.top_k
+        owner = []
+        for mr in st.members:
+            owner += [(mr.seq.id, t) for t in range(mr.n)]
+        self.log.append(["Q", layer, expert, [list(owner[s // k]) for s in slots]])
+
+    def _preempt(self, st: _State, layer: int, resume_stage: Stage) -> Preempted:
+        k = self.model.config.top_k
+        routed = resume_stage > Stage.ROUTER
+        out: dict[int, Checkpoint] = {}
+        for mr in st.members:
+            r = slice(mr.row0, mr.row0 + mr.n)
+            ck = Checkpoint(layer_index=layer, stage=resume_stage, hidden=st.x[r], residual=st.res[r],
+                            ids=st.ids[r] if routed else None, weights=st.w[r] if routed else None,
+                            y=st.y[mr.row0 * k:(mr.row0 + mr.n) * k] if routed else None,
+                            cursor=st.cursor[r] if routed else None)
+            ck.origin = (st, mr.row0, mr.row0 + mr.n)
+            ck.validate()
+            mr.seq.checkpoint = ck
+            out[mr.seq.id] = ck
+        self.stats["preemptions"] += 1
+        self._charge(self.cost.checkpoint_cost)
+        return Preempted(out)

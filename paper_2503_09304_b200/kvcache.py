@@ -1,0 +1,145 @@
+"""Unified Dynamic Cache on the device: paged KV storage owned by sequences, never by batches.
+
+Mirrors the reference UnifiedDynamicCache API (reference model.py:266-337: register, has_handle,
+can_admit, append/append_many, entries, count, evict_sequence, usage_bytes, recount_bytes) but
+stores entries in fixed-size device pages:
+
+  pool[l]  [n_pages, page_size, *row_shape]   one pool per layer (same page ids in every layer)
+  pages[h] host list of page ids of sequence h; token position p lives at
+           slot = pages[h][p // page_size] * page_size + p % page_size in every layer's pool
+
+Appends are one qmoe_kv_append launch (row scatter by slot mapping); reads are a qmoe_kv_gather
+(toy attention) or the page table handed to a paged attention kernel.  Changing batch
+composition moves nothing.  The byte ledger is kept in the caller's units: the reference's
+``2 * d * 8`` per entry for parity runs (model.py:277), real KV bytes for production models.
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Sequence as Seq
+
+import torch
+
+from . import kernels as K
+from .core import CacheCapacityError, SimulationError, StateCorruptionError
+
+
+class UnifiedDynamicCache:
+    def __init__(self, num_layers: int, row_shape: Seq[int], dtype: torch.dtype, device: torch.device,
+                 entry_bytes: int, capacity_bytes: float = 8 * 1024**3, page_size: int = 16,
+                 initial_pages: int = 256, max_pages: Optional[int] = None):
+        self.num_layers = num_layers
+        self.row_shape = tuple(row_shape)
+        self.dtype = dtype
+        self.device = device
+        self.entry_bytes = int(entry_bytes)
+        self.capacity_bytes = capacity_bytes
+        self.page_size = page_size
+        self.max_pages = max_pages
+        self._pools: list[torch.Tensor] = []
+        self._n_pages = 0
+        self._free: list[int] = []
+        self._grow(initial_pages)
+        self._pages: dict[int, list[int]] = {}
+        self._counts: dict[int, list[int]] = {}
+        self._ledger = 0
+
+    # -- physical pages ------------------------------------------------------------------------
+    def _grow(self, n_pages: int) -> None:
+        if self.max_pages is not None and n_pages > self.max_pages:
+            raise CacheCapacityError(f"paged KV pool cannot grow to {n_pages} pages (max {self.max_pages})")
+        shape = (n_pages, self.page_size) + self.row_shape
+        new = [torch.zeros(shape, dtype=self.dtype, device=self.device) for _ in range(self.num_layers)]
+        for l, old in enumerate(self._pools):
+            new[l][: old.shape[0]].copy_(old)
+        self._free.extend(range(n_pages - 1, self._n_pages - 1, -1))
+        self._pools = new
+        self._n_pages = n_pages
+
+    def pool(self, layer: int) -> torch.Tensor:
+        return self._pools[layer]
+
+    def _ensure_pages(self, handle: int, upto: int) -> None:
+        pages = self._pages[handle]
+        need = -(-upto // self.page_size)
+        while len(pages) < need:
+            if not self._free:
+                self._grow(self._n_pages * 2)
+            pages.append(self._free.pop())
+
+    def slots(self, handle: int, start: int, n: int) -> list[int]:
+        pages, ps = self._pages[handle], self.page_size
+        return [pages[p // ps] * ps + p % ps for p in range(start, start + n)]
+
+    def page_table(self, handle: int) -> list[int]:
+        return list(self._pages[handle])
+
+    # -- reference API -----------------------------------------------------------------------------
+    def register(self, handle: int) -> None:
+        if handle in self._pages:
+            raise SimulationError(f"cache handle {handle} already registered")
+        self._pages[handle] = []
+        self._counts[handle] = [0] * self.num_layers
+
+    def has_handle(self, handle: int) -> bool:
+        return handle in self._pages
+
+    def can_admit(self, new_entries: int) -> bool:
+        return self._ledger + new_entries * self.entry_bytes <= self.capacity_bytes
+
+    def reserve(self, handle: int, layer: int, n: int) -> list[int]:
+        """Account n new entries of one sequence at one layer and return their slots."""
+        if handle not in self._pages:
+            raise StateCorruptionError(f"unknown cache handle {handle}")
+        if not self.can_admit(n):
+            raise CacheCapacityError(
+                f"cache capacity {self.capacity_bytes} bytes exceeded at {self._ledger} used")
+        start = self._counts[handle][layer]
+        self._ensure_pages(handle, start + n)
+        self._counts[handle][layer] = start + n
+        self._ledger += n * self.entry_bytes
+        return self.slots(handle, start, n)
+
+    def append_many(self, handle: int, layer: int, rows: torch.Tensor) -> None:
+        slots = self.reserve(handle, layer, rows.shape[0])
+        K.kv_append(self._pools[layer], torch.tensor(slots, dtype=torch.int32, device=self.device),
+                    rows.contiguous())
+
+    def append(self, handle: int, layer: int, row: torch.Tensor) -> None:
+        self.append_many(handle, layer, row.unsqueeze(0))
+
+    def scatter(self, layer: int, slots: list[int], rows: torch.Tensor) -> None:
+        """One launch for the new rows of many sequences (slots from ``reserve``)."""
+        if slots:
+            K.kv_append(self._pools[layer], torch.tensor(slots, dtype=torch.int32, device=self.device),
+                        rows.contiguous())
+
+    def entries(self, handle: int, layer: int) -> torch.Tensor:
+        """All entries of one sequence at one layer, ascending entry order, gathered to [n, *row]."""
+        n = self._counts[handle][layer]
+        if n == 0:
+            raise StateCorruptionError(f"no cache entries for handle {handle} layer {layer}")
+        out = torch.empty((n,) + self.row_shape, dtype=self.dtype, device=self.device)
+        return K.kv_gather(self._pools[layer], torch.tensor(self.slots(handle, 0, n), dtype=torch.int32,
+                                                            device=self.device), out)
+
+    def count(self, handle: int, layer: int) -> int:
+        return self._counts[handle][layer]
+
+    def evict_sequence(self, handle: int) -> None:
+        pages = self._pages.pop(handle, None)
+        if pages is None:
+            return
+        counts = self._counts.pop(handle)
+        self._ledger -= sum(counts) * self.entry_bytes
+        self._free.extend(reversed(pages))
+
+    def usage_bytes(self) -> int:
+        return self._ledger
+
+    def recount_bytes(self) -> int:
+        """Brute-force recount from the per-sequence counts (ledger test oracle)."""
+        return sum(sum(c) for c in self._counts.values()) * self.entry_bytes
+
+    def pages_in_use(self) -> int:
+        return sum(len(p) for p in self._pages.values())
