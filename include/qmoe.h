@@ -141,6 +141,11 @@ QMOE_API int qmoe_combine(int dtype, const void* y, const void* w, const void* r
 QMOE_API int qmoe_gather_rows(const void* src, const int32_t* idx, int rows, size_t row_bytes, void* dst,
                      void* stream);
 
+/* Row scatter: dst[idx[i]] = src[i] for i < rows (expert-parallel return path: outputs received
+ * in expert-major order go back to their token slots). */
+QMOE_API int qmoe_scatter_rows(const void* src, const int32_t* idx, int rows, size_t row_bytes, void* dst,
+                               void* stream);
+
 /*
  * Cursor advance after a (possibly partial) expert launch: for every token, the next pending
  * expert becomes max(cursor[t], stop_expert) (pending = routed ∩ {e >= cursor}).  stop_expert is

@@ -193,6 +193,11 @@ extern "C" int qmoe_gather_rows(const void* src, const int32_t* idx, int rows, s
   return qmoe::launch_rows(src, idx, rows, row_bytes, dst, 0, qmoe::as_stream(stream), "qmoe_gather_rows");
 }
 
+extern "C" int qmoe_scatter_rows(const void* src, const int32_t* idx, int rows, size_t row_bytes, void* dst,
+                                 void* stream) {
+  return qmoe::launch_rows(src, idx, rows, row_bytes, dst, 1, qmoe::as_stream(stream), "qmoe_scatter_rows");
+}
+
 extern "C" int qmoe_cursor_advance(int32_t* cursor, int T, const int32_t* stop_expert_dev, void* stream) {
   using namespace qmoe;
   QMOE_REQUIRE(T >= 0, "qmoe_cursor_advance: bad T");

@@ -1,0 +1,141 @@
+"""Expert parallelism across the GPUs of one node: experts sharded in contiguous blocks, tokens
+data-parallel, NCCL all-to-all-v dispatch and combine per MoE layer.
+
+Per layer on every rank (T local tokens):
+  1. router + permute on the local tokens over ALL E experts (libqmoe).  The permute's
+     expert-major order makes the rows bound for rank g one contiguous block of Xp.
+  2. one all_gather of the E per-expert queue lengths (the same counts the virtual-clock
+     boundary decisions need, so every rank can replicate the scheduler's decisions).
+  3. dispatch all-to-all-v of Xp rows (bf16, d each).
+  4. a local regroup gather (qmoe_gather_rows) puts received rows in local-expert-major order;
+     the grouped tcgen05 expert FFN runs on the local experts and, through its perm argument,
+     writes each output straight back to its received position.
+  5. combine all-to-all-v returns the rows; qmoe_scatter_rows puts them in token-slot order;
+     qmoe_combine does the weighted sum (+ residual).
+Expert ids, queue order and therefore outputs are identical to the single-GPU path (the local
+expert FFN sees exactly the same rows in the same order per expert).
+
+``ops`` is the kernel module (paper_2503_09304_b200.kernels); tests substitute a CPU double to
+exercise the exchange logic under gloo.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from . import kernels as K
+
+
+def expert_bounds(num_experts: int, world: int) -> list[int]:
+    """Contiguous expert blocks; uneven counts (60 over 8) get sizes differing by at most one."""
+    return [(num_experts * g) // world for g in range(world + 1)]
+
+
+def regroup_index(counts: list[list[int]], e_lo: int, e_hi: int) -> tuple[list[int], list[int]]:
+    """Rows arrive ordered (source rank, local expert); return (index into the received buffer
+    for local-expert-major order, local offsets [E_local + 1]).  counts[src][e] = rows of expert
+    e that rank src sends."""
+    world = len(counts)
+    base, acc = [], 0
+    for src in range(world):  # start of (src, e) block in the received buffer
+        row = {}
+        for e in range(e_lo, e_hi):
+            row[e] = acc
+            acc += counts[src][e]
+        base.append(row)
+    idx, offsets = [], [0]
+    for e in range(e_lo, e_hi):
+        for src in range(world):
+            b = base[src][e]
+            idx.extend(range(b, b + counts[src][e]))
+        offsets.append(len(idx))
+    return idx, offsets
+
+
+class ExpertParallelMoE(torch.nn.Module):
+    """Mixtral-style sparse MoE block with experts sharded over the process group."""
+
+    def __init__(self, hidden_size: int, intermediate_size: int, num_experts: int, top_k: int, rank: int,
+                 world: int, device: Optional[torch.device] = None, dtype: torch.dtype = torch.bfloat16,
+                 group=None, ops=K, route_mode: int = K.ROUTE_TOPK_SOFTMAX):
+        super().__init__()
+        self.d, self.F, self.E, self.k = hidden_size, intermediate_size, num_experts, top_k
+        self.rank, self.world, self.group, self.ops = rank, world, group, ops
+        self.route_mode = route_mode
+        self.device = device or torch.device("cuda")
+        self.dtype = dtype
+        b = expert_bounds(num_experts, world)
+        self.bounds = b
+        self.e_lo, self.e_hi = b[rank], b[rank + 1]
+        El = self.e_hi - self.e_lo
+        self.w_router = torch.empty((num_experts, hidden_size), dtype=dtype, device=self.device)
+        self.gate_up = torch.empty((El, 2 * intermediate_size, hidden_size), dtype=dtype, device=self.device)
+        self.down = torch.empty((El, hidden_size, intermediate_size), dtype=dtype, device=self.device)
+
+    @torch.no_grad()
+    def init_random(self, seed: int = 0) -> "ExpertParallelMoE":
+        """Same draws as SparseMoeBlock.init_random for the full layer, sliced to the local experts,
+        so an EP run and a single-GPU run share weights."""
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        d, F, E = self.d, self.F, self.E
+        wr = torch.randn((E, d), generator=g, device=self.device, dtype=torch.float32) * d ** -0.5
+        self.w_router.copy_(wr)
+        gu = torch.randn((E, 2 * F, d), generator=g, device=self.device, dtype=torch.float32).mul_(d ** -0.5)
+        self.gate_up.copy_(gu[self.e_lo:self.e_hi])
+        del gu
+        dn = torch.randn((E, d, F), generator=g, device=self.device, dtype=torch.float32).mul_(F ** -0.5)
+        self.down.copy_(dn[self.e_lo:self.e_hi])
+        del dn
+        return self
+
+    @torch.no_grad()
+    def load_full(self, w_router, gate_up, down) -> "ExpertParallelMoE":
+        self.w_router.copy_(w_router)
+        self.gate_up.copy_(gate_up[self.e_lo:self.e_hi])
+        self.down.copy_(down[self.e_lo:self.e_hi])
+        return self
+
+    def exchange_counts(self, counts: list[int]) -> list[list[int]]:
+        t = torch.tensor(counts, dtype=torch.int64, device=self._comm_device())
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return [o.tolist() for o in out]
+
+    def _comm_device(self):
+        return self.device
+
+    @torch.no_grad()
+    def forward(self, hidden_states: torch.Tensor, residual: Optional[torch.Tensor] = None) -> torch.Tensor:
+        ops, E, k, d = self.ops, self.E, self.k, self.d
+        shape = hidden_states.shape
+        x = hidden_states.reshape(-1, d).contiguous()
+        T = x.shape[0]
+        ids, w = ops.router(x, self.w_router, k, self.route_mode)
+        perm, offsets, xp = ops.permute(ids, E, x=x)
+        off = offsets.tolist()
+        counts = [off[e + 1] - off[e] for e in range(E)]
+        allc = self.exchange_counts(counts)
+        b = self.bounds
+        send = [off[b[g + 1]] - off[b[g]] for g in range(self.world)]
+        recv = [sum(allc[src][self.e_lo:self.e_hi]) for src in range(self.world)]
+        R = off[E]
+        x_in = torch.empty((sum(recv), d), dtype=x.dtype, device=x.device)
+        dist.all_to_all_single(x_in, xp[:R], output_split_sizes=recv, input_split_sizes=send, group=self.group)
+        idx, loc_off = regroup_index(allc, self.e_lo, self.e_hi)
+        y_in = torch.empty_like(x_in)
+        if idx:
+            gidx = torch.tensor(idx, dtype=torch.int32, device=x.device)
+            xg = ops.gather_rows(x_in, gidx)
+            loc = torch.tensor(loc_off, dtype=torch.int32, device=x.device)
+            act = torch.empty((len(idx), self.F), dtype=x.dtype, device=x.device)
+            ops.expert_ffn(K.EXPERT_SWIGLU, xg, loc, gidx, self.gate_up, self.down, y_in, act_ws=act)
+        y_back = torch.empty((R, d), dtype=x.dtype, device=x.device)
+        dist.all_to_all_single(y_back, y_in, output_split_sizes=send, input_split_sizes=recv, group=self.group)
+        y = torch.empty((T * k, d), dtype=x.dtype, device=x.device)
+        if R:
+            ops.scatter_rows(y_back, perm[:R].contiguous(), y)
+        res = None if residual is None else residual.reshape(-1, d).contiguous()
+        return ops.combine(y, w, res).reshape(shape)

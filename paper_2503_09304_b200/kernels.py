@@ -185,6 +185,26 @@ def gather_rows(src: torch.Tensor, idx: torch.Tensor, out: Optional[torch.Tensor
     return out
 
 
+def scatter_rows(src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """out[idx[i]] = src[i]."""
+    _need(src, "src")
+    _need(out, "out", src.dtype)
+    _need(idx, "idx", torch.int32)
+    rows = idx.shape[0]
+    row_bytes = out[0].numel() * out.element_size() if out.shape[0] else 1
+    lib = _lib.load()
+    check(lib.qmoe_scatter_rows(_ptr(src), _ptr(idx), rows, row_bytes, _ptr(out), _stream()), "qmoe_scatter_rows")
+    return out
+
+
+def permute_launches(T: int, k: int, gather: bool = True) -> int:
+    """Kernel launches qmoe_permute issues (mirrors csrc/permute.cu: chunk 2048 slots; a count
+    pass only with >1 chunk; the wide gather only when more than 32 slots)."""
+    S = T * k
+    nblk = -(-S // 2048)
+    return (1 if nblk > 1 else 0) + 1 + (1 if gather and S > 32 else 0)
+
+
 def cursor_advance(cursor: torch.Tensor, stop_dev: torch.Tensor) -> None:
     _need(cursor, "cursor", torch.int32)
     _need(stop_dev, "stop", torch.int32)
