@@ -151,6 +151,7 @@ class _State:
     w: object = None
     y: object = None
     cursor: object = None
+    progress: tuple = ()     # MemberProgress of every member (constant within one execute)
 
 
 class InferenceEngine:
@@ -266,6 +267,7 @@ class InferenceEngine:
             members.append(MemberRows(seq, row, len(toks)))
             row += len(toks)
         st = _State(list(sequences), members, row)
+        st.progress = tuple(MemberProgress(s.id, s.priority, s.phase, len(s.generated)) for s in sequences)
         ckpts = [s.checkpoint for s in sequences]
         if ckpts[0] is None:
             st.h = self.model.embed_batch([t for toks in inputs for t in toks])
@@ -301,8 +303,7 @@ class InferenceEngine:
 
     def _report(self, batch: Batch, stage: Stage, layer: int, st: _State,
                 expert_id: Optional[int] = None) -> EngineReport:
-        progress = tuple(MemberProgress(s.id, s.priority, s.phase, len(s.generated)) for s in st.seqs)
-        return EngineReport(batch.batch_id, stage, layer, self.clock.now, progress, expert_id)
+        return EngineReport(batch.batch_id, stage, layer, self.clock.now, st.progress, expert_id)
 
     def _log_queue(self, st: _State, layer: int, expert: int, slots: list[int]) -> None:
         k = self.model.config.top_k

@@ -87,8 +87,9 @@ class UnifiedDynamicCache:
     def can_admit(self, new_entries: int) -> bool:
         return self._ledger + new_entries * self.entry_bytes <= self.capacity_bytes
 
-    def reserve(self, handle: int, layer: int, n: int) -> list[int]:
-        """Account n new entries of one sequence at one layer and return their slots."""
+    def reserve(self, handle: int, layer: int, n: int, want_slots: bool = True) -> list[int]:
+        """Account n new entries of one sequence at one layer and return their slots (the same
+        slots in every layer, so callers may skip recomputing them with want_slots=False)."""
         if handle not in self._pages:
             raise StateCorruptionError(f"unknown cache handle {handle}")
         if not self.can_admit(n):
@@ -98,7 +99,7 @@ class UnifiedDynamicCache:
         self._ensure_pages(handle, start + n)
         self._counts[handle][layer] = start + n
         self._ledger += n * self.entry_bytes
-        return self.slots(handle, start, n)
+        return self.slots(handle, start, n) if want_slots else []
 
     def append_many(self, handle: int, layer: int, rows: torch.Tensor) -> None:
         slots = self.reserve(handle, layer, rows.shape[0])
@@ -108,11 +109,13 @@ class UnifiedDynamicCache:
     def append(self, handle: int, layer: int, row: torch.Tensor) -> None:
         self.append_many(handle, layer, row.unsqueeze(0))
 
-    def scatter(self, layer: int, slots: list[int], rows: torch.Tensor) -> None:
-        """One launch for the new rows of many sequences (slots from ``reserve``)."""
-        if slots:
-            K.kv_append(self._pools[layer], torch.tensor(slots, dtype=torch.int32, device=self.device),
-                        rows.contiguous())
+    def scatter(self, layer: int, slots, rows: torch.Tensor) -> None:
+        """One launch for the new rows of many sequences (slots from ``reserve``: a list or an
+        int32 device tensor)."""
+        if len(slots):
+            if not isinstance(slots, torch.Tensor):
+                slots = torch.tensor(slots, dtype=torch.int32, device=self.device)
+            K.kv_append(self._pools[layer], slots, rows.contiguous())
 
     def entries(self, handle: int, layer: int) -> torch.Tensor:
         """All entries of one sequence at one layer, ascending entry order, gathered to [n, *row]."""

@@ -1,0 +1,226 @@
+"""Mixtral-8x7B- and Qwen1.5-MoE-A2.7B-shaped decoder plugins for the serving engine.
+
+Random-init bf16 weights of the real architectures (no checkpoints exist offline): RMSNorm,
+GQA attention with RoPE over the device paged KV cache, a sparse MoE block per layer, final
+norm + LM head with greedy (lowest-id-on-tie) emission.  The MoE block is the hot path and runs
+entirely on libqmoe (router, permute, tcgen05 grouped SwiGLU experts, combine with the residual
+fused); attention is outside the north-star path and uses flash-attn's paged kernels (library
+code, like cuBLAS) on the engine-owned page pool.
+
+Layer semantics = HF MixtralDecoderLayer / Qwen2MoeDecoderLayer:
+  h2 = h + o_proj(attn(rope(q), rope(k), v))          (ATTENTION stage: returns x=norm2(h2), res=h2)
+  h' = h2 + sum_j w_j * expert_j(x)  [+ sigmoid(g.x) * shared(x) for Qwen]   (ROUTER + EXPERTS)
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import kernels as K
+from .core import Phase, StateCorruptionError
+
+
+@dataclass(frozen=True)
+class DecoderConfig:
+    name: str
+    num_layers: int
+    hidden_dim: int
+    ffn_dim: int
+    num_experts: int
+    top_k: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    vocab_size: int
+    rope_theta: float
+    rms_eps: float
+    route_mode: int = K.ROUTE_TOPK_SOFTMAX
+    shared_ffn_dim: int = 0
+    max_position: int = 4096
+
+
+MIXTRAL_8X7B = DecoderConfig("mixtral-8x7b", 32, 4096, 14336, 8, 2, 32, 8, 128, 32000, 1e6, 1e-5)
+QWEN15_MOE_A27B = DecoderConfig("qwen1.5-moe-a2.7b", 24, 2048, 1408, 60, 4, 16, 16, 128, 151936, 1e6, 1e-6,
+                                route_mode=K.ROUTE_SOFTMAX_TOPK, shared_ffn_dim=5632)
+
+
+def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    xf = x.float()
+    return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)).to(x.dtype) * w
+
+
+class _Layer:
+    pass
+
+
+class DecoderMoEModel:
+    """Device plugin (engine.py interface) for a Mixtral/Qwen-shaped decoder."""
+
+    # flash-attn paged KV needs blocks of 256 tokens; 384 pages/layer hold 32 x 3072 tokens
+    kv_page_kwargs = {"page_size": 256, "initial_pages": 384}
+
+    def __init__(self, cfg: DecoderConfig, device: Optional[torch.device] = None, seed: int = 0,
+                 dtype: torch.dtype = torch.bfloat16):
+        self.cfg = cfg
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.dtype = dtype
+        self.config = cfg  # engine reads num_layers / hidden_dim / num_experts / top_k / vocab_size
+        from flash_attn import flash_attn_varlen_func, flash_attn_with_kvcache
+
+        self._fa_varlen, self._fa_kvcache = flash_attn_varlen_func, flash_attn_with_kvcache
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        d, F, E, hd = cfg.hidden_dim, cfg.ffn_dim, cfg.num_experts, cfg.head_dim
+        H, KV = cfg.n_heads, cfg.n_kv_heads
+
+        def rnd(shape, std):
+            return (torch.randn(shape, generator=g, device=self.device, dtype=torch.float32) * std).to(dtype)
+
+        self.embedding = rnd((cfg.vocab_size, d), 1.0)
+        self.layers = []
+        for _ in range(cfg.num_layers):
+            L = _Layer()
+            L.ln1 = torch.ones(d, dtype=dtype, device=self.device)
+            L.ln2 = torch.ones(d, dtype=dtype, device=self.device)
+            L.w_qkv = rnd(((H + 2 * KV) * hd, d), d ** -0.5)
+            L.w_o = rnd((d, H * hd), (H * hd) ** -0.5)
+            L.w_router = rnd((E, d), d ** -0.5)
+            L.gate_up = torch.empty((E, 2 * F, d), dtype=dtype, device=self.device)
+            L.down = torch.empty((E, d, F), dtype=dtype, device=self.device)
+            for e in range(E):  # per expert to bound the fp32 temporary
+                L.gate_up[e] = rnd((2 * F, d), d ** -0.5)
+                L.down[e] = rnd((d, F), F ** -0.5)
+            if cfg.shared_ffn_dim:
+                Fs = cfg.shared_ffn_dim
+                L.sh_gate_up = rnd((1, 2 * Fs, d), d ** -0.5)
+                L.sh_down = rnd((1, d, Fs), Fs ** -0.5)
+                L.sh_gate = rnd((1, d), d ** -0.5)
+            self.layers.append(L)
+        self.final_norm = torch.ones(d, dtype=dtype, device=self.device)
+        self.lm_head = rnd((cfg.vocab_size, d), d ** -0.5)
+        inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, device=self.device, dtype=torch.float32) / hd))
+        ang = torch.arange(cfg.max_position, device=self.device, dtype=torch.float32)[:, None] * inv[None, :]
+        emb = torch.cat([ang, ang], -1)
+        self._cos, self._sin = emb.cos(), emb.sin()
+        self._stop = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._meta, self._meta_key = None, None
+
+    # ------------------------------------------------------------------ cache geometry
+    def kv_row_shape(self):
+        return (2, self.cfg.n_kv_heads, self.cfg.head_dim)
+
+    def kv_entry_bytes(self) -> int:
+        return 2 * self.cfg.n_kv_heads * self.cfg.head_dim * 2  # real bf16 K+V bytes per token per layer
+
+    @property
+    def kv_dtype(self):
+        return self.dtype
+
+    # ------------------------------------------------------------------ engine interface
+    def embed_batch(self, tokens: list[int]) -> torch.Tensor:
+        return self.embedding.index_select(0, torch.tensor(tokens, dtype=torch.long, device=self.device))
+
+    def _rope(self, t: torch.Tensor, pos: torch.Tensor) -> torch.Tensor:
+        cos, sin = self._cos[pos][:, None, :], self._sin[pos][:, None, :]
+        tf = t.float()
+        half = tf.shape[-1] // 2
+        rot = torch.cat([-tf[..., half:], tf[..., :half]], -1)
+        return (tf * cos + rot * sin).to(t.dtype)
+
+    def attention_batch(self, layer: int, h: torch.Tensor, members, cache):
+        cfg, L = self.cfg, self.layers[layer]
+        H, KV, hd = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+        T = h.shape[0]
+        x = rms_norm(h, L.ln1, cfg.rms_eps)
+        qkv = x @ L.w_qkv.T
+        q = qkv[:, : H * hd].view(T, H, hd)
+        k = qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd)
+        v = qkv[:, (H + KV) * hd:].view(T, KV, hd)
+        # Per-iteration metadata (positions, slot mapping, block table, lengths) is identical in
+        # every layer of a decode/prefill pass, so it is built once and reused across layers.
+        key = tuple((m.seq.cache_handle, cache.count(m.seq.cache_handle, layer), m.n) for m in members)
+        meta = self._meta if self._meta_key == key else None
+        decode = members[0].seq.phase is Phase.DECODE
+        slots = []
+        for m, (handle, have, n) in zip(members, key):
+            seq = m.seq
+            if (seq.phase is Phase.DECODE) != decode or have != (seq.tokens_fed() if decode else 0):
+                raise StateCorruptionError(f"sequence {seq.id} layer {layer}: {have} cached entries")
+            slots += cache.reserve(handle, layer, n, want_slots=meta is None)
+        if meta is None:
+            pos = [p for (_, have, n) in key for p in range(have, have + n)]
+            meta = {"pos": torch.tensor(pos, dtype=torch.long, device=self.device),
+                    "slots": torch.tensor(slots, dtype=torch.int32, device=self.device)}
+            if decode:
+                tables = [cache.page_table(h_) for (h_, _, _) in key]
+                width = max(len(t) for t in tables)
+                meta["bt"] = torch.tensor([t + [0] * (width - len(t)) for t in tables], dtype=torch.int32,
+                                          device=self.device)
+                meta["lens"] = torch.tensor([have + n for (_, have, n) in key], dtype=torch.int32, device=self.device)
+            else:
+                cu = [0]
+                for (_, _, n) in key:
+                    cu.append(cu[-1] + n)
+                meta["cu"] = torch.tensor(cu, dtype=torch.int32, device=self.device)
+                meta["max"] = max(n for (_, _, n) in key)
+            self._meta, self._meta_key = meta, key
+        q, k = self._rope(q, meta["pos"]), self._rope(k, meta["pos"])
+        cache.scatter(layer, meta["slots"], torch.stack([k, v], 1))
+        if decode:
+            pool = cache.pool(layer)
+            attn = self._fa_kvcache(q.view(T, 1, H, hd), pool[:, :, 0], pool[:, :, 1], cache_seqlens=meta["lens"],
+                                    block_table=meta["bt"], causal=True).view(T, H * hd)
+        else:
+            attn = self._fa_varlen(q, k, v, meta["cu"], meta["cu"], meta["max"], meta["max"],
+                                   causal=True).reshape(T, H * hd)
+        h2 = h + attn @ L.w_o.T
+        return rms_norm(h2, L.ln2, cfg.rms_eps).contiguous(), h2.contiguous()
+
+    def route_batch(self, layer: int, x: torch.Tensor):
+        return K.router(x, self.layers[layer].w_router, self.cfg.top_k, self.cfg.route_mode)
+
+    def new_expert_state(self, T: int):
+        y = torch.empty((T * self.cfg.top_k, self.cfg.hidden_dim), dtype=self.dtype, device=self.device)
+        return y, torch.zeros(T, dtype=torch.int32, device=self.device)
+
+    def permute(self, ids, cursor, x):
+        perm, offsets, xp = K.permute(ids, self.cfg.num_experts, cursor=cursor, x=x)
+        off = offsets.tolist()
+        return perm, offsets, xp, [off[e + 1] - off[e] for e in range(self.cfg.num_experts)]
+
+    def run_experts(self, layer: int, xp, offsets, perm, y, e_begin: int, e_end: int, preempt_flag=None):
+        L = self.layers[layer]
+        rows = xp.shape[0]
+        F = self.cfg.ffn_dim
+        act = K.workspace(rows * F * 2, "act", self.device).view(self.dtype)[: rows * F].view(rows, F)
+        K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, L.gate_up, L.down, y, e_begin=e_begin, e_end=e_end,
+                     act_ws=act, preempt_flag=preempt_flag, cursor_out=self._stop)
+        return self._stop
+
+    def advance_cursor(self, cursor, stop_dev):
+        K.cursor_advance(cursor, stop_dev)
+
+    def combine_batch(self, layer: int, y, w, res, x):
+        if self.cfg.shared_ffn_dim:
+            L = self.layers[layer]
+            T = x.shape[0]
+            Fs = self.cfg.shared_ffn_dim
+            offsets = torch.tensor([0, T], dtype=torch.int32, device=self.device)
+            ident = torch.arange(T, dtype=torch.int32, device=self.device)
+            ys = torch.empty_like(x)
+            act = K.workspace(T * Fs * 2, "act_shared", self.device).view(self.dtype)[: T * Fs].view(T, Fs)
+            K.expert_ffn(K.EXPERT_SWIGLU, x, offsets, ident, L.sh_gate_up, L.sh_down, ys, act_ws=act)
+            gate = torch.sigmoid(x.float() @ L.sh_gate.float().T)
+            res = (res.float() + gate * ys.float()).to(self.dtype)
+        return K.combine(y, w, res)
+
+    def emit_batch(self, h: torch.Tensor, rows: list[int]) -> list[int]:
+        hl = h.index_select(0, torch.tensor(rows, dtype=torch.long, device=self.device))
+        logits = (rms_norm(hl, self.final_norm, self.cfg.rms_eps) @ self.lm_head.T).float()
+        return torch.argmax(logits, dim=1).tolist()  # first maximal index: ties to the lowest id
+
+    @staticmethod
+    def cat_rows(parts):
+        return parts[0] if len(parts) == 1 else torch.cat(parts, 0)
