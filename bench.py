@@ -194,6 +194,25 @@ def count_launches(T: int, world: int) -> int:
     return 1 + permute_launches(T, TOPK) + 4 + 1 + (2 if world > 1 else 0)
 
 
+def run_serving(args) -> dict:
+    """The LS TTFT p50/p99 + BE tokens/s half of the metric: wall-clock QLLM vs FCFS serving of a
+    full 32-layer Mixtral-8x7B-shaped model (random-init bf16) on the paper workload."""
+    import torch
+
+    from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, DecoderMoEModel
+    from paper_2503_09304_b200.serving import compare, warm_up
+
+    model = DecoderMoEModel(MIXTRAL_8X7B)
+    warm_up(model)
+    out = compare(model, args.serve_rate, args.serve_duration)
+    for k in ("fcfs", "qllm"):
+        out[k].pop("engine", None)
+    out["model"] = "mixtral-8x7b (32 layers, random-init bf16), batch 32, SLO 3000 ms, paper workload (20% LS)"
+    del model
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, rank: int, world: int) -> None:
     import torch
     import torch.distributed as dist
@@ -287,6 +306,11 @@ def run_ours(args, rank: int, world: int) -> None:
         dec.append((a, b))
     barrier()
     dec_ms = statistics.median(a.elapsed_time(b) for a, b in dec)
+    serving = None
+    if world == 1 and args.serve_duration > 0:
+        del block, x, xd, flush
+        torch.cuda.empty_cache()
+        serving = run_serving(args)
     if rank != 0:
         return
 
@@ -335,6 +359,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "gpu_launches": count_launches(T, world) * args.steps,
         "clocks": clocks,
         "cpu_baseline": cpu,
+        "serving": serving,
     }
     print(json.dumps(line), flush=True)
 
@@ -349,6 +374,9 @@ def main():
     ap.add_argument("--decode-tokens", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--serve-rate", type=float, default=7.0)
+    ap.add_argument("--serve-duration", type=float, default=20.0,
+                    help="seconds of paper-workload trace served by QLLM and by FCFS (0 disables)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

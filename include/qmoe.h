@@ -109,13 +109,16 @@ QMOE_API int qmoe_permute(const int32_t* ids, const int32_t* cursor, int T, int 
  *                act_ws = [R, F] scratch of the input dtype.
  * dtype QMOE_BF16 runs on tcgen05/TMEM tensor cores (TMA-fed); F32/F64 run the SIMT path used
  * for bit-faithful parity builds.
- * preempt_flag (optional, device-visible, e.g. mapped host memory): polled at every expert
- * boundary; once non-zero, no tile of a later expert is started.  cursor_out (optional, device
+ * preempt_flag (optional, device-visible, e.g. mapped host memory): 0 = run on; s > 0 requests a
+ * stop at the first expert boundary >= s (experts < s always complete).  Polled at every tile
+ * claim, so the launch stops at the next expert boundary without a host round trip.  cursor_out (optional, device
  * int32[1]) receives the first expert NOT completed (== e_end when the launch ran to completion).
  * xp_rows = allocated rows of Xp / act_ws (>= offsets[E]; bounds the TMA tensor maps).
- * workspace: qmoe_expert_ffn_workspace_bytes() bytes of device memory (tile claim counters).
+ * workspace: qmoe_expert_ffn_workspace_bytes(variant, dtype, d, xp_rows) bytes of device memory
+ * (tile claim counters; for small bf16 SwiGLU batches also the fp32 split-K partials of the down
+ * projection, which is then K-split so few-expert launches still fill every SM).
  */
-QMOE_API size_t qmoe_expert_ffn_workspace_bytes(void);
+QMOE_API size_t qmoe_expert_ffn_workspace_bytes(int variant, int dtype, int d, int xp_rows);
 QMOE_API int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int32_t* offsets,
                     const int32_t* perm, int E, int d, int F, const void* w1, const void* w2,
                     int e_begin, int e_end, int xp_rows, void* act_ws, void* y,

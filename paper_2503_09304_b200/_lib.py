@@ -46,7 +46,7 @@ SIGNATURES = {
     "qmoe_router": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
     "qmoe_permute_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int]),
     "qmoe_permute": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_size, _vp, _vp, _c_size, _vp]),
-    "qmoe_expert_ffn_workspace_bytes": (_c_size, []),
+    "qmoe_expert_ffn_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int, _c_int]),
     "qmoe_expert_ffn": (_c_int, [_c_int, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _c_int,
                                  _c_int, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
     "qmoe_combine": (_c_int, [_c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp]),

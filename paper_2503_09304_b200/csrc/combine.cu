@@ -46,12 +46,15 @@ combine_exact_kernel(const T* __restrict__ y, const T* __restrict__ w, const T* 
 }
 
 // bf16 Y/residual/out, fp32 weights and accumulation, 8 elements (16 B) per lane per step.
+// `parts` warps share one token (each a contiguous slice of the row) so small decode batches
+// still put enough warps in flight.
 template <int K>
 __global__ void __launch_bounds__(kCombWarps * 32)
 combine_bf16_kernel(const __nv_bfloat16* __restrict__ y, const float* __restrict__ w,
-                    const __nv_bfloat16* __restrict__ residual, int ntok, int k, int d,
+                    const __nv_bfloat16* __restrict__ residual, int ntok, int k, int d, int parts,
                     __nv_bfloat16* __restrict__ out) {
-  const int tok = blockIdx.x * kCombWarps + warp_id();
+  const int gw = blockIdx.x * kCombWarps + warp_id();
+  const int tok = gw / parts, part = gw - tok * parts;
   if (tok >= ntok) return;
   const int lane = lane_id();
   float wt[8];
@@ -60,7 +63,9 @@ combine_bf16_kernel(const __nv_bfloat16* __restrict__ y, const float* __restrict
   for (int j = 0; j < 8; ++j) wt[j] = j < kk ? w[(size_t)tok * kk + j] : 0.f;
   const uint4* y4 = reinterpret_cast<const uint4*>(y + (size_t)tok * kk * d);
   const int nv = d >> 3;  // uint4 per row
-  for (int v = lane; v < nv; v += 32) {
+  const int per = (nv + parts - 1) / parts;
+  const int v_end = min(nv, (part + 1) * per);
+  for (int v = part * per + lane; v < v_end; v += 32) {
     float acc[8];
     if (residual != nullptr) {
       uint4 r = __ldg(reinterpret_cast<const uint4*>(residual + (size_t)tok * d) + v);
@@ -173,12 +178,17 @@ extern "C" int qmoe_combine(int dtype, const void* y, const void* w, const void*
       auto yb = (const __nv_bfloat16*)y;
       auto rb = (const __nv_bfloat16*)residual;
       auto ob = (__nv_bfloat16*)out;
+      // enough warps to cover the SMs: split each row over up to d/256 warps for small T
+      int parts = (148 * kCombWarps + T - 1) / T;
+      const int max_parts = d / 256 > 0 ? d / 256 : 1;
+      parts = parts < 1 ? 1 : (parts > max_parts ? max_parts : parts);
+      const dim3 g2((T * parts + kCombWarps - 1) / kCombWarps);
       if (k == 2)
-        combine_bf16_kernel<2><<<grid, block, 0, s>>>(yb, (const float*)w, rb, T, k, d, ob);
+        combine_bf16_kernel<2><<<g2, block, 0, s>>>(yb, (const float*)w, rb, T, k, d, parts, ob);
       else if (k == 4)
-        combine_bf16_kernel<4><<<grid, block, 0, s>>>(yb, (const float*)w, rb, T, k, d, ob);
+        combine_bf16_kernel<4><<<g2, block, 0, s>>>(yb, (const float*)w, rb, T, k, d, parts, ob);
       else
-        combine_bf16_kernel<0><<<grid, block, 0, s>>>(yb, (const float*)w, rb, T, k, d, ob);
+        combine_bf16_kernel<0><<<g2, block, 0, s>>>(yb, (const float*)w, rb, T, k, d, parts, ob);
       break;
     }
     default:

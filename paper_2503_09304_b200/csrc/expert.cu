@@ -26,8 +26,10 @@ int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cur
 
 }  // namespace qmoe
 
-extern "C" size_t qmoe_expert_ffn_workspace_bytes(void) {
-  return sizeof(qmoe::FfnWorkspace) * qmoe::kFfnWorkspaceSlots;
+extern "C" size_t qmoe_expert_ffn_workspace_bytes(int variant, int dtype, int d, int xp_rows) {
+  size_t n = sizeof(qmoe::FfnWorkspace) * qmoe::kFfnWorkspaceSlots;
+  if (variant == QMOE_EXPERT_SWIGLU && dtype == QMOE_BF16) n += qmoe::splitk_bytes(xp_rows, d);
+  return n;
 }
 
 extern "C" int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int32_t* offsets,
@@ -42,8 +44,9 @@ extern "C" int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int
   QMOE_REQUIRE(variant == QMOE_EXPERT_TANH_AFFINE || F >= 1, "qmoe_expert_ffn: SwiGLU needs F >= 1");
   QMOE_REQUIRE(0 <= e_begin && e_begin <= e_end && e_end <= E, "qmoe_expert_ffn: bad expert range [%d, %d)",
                e_begin, e_end);
-  QMOE_REQUIRE(workspace != nullptr && workspace_bytes >= qmoe_expert_ffn_workspace_bytes(),
-               "qmoe_expert_ffn: workspace too small");
+  QMOE_REQUIRE(workspace != nullptr && workspace_bytes >= qmoe_expert_ffn_workspace_bytes(variant, dtype, d, xp_rows),
+               "qmoe_expert_ffn: workspace too small (%zu < %zu)", workspace_bytes,
+               qmoe_expert_ffn_workspace_bytes(variant, dtype, d, xp_rows));
   QMOE_REQUIRE(offsets && w1 && y && (xp_rows == 0 || (xp && perm)), "qmoe_expert_ffn: null pointer");
   QMOE_REQUIRE(variant != QMOE_EXPERT_SWIGLU || act_ws != nullptr, "qmoe_expert_ffn: SwiGLU needs act_ws");
   QMOE_REQUIRE(variant != QMOE_EXPERT_TANH_AFFINE || w2 != nullptr, "qmoe_expert_ffn: tanh expert needs bias");

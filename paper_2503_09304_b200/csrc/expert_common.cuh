@@ -3,10 +3,13 @@
 // Tiles are numbered expert-major (ascending expert id, the reference's drain order,
 // model.py:202-204), then by N block, then by M block (M fastest, so consecutive claims reuse the
 // same weight block from L2).  They are claimed from one global counter, so at any instant the
-// claimed set is a prefix of that order.  The device preempt flag is checked at each claim:
-// seeing it at the FIRST tile of expert e stops before e; seeing it inside e lets e finish and
-// stops before e+1.  The stop expert is kept as max(INT_MAX - stop) so a zeroed workspace means
-// "no stop".  Invariant: every tile of every expert < final stop is executed.
+// claimed set is a prefix of that order.  The device preempt flag holds 0 (run on) or s > 0:
+// "stop at the first expert boundary >= s" — the scheduler answered PREEMPT at the report of
+// expert s-1, so experts < s always complete (progress is guaranteed, as in the reference where
+// a preemption lands after the reported expert's drain).  Seen at a claim of expert e it votes
+// for max(s, e) if the tile is e's first (stop before e), else max(s, e+1).  The stop expert
+// is kept as max(INT_MAX - stop) so a zeroed workspace means "no stop".  Invariant: every tile
+// of every expert < final stop is executed.
 #pragma once
 
 #include <limits.h>
@@ -32,43 +35,73 @@ struct TileMap {
   int row_begin[64];        // offsets[e]
   int m_tiles[64];
 
-  __device__ __forceinline__ void locate(int tile, int bm, int n_tiles_n, int bn, int& e, int& m0, int& n0) const {
-    int i = 0;
-    while (tile >= tile_begin[i + 1]) ++i;
+  // Index of the covered expert owning `tile` (binary search over the tile prefix).
+  __device__ __forceinline__ int slot_of(int tile) const {
+    int lo = 0, hi = n_exp - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tile_begin[mid] <= tile) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  }
+  // Tile -> (expert, first row, first column, split).  Within an expert tiles run N-block
+  // major, M fastest; the `nsplit` K-splits of one (M, N) tile are adjacent N-block entries.
+  __device__ __forceinline__ void locate(int tile, int bm, int n_tiles_n, int bn, int& e, int& m0, int& n0,
+                                         int nsplit = 1, int* split = nullptr) const {
+    const int i = slot_of(tile);
     const int local = tile - tile_begin[i];
     const int nt = local / m_tiles[i];
     const int mt = local - nt * m_tiles[i];
     e = e_first + i;
     m0 = row_begin[i] + mt * bm;
-    n0 = nt * bn;
+    n0 = (nt / nsplit) * bn;
+    if (split != nullptr) *split = nt % nsplit;
   }
   __device__ __forceinline__ int expert_of(int tile, int& local) const {
-    int i = 0;
-    while (tile >= tile_begin[i + 1]) ++i;
+    const int i = slot_of(tile);
     local = tile - tile_begin[i];
     return e_first + i;
   }
 };
 
-// Called by one thread.  e_limit (optional, device) caps the covered experts (chained launches).
+// Called by all 32 lanes of ONE warp: per-expert row ranges loaded in parallel, tile counts
+// prefix-summed with warp shuffles (E <= 64).  e_limit (optional, device) caps the covered
+// experts (chained launches).  n_tiles_n already includes any K-split factor.
 __device__ __forceinline__ void build_tile_map(TileMap& m, const int32_t* offsets, int e_begin, int e_end,
                                                const int32_t* e_limit, int bm, int n_tiles_n) {
+  const int lane = threadIdx.x & 31;
   int hi = e_end;
   if (e_limit != nullptr) hi = min(hi, *e_limit);
   if (hi < e_begin) hi = e_begin;
-  m.e_first = e_begin;
-  m.n_exp = hi - e_begin;
-  int acc = 0;
-  m.tile_begin[0] = 0;
-  for (int i = 0; i < m.n_exp; ++i) {
-    const int r0 = offsets[e_begin + i], r1 = offsets[e_begin + i + 1];
-    const int mt = (r1 - r0 + bm - 1) / bm;
-    m.row_begin[i] = r0;
-    m.m_tiles[i] = mt;
-    acc += mt * n_tiles_n;
-    m.tile_begin[i + 1] = acc;
+  const int n = hi - e_begin;
+  int carry = 0;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int i = lane + 32 * half;
+    int tiles = 0;
+    if (i < n) {
+      const int r0 = offsets[e_begin + i], r1 = offsets[e_begin + i + 1];
+      const int mt = (r1 - r0 + bm - 1) / bm;
+      m.row_begin[i] = r0;
+      m.m_tiles[i] = mt;
+      tiles = mt * n_tiles_n;
+    }
+    int incl = tiles;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (i < n) m.tile_begin[i + 1] = carry + incl;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
   }
-  m.total = acc;
+  if (lane == 0) {
+    m.tile_begin[0] = 0;
+    m.e_first = e_begin;
+    m.n_exp = n;
+    m.total = carry;
+  }
+  __syncwarp();
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -78,20 +111,31 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 
 // Claim the next tile or return -1 (no work left, or the preempt boundary was reached).
-__device__ __forceinline__ int ffn_claim(const TileMap& m, FfnWorkspace* ws, const volatile int32_t* flag) {
+// `last_e` is the caller's previously claimed expert: the (possibly host-mapped, PCIe-latency)
+// flag is only read when the claimer moves to a new expert — the only place a stop can take
+// effect — while the device-side stop vote is consulted on every claim.
+__device__ __forceinline__ int ffn_claim(const TileMap& m, FfnWorkspace* ws, const volatile int32_t* flag,
+                                         int& last_e) {
   const int t = atomicAdd(&ws->next, 1);
   if (t >= m.total) return -1;
   int local;
   const int e = m.expert_of(t, local);
-  if (flag != nullptr && *flag != 0) {
-    const int cand = local == 0 ? e : e + 1;
-    atomicMax(&ws->stop_inv, INT_MAX - cand);
+  if (flag != nullptr && e != last_e) {
+    const int s = *flag;
+    if (s > 0) {
+      int cand = local == 0 ? e : e + 1;
+      if (cand < s) cand = s;
+      atomicMax(&ws->stop_inv, INT_MAX - cand);
+    }
   }
+  last_e = e;
   const int stop = INT_MAX - ld_acquire(&ws->stop_inv);
   return e < stop ? t : -1;
 }
 
 int ffn_ws_reset(FfnWorkspace* ws, cudaStream_t s);
+// Extra workspace the bf16 SwiGLU path needs for split-K partials of the down projection.
+size_t splitk_bytes(int xp_rows, int d);
 // cursor = min(stop of ws, *limit (optional), e_end); written to ws->stop and cursor_out (optional).
 int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out, cudaStream_t s);
 

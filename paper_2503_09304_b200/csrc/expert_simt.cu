@@ -39,12 +39,13 @@ ffn_simt_kernel(const T* __restrict__ a_rows, const int32_t* __restrict__ offset
   __shared__ int s_tile;
   const int tid = threadIdx.x;
   const int n_tiles_n = (N + BN - 1) / BN;
-  if (tid == 0) build_tile_map(map, offsets, e_begin, e_end, e_limit, BM, n_tiles_n);
+  if (tid < 32) build_tile_map(map, offsets, e_begin, e_end, e_limit, BM, n_tiles_n);
   __syncthreads();
   const int ty = tid >> 5, tx = tid & 31;  // rows ty*4.., cols tx, tx+32
+  int last_e = -1;
 
   while (true) {
-    if (tid == 0) s_tile = ffn_claim(map, ws, flag);
+    if (tid == 0) s_tile = ffn_claim(map, ws, flag, last_e);
     __syncthreads();
     const int tile = s_tile;
     __syncthreads();

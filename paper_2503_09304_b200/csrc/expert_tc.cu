@@ -31,7 +31,17 @@ constexpr int kTileRing = 4;
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
 
-enum { EPI_TANH = 0, EPI_SWIGLU = 1, EPI_DOWN = 2 };
+enum { EPI_TANH = 0, EPI_SWIGLU = 1, EPI_DOWN = 2, EPI_DOWN_PART = 3 };
+
+// Small-batch down projection: split the K loop so a launch with few (expert, N-block) tiles
+// still spreads over every SM.  Partials are fp32 [split][row][N], reduced in fixed split order
+// (deterministic) by splitk_reduce_kernel, which also scatters rows to their token slots.
+constexpr int kMaxSplit = 8;
+constexpr int kSplitRowsMax = 512;
+}  // namespace
+int down_splits(int xp_rows, int n_experts, int d, int F);
+float* splitk_buffer(FfnWorkspace* ws);
+namespace {
 
 struct TcParams {
   int N;         // output columns of this GEMM (act columns F for the SwiGLU gate_up pass)
@@ -46,6 +56,10 @@ struct TcParams {
   int out_ld;
   const volatile int32_t* flag;
   FfnWorkspace* ws;
+  int nsplit;         // K splits per (M, N) tile (EPI_DOWN_PART), else 1
+  int kb_per_split;
+  float* part;        // [nsplit][part_rows][N] fp32 partials
+  int part_rows;
 };
 
 template <int BN>
@@ -70,6 +84,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   __shared__ TileMap map;
 
   constexpr int BN_OUT = (EPI == EPI_SWIGLU) ? BN / 2 : BN;  // output columns per tile
+  const int nsplit = (EPI == EPI_DOWN_PART) ? p.nsplit : 1;
   constexpr int kStageBytes = stage_bytes<BN>();
   constexpr int kABytes = BM * BK * 2;
   constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(BM, BN);
@@ -79,8 +94,8 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const int n_tiles_n = (p.N + BN_OUT - 1) / BN_OUT;
   const int nkb = (p.K + BK - 1) / BK;
 
-  if (threadIdx.x == 0) {
-    build_tile_map(map, p.offsets, p.e_begin, p.e_end, p.e_limit, BM, n_tiles_n);
+  if (warp == 0) build_tile_map(map, p.offsets, p.e_begin, p.e_end, p.e_limit, BM, n_tiles_n * nsplit);
+  if (threadIdx.x == 32) {
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
@@ -106,22 +121,24 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmA);
       ptx::tma_prefetch_desc(&tmB);
-      int stage = 0, slot = 0;
+      int stage = 0, slot = 0, last_e = -1;
       uint32_t phase = 0, rphase = 0;
       while (true) {
-        const int tile = ffn_claim(map, p.ws, p.flag);
+        const int tile = ffn_claim(map, p.ws, p.flag, last_e);
         ptx::mbar_wait(&ring_empty[slot], rphase ^ 1);
         ring_tile[slot] = tile;
         ptx::mbar_arrive(&ring_full[slot]);
         if (++slot == kTileRing) { slot = 0; rphase ^= 1; }
         if (tile < 0) break;
-        int e, m0, n0;
-        map.locate(tile, BM, n_tiles_n, BN_OUT, e, m0, n0);
+        int e, m0, n0, split;
+        map.locate(tile, BM, n_tiles_n * nsplit, BN_OUT, e, m0, n0, nsplit, &split);
         // B rows of this tile: two halves of BN/2 rows each.  gate_up: gate rows [n0, n0+BN/2),
         // up rows F + [n0, n0+BN/2) so accumulator columns [0,BN/2) = gate, [BN/2,BN) = up.
         const int brow0 = e * p.b_rows + n0;
         const int brow1 = (EPI == EPI_SWIGLU) ? e * p.b_rows + p.N + n0 : brow0 + BN / 2;
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int kb0 = split * (nsplit > 1 ? p.kb_per_split : nkb);
+        const int kb1 = min(nkb, kb0 + (nsplit > 1 ? p.kb_per_split : nkb));
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes;
           uint8_t* sb = sa + kABytes;
@@ -145,10 +162,14 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         ptx::mbar_arrive(&ring_empty[slot]);
         if (++slot == kTileRing) { slot = 0; rphase ^= 1; }
         if (tile < 0) break;
+        int e_, m0_, n0_, split;
+        map.locate(tile, BM, n_tiles_n * nsplit, BN_OUT, e_, m0_, n0_, nsplit, &split);
+        const int kb0 = split * (nsplit > 1 ? p.kb_per_split : nkb);
+        const int kb1 = min(nkb, kb0 + (nsplit > 1 ? p.kb_per_split : nkb));
         ptx::mbar_wait(&tempty_bar[acc], aphase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(smem + stage * kStageBytes);
@@ -156,7 +177,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             ptx::tc_mma_bf16(d_tmem, ptx::sw128_kmajor_desc(a_addr + k * 32), ptx::sw128_kmajor_desc(b_addr + k * 32),
-                             kIdesc, (kb | k) != 0);
+                             kIdesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           ptx::tc_commit(&empty_bar[stage]);  // smem slot free once these MMAs retire
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -178,14 +199,19 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       if (lane == 0) ptx::mbar_arrive(&ring_empty[slot]);
       if (++slot == kTileRing) { slot = 0; rphase ^= 1; }
       if (tile < 0) break;
-      int e, m0, n0;
-      map.locate(tile, BM, n_tiles_n, BN_OUT, e, m0, n0);
+      int e, m0, n0, split;
+      map.locate(tile, BM, n_tiles_n * nsplit, BN_OUT, e, m0, n0, nsplit, &split);
       const int row = m0 + ew * 32 + lane;
       const bool valid = row < p.offsets[e + 1];
       __nv_bfloat16* dst_row = nullptr;
+      float* part_row = nullptr;
       if (valid) {
-        const size_t orow = (EPI == EPI_SWIGLU) ? (size_t)row : (size_t)p.perm[row];
-        dst_row = p.out + orow * p.out_ld;
+        if constexpr (EPI == EPI_DOWN_PART) {
+          part_row = p.part + ((size_t)split * p.part_rows + row) * p.N;
+        } else {
+          const size_t orow = (EPI == EPI_SWIGLU) ? (size_t)row : (size_t)p.perm[row];
+          dst_row = p.out + orow * p.out_ld;
+        }
       }
       ptx::mbar_wait(&tfull_bar[acc], aphase);
       ptx::tc_fence_after();
@@ -195,7 +221,15 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         uint32_t v[32];
         ptx::tmem_ld32(t_row + c, v);
         uint32_t packed[16];
-        if constexpr (EPI == EPI_SWIGLU) {
+        if constexpr (EPI == EPI_DOWN_PART) {
+          ptx::tmem_ld_wait();
+          if (valid && n0 + c < p.N) {
+            uint4* d4 = reinterpret_cast<uint4*>(part_row + n0 + c);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) d4[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          }
+          continue;
+        } else if constexpr (EPI == EPI_SWIGLU) {
           uint32_t u[32];
           ptx::tmem_ld32(t_row + BN / 2 + c, u);
           ptx::tmem_ld_wait();
@@ -236,6 +270,29 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<2 * BN>(tmem_base);
+  }
+}
+
+// Y[perm[r]] = bf16(sum_s part[s][r]) for the rows of experts [e_begin, stop); one warp per row.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ part, int nsplit, int part_rows,
+                                                            int N, const int32_t* __restrict__ perm,
+                                                            const int32_t* __restrict__ offsets, int e_begin,
+                                                            const int32_t* __restrict__ stop,
+                                                            __nv_bfloat16* __restrict__ y) {
+  const int r0 = offsets[e_begin], r1 = offsets[*stop];
+  const int lane = threadIdx.x & 31;
+  for (int r = r0 + blockIdx.x * 8 + (threadIdx.x >> 5); r < r1; r += gridDim.x * 8) {
+    __nv_bfloat16* dst = y + (size_t)perm[r] * N;
+    for (int c = lane * 8; c < N; c += 256) {
+      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int s = 0; s < nsplit; ++s) {
+        const float4* src = reinterpret_cast<const float4*>(part + ((size_t)s * part_rows + r) * N + c);
+        const float4 u = __ldg(src), w = __ldg(src + 1);
+        a[0] += u.x; a[1] += u.y; a[2] += u.z; a[3] += u.w; a[4] += w.x; a[5] += w.y; a[6] += w.z; a[7] += w.w;
+      }
+      uint4 o = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+      *reinterpret_cast<uint4*>(dst + c) = o;
+    }
   }
 }
 
@@ -345,8 +402,45 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   p2.out = (__nv_bfloat16*)y; p2.out_ld = d;
   p2.e_limit = &ws[0].stop;
   p2.ws = ws + 1;
+  const int nsplit = down_splits(xp_rows, e_end - e_begin, d, F);
+  if (nsplit > 1) {
+    const int nkb = (F + BK - 1) / BK;
+    p2.kb_per_split = (nkb + nsplit - 1) / nsplit;
+    p2.nsplit = (nkb + p2.kb_per_split - 1) / p2.kb_per_split;  // every split non-empty
+    p2.part = splitk_buffer(ws);
+    p2.part_rows = xp_rows;
+    if ((st = launch_tc<BN, EPI_DOWN_PART>(ta2, tb2, p2, s))) return st;
+    if ((st = ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s))) return st;
+    const int grid = xp_rows / 8 + 1 < 148 * 4 ? xp_rows / 8 + 1 : 148 * 4;
+    splitk_reduce_kernel<<<grid, 256, 0, s>>>(p2.part, p2.nsplit, xp_rows, d, perm, offsets, e_begin, &ws[1].stop,
+                                               (__nv_bfloat16*)y);
+    return check_launch("qmoe_expert_ffn(split-K reduce)");
+  }
+  p2.nsplit = 1;
   if ((st = launch_tc<BN, EPI_DOWN>(ta2, tb2, p2, s))) return st;
   return ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s);
+}
+
+int down_splits(int xp_rows, int n_experts, int d, int F) {
+  // Small batches (<= 512 routed rows) run the down projection K-split so launches covering few
+  // experts (a resume after an expert-boundary preemption, or a batch hitting 1-2 experts) still
+  // fill every SM.  The split count depends only on the problem shape — never on the expert
+  // range — so a resumed launch rounds exactly like an uninterrupted one (bit-identical resume).
+  (void)n_experts;
+  (void)d;
+  if (xp_rows > kSplitRowsMax) return 1;
+  int want = 4;
+  if (want > (F / BK) / 16) want = (F / BK) / 16;  // >= 16 K blocks (1024) per split
+  if (want > kMaxSplit) want = kMaxSplit;
+  return want < 1 ? 1 : want;
+}
+
+size_t splitk_bytes(int xp_rows, int d) {
+  return xp_rows > kSplitRowsMax ? 0 : (size_t)kMaxSplit * xp_rows * d * sizeof(float);
+}
+
+float* splitk_buffer(FfnWorkspace* ws) {
+  return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + sizeof(FfnWorkspace) * kFfnWorkspaceSlots);
 }
 
 }  // namespace qmoe

@@ -66,7 +66,13 @@ router_kernel(const T* __restrict__ x, const T* __restrict__ wr, int ntok, int d
   const int per_warp = (nvec + kWarps - 1) / kWarps;
   const int v0 = warp * per_warp, v1 = min(nvec, v0 + per_warp);
 
-  for (int ec = 0; ec < E; ec += kExpChunk) {
+  // Few experts (E <= 16): the warps split d and every warp covers all experts.  Many experts
+  // (Qwen: 60): the warps take 8-expert chunks in parallel over the full d (no serial chunk loop).
+  const bool split_d = E <= 2 * kExpChunk;
+  const int c_begin = split_d ? 0 : warp * kExpChunk;
+  const int c_step = split_d ? kExpChunk : kWarps * kExpChunk;
+  const int w_v0 = split_d ? v0 : 0, w_v1 = split_d ? v1 : nvec;
+  for (int ec = c_begin; ec < E; ec += c_step) {
     A acc[TPC][kExpChunk];
 #pragma unroll
     for (int t = 0; t < TPC; ++t)
@@ -79,7 +85,7 @@ router_kernel(const T* __restrict__ x, const T* __restrict__ wr, int ntok, int d
 #pragma unroll
     for (int t = 0; t < TPC; ++t) xrow[t] = x + (size_t)min(tok0 + t, ntok - 1) * d;
 
-    for (int v = v0 + lane; v < v1; v += 32) {
+    for (int v = w_v0 + lane; v < w_v1; v += 32) {
       A xv[TPC][N], wv[kExpChunk][N];
       if constexpr (VEC) {
         using U = typename Vec<T>::U;
@@ -105,23 +111,34 @@ router_kernel(const T* __restrict__ x, const T* __restrict__ wr, int ntok, int d
 #pragma unroll
           for (int q = 0; q < N; ++q) acc[t][j] += xv[t][q] * wv[j][q];
     }
+    if (split_d) {
 #pragma unroll
-    for (int t = 0; t < TPC; ++t)
+      for (int t = 0; t < TPC; ++t)
 #pragma unroll
-      for (int j = 0; j < kExpChunk; ++j) {
-        const A sum = warp_sum(acc[t][j]);
-        if (lane == 0) s_part[warp][t][j] = sum;
+        for (int j = 0; j < kExpChunk; ++j) {
+          const A sum = warp_sum(acc[t][j]);
+          if (lane == 0) s_part[warp][t][j] = sum;
+        }
+      __syncthreads();
+      if (threadIdx.x < TPC * kExpChunk) {
+        const int t = threadIdx.x / kExpChunk, j = threadIdx.x % kExpChunk;
+        A sum = A(0);
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) sum += s_part[w][t][j];
+        if (ec + j < E) s_logit[t][ec + j] = sum;
       }
-    __syncthreads();
-    if (threadIdx.x < TPC * kExpChunk) {
-      const int t = threadIdx.x / kExpChunk, j = threadIdx.x % kExpChunk;
-      A sum = A(0);
+      __syncthreads();
+    } else {
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) sum += s_part[w][t][j];
-      if (ec + j < E) s_logit[t][ec + j] = sum;
+      for (int t = 0; t < TPC; ++t)
+#pragma unroll
+        for (int j = 0; j < kExpChunk; ++j) {
+          const A sum = warp_sum(acc[t][j]);
+          if (lane == 0 && ec + j < E) s_logit[t][ec + j] = sum;
+        }
     }
-    __syncthreads();
   }
+  if (!split_d) __syncthreads();
 
   // Selection: thread t owns token tok0 + t.
   if (threadIdx.x < TPC) {

@@ -158,7 +158,7 @@ class InferenceEngine:
     """Single-host-thread engine; all tensor work is enqueued on the current CUDA stream."""
 
     def __init__(self, model, cache, clock, cost_model: CostModel = CostModel(), max_batch_size: int = 32,
-                 log: Optional[list] = None):
+                 log: Optional[list] = None, device_preempt: Optional[bool] = None):
         cost_model.validate()
         self.model = model
         self.cache = cache
@@ -170,6 +170,13 @@ class InferenceEngine:
         self._batch_counter = 0
         self.stats = {"iterations": 0, "preemptions": 0, "expert_launches": 0, "zero_copy_restores": 0,
                       "copy_restores": 0}
+        # Device-resident preemption (flag polled by the grouped kernel) is the wall-clock default;
+        # virtual-clock runs decide the boundary before the launch so they replay the reference
+        # decision log exactly.
+        self._device_preempt = (not getattr(clock, "virtual", True)) if device_preempt is None else device_preempt
+        self._pinned_off = None
+        self._flags = None
+        self._flag_slot = 0
 
     def next_batch_id(self) -> int:
         self._batch_counter += 1
@@ -221,26 +228,11 @@ class InferenceEngine:
                 stage = Stage.EXPERTS
 
             # EXPERTS: queue build for the pending slots, boundary decisions, one grouped launch.
-            perm, offsets, xp, counts = m.permute(st.ids, st.cursor, st.x)
-            slots = None
-            if self.log is not None and sum(counts):
-                slots = perm[: sum(counts)].tolist()
-            stop, preempted, start = E, False, 0
-            for e in range(E):
-                n = counts[e]
-                if n == 0:
-                    continue
-                if slots is not None:
-                    self._log_queue(st, layer, e, slots[start:start + n])
-                start += n
-                self._charge(self.cost.expert_cost(n))
-                if on_report(self._report(batch, Stage.EXPERTS, layer, st, expert_id=e)) is PREEMPT:
-                    stop, preempted = e + 1, True
-                    break
-            stop_dev = None
-            if sum(counts):
-                stop_dev = m.run_experts(layer, xp, offsets, perm, st.y, 0, stop)
-                self.stats["expert_launches"] += 1
+            perm, offsets, xp = m.permute(st.ids, st.cursor, st.x)
+            if self._device_preempt:
+                stop_dev, preempted = self._experts_device_preempt(batch, st, layer, perm, offsets, xp, on_report)
+            else:
+                stop_dev, preempted = self._experts_host_boundary(batch, st, layer, perm, offsets, xp, on_report)
             if preempted:
                 m.advance_cursor(st.cursor, stop_dev)
                 return self._preempt(st, layer, Stage.EXPERTS)
@@ -254,6 +246,78 @@ class InferenceEngine:
         return Completed({s.id: int(t) for s, t in zip(st.seqs, tokens)})
 
     # ------------------------------------------------------------------------------------------
+    def _experts_host_boundary(self, batch, st, layer, perm, offsets, xp, on_report):
+        """Virtual-clock / exact mode: read the queue lengths (one small D2H), answer every
+        expert-boundary report on the host, then ONE launch for experts [0, stop)."""
+        m = self.model
+        E = m.config.num_experts
+        off = offsets.tolist()
+        counts = [off[e + 1] - off[e] for e in range(E)]
+        slots = perm[: off[E]].tolist() if (self.log is not None and off[E]) else None
+        stop, preempted = E, False
+        for e in range(E):
+            n = counts[e]
+            if n == 0:
+                continue
+            if slots is not None:
+                self._log_queue(st, layer, e, slots[off[e]:off[e] + n])
+            self._charge(self.cost.expert_cost(n))
+            if self._on_report(batch, st, layer, e, on_report) is PREEMPT:
+                stop, preempted = e + 1, True
+                break
+        stop_dev = None
+        if off[E]:
+            stop_dev = m.run_experts(layer, xp, offsets, perm, st.y, 0, stop)
+            self.stats["expert_launches"] += 1
+        return stop_dev, preempted
+
+    def _experts_device_preempt(self, batch, st, layer, perm, offsets, xp, on_report):
+        """Wall-clock mode: launch ALL experts at once with a fresh device preempt flag (polled by
+        the kernel whenever a CTA moves to a new expert), copy the queue lengths asynchronously,
+        and answer the expert-boundary reports on the host WHILE the grouped GEMM runs.  A PREEMPT
+        answer raises the flag: the kernel stops at the next expert boundary and writes where it
+        stopped (cursor_out), from which the per-token cursors advance on the device — no host
+        round trip between the decision and the stop."""
+        import torch
+
+        m = self.model
+        E = m.config.num_experts
+        dev = m.device
+        if self._pinned_off is None or self._pinned_off.numel() != E + 1:
+            self._pinned_off = torch.empty(E + 1, dtype=torch.int32, pin_memory=True)
+            self._off_ready = torch.cuda.Event()
+            # Flags live in DEVICE memory (an L2 hit for the polling SMs; host-mapped memory polled
+            # by every CTA serialises on PCIe).  A ring of slots, one per launch; slot i+512 is
+            # zeroed in stream order so a slot is clean long before reuse.
+            self._flags = torch.zeros(1024, dtype=torch.int32, device=dev)
+            self._sig_src = torch.zeros(1024, dtype=torch.int32, pin_memory=True)
+            self._sig_stream = torch.cuda.Stream(device=dev)
+        self._pinned_off.copy_(offsets, non_blocking=True)
+        self._off_ready.record()
+        slot = self._flag_slot = (self._flag_slot + 1) % 1024
+        self._flags[(slot + 512) % 1024].zero_()
+        flag = self._flags[slot:slot + 1]
+        stop_dev = m.run_experts(layer, xp, offsets, perm, st.y, 0, E, preempt_flag=flag)
+        self.stats["expert_launches"] += 1
+        self._off_ready.synchronize()  # waits for the permute only; the GEMM keeps running
+        off = self._pinned_off.tolist()
+        for e in range(E):
+            n = off[e + 1] - off[e]
+            if n == 0:
+                continue
+            self._charge(self.cost.expert_cost(n))
+            if self._on_report(batch, st, layer, e, on_report) is PREEMPT:
+                # raise "stop at the first boundary >= e+1" while the kernel runs: an async H2D
+                # write on a side stream (copy engine), so expert e always completes
+                self._sig_src[slot] = e + 1
+                with torch.cuda.stream(self._sig_stream):
+                    flag.copy_(self._sig_src[slot:slot + 1], non_blocking=True)
+                return stop_dev, True
+        return stop_dev, False
+
+    def _on_report(self, batch, st, layer, expert, on_report):
+        return on_report(self._report(batch, Stage.EXPERTS, layer, st, expert_id=expert))
+
     def _init_state(self, sequences: list[Sequence]) -> _State:
         members, row = [], 0
         inputs = []

@@ -147,7 +147,7 @@ def expert_ffn(variant: int, xp: torch.Tensor, offsets: torch.Tensor, perm: torc
     if preempt_flag is not None and preempt_flag.dtype != torch.int32:
         raise ValueError("preempt_flag must be int32")
     lib = _lib.load()
-    nbytes = lib.qmoe_expert_ffn_workspace_bytes()
+    nbytes = lib.qmoe_expert_ffn_workspace_bytes(variant, _code(xp), d, xp.shape[0])
     ws = workspace(nbytes, "ffn", xp.device)
     check(lib.qmoe_expert_ffn(variant, _code(xp), _ptr(xp), _ptr(offsets), _ptr(perm), E, d, F, _ptr(w1), _ptr(w2),
                               e_begin, e_end, xp.shape[0], _ptr(act_ws), _ptr(y), _ptr(preempt_flag),

@@ -186,9 +186,7 @@ class DecoderMoEModel:
         return y, torch.zeros(T, dtype=torch.int32, device=self.device)
 
     def permute(self, ids, cursor, x):
-        perm, offsets, xp = K.permute(ids, self.cfg.num_experts, cursor=cursor, x=x)
-        off = offsets.tolist()
-        return perm, offsets, xp, [off[e + 1] - off[e] for e in range(self.cfg.num_experts)]
+        return K.permute(ids, self.cfg.num_experts, cursor=cursor, x=x)
 
     def run_experts(self, layer: int, xp, offsets, perm, y, e_begin: int, e_end: int, preempt_flag=None):
         L = self.layers[layer]

@@ -195,9 +195,7 @@ class MoEModel:
         return y, cursor
 
     def permute(self, ids: torch.Tensor, cursor: torch.Tensor, x: torch.Tensor):
-        perm, offsets, xp = K.permute(ids, self.config.num_experts, cursor=cursor, x=x)
-        off = offsets.tolist()  # the one small D2H per layer: per-expert queue lengths
-        return perm, offsets, xp, [off[e + 1] - off[e] for e in range(self.config.num_experts)]
+        return K.permute(ids, self.config.num_experts, cursor=cursor, x=x)
 
     def run_experts(self, layer: int, xp, offsets, perm, y, e_begin: int, e_end: int,
                     preempt_flag: Optional[torch.Tensor] = None) -> torch.Tensor:

@@ -1,0 +1,59 @@
+"""Wall-clock serving runs (QLLM vs FCFS on the same kernels) and their summary metrics.
+
+Used by tools/serve.py (rate sweeps) and bench.py (the LS TTFT / BE tokens/s half of the
+headline metric).  The trace is the paper workload (reference workload.py defaults, Poisson
+arrivals, 20% LS) seeded per rate exactly like the reference runner (cli.py:172-190)."""
+
+from __future__ import annotations
+
+import time
+from dataclasses import replace
+from typing import Optional
+
+import torch
+
+from .engine import WallClock
+from .metrics import aggregate
+from .sim import Simulation
+from .workload import WorkloadSpec, trace_for_rate
+
+
+def serve_once(model, trace, scheduler: str, max_batch_size: int = 32, slo_ms: float = 3000.0) -> dict:
+    torch.cuda.synchronize()
+    sim = Simulation(trace, model=model, scheduler=scheduler, max_batch_size=max_batch_size, clock=WallClock())
+    t0 = time.perf_counter()
+    res = sim.run()
+    wall = time.perf_counter() - t0
+    rep = aggregate(res.records, slo_ms, res.makespan_ms)
+    dec = sorted(r.duration_ms for r in res.probes.iterations if not r.preempted and r.phase.name == "DECODE")
+    ls, be = rep.ls, rep.be
+    out = {
+        "scheduler": scheduler, "jobs": rep.jobs, "makespan_ms": res.makespan_ms, "wall_s": wall,
+        "ls_jobs": ls.jobs if ls else 0,
+        "ls_ttft_p50_ms": ls.median_ttft_ms if ls else None, "ls_ttft_p99_ms": ls.p99_ttft_ms if ls else None,
+        "ls_mean_turnaround_ms": ls.mean_turnaround_ms if ls else None,
+        "ls_slo_attainment": ls.slo_attainment if ls else None,
+        "be_ttft_p50_ms": be.median_ttft_ms if be else None,
+        "be_mean_turnaround_ms": be.mean_turnaround_ms if be else None,
+        "be_tokens_per_s": rep.be_tokens_per_s, "ls_tokens_per_s": rep.ls_tokens_per_s,
+        "completion_rate_jps": rep.completion_rate_jps, "preemptions": res.probes.preemptions,
+        "decode_iter_ms_median": dec[len(dec) // 2] if dec else None,
+        "engine": res.engine_stats,
+    }
+    del sim, res
+    return out
+
+
+def warm_up(model, max_batch_size: int = 32) -> None:
+    """Short run through prefill, decode and preemption so later timings exclude one-time init."""
+    warm = trace_for_rate(WorkloadSpec(duration_s=2.0, prompt_mean=64, output_mean=8), 4.0, seed=99)
+    serve_once(model, warm, "qllm", max_batch_size)
+
+
+def compare(model, rate: float, duration_s: float, seed: int = 0, max_batch_size: int = 32,
+            slo_ms: float = 3000.0, schedulers=("baseline", "qllm"), workload: Optional[WorkloadSpec] = None) -> dict:
+    trace = trace_for_rate(replace(workload or WorkloadSpec(), duration_s=duration_s), rate, seed=seed)
+    out = {"rate": rate, "duration_s": duration_s, "jobs": len(trace), "slo_ms": slo_ms}
+    for s in schedulers:
+        out["fcfs" if s == "baseline" else s] = serve_once(model, trace, s, max_batch_size, slo_ms)
+    return out

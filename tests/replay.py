@@ -87,7 +87,7 @@ class ReplayModel:
         counts = torch.bincount(flat[pend], minlength=E)[:E].tolist()
         perm = order[: int(pend.sum())].to(torch.int32)
         offsets = torch.tensor([0] + list(torch.tensor(counts).cumsum(0).tolist()), dtype=torch.int32)
-        return perm, offsets, None, counts
+        return perm, offsets, None
 
     def run_experts(self, layer, xp, offsets, perm, y, e_begin, e_end, preempt_flag=None):
         return torch.tensor([e_end], dtype=torch.int32)

@@ -222,3 +222,20 @@ def test_reference_plugin_api_matches_oracle(cuda):
     assert m.emit_token(np.zeros(4)) == int(np.argmax(p.b_out))
     with pytest.raises(Exception):
         m.combine(h, r, {0: outs[0]}, {1})
+
+
+@pytest.mark.parametrize("name", ["random0_qllm", "random4_qllm", "random7_qllm"])
+def test_device_flag_preemption_is_transparent_in_wall_clock_mode(cuda, name):
+    """Wall-clock runs launch every expert at once and preempt through the device flag (the
+    kernel stops at the next expert boundary, cursors advance from cursor_out on the device).
+    Schedules differ from the virtual run, but every sequence's tokens must still equal the
+    reference's (preemption transparency, reference tests/test_sim.py:40-52)."""
+    from paper_2503_09304_b200.engine import WallClock
+
+    rec = load_log(name)
+    sim = Simulation(trace_of(rec), model_config=ModelConfig(**rec["model"]), scheduler="qllm",
+                     max_batch_size=rec["max_batch_size"], policy=policy_for(rec), clock=WallClock())
+    assert sim.engine._device_preempt
+    res = sim.run()
+    assert res.probes.preemptions > 0
+    assert {str(k): s.generated for k, s in sorted(res.sequences.items())} == rec["tokens"]

