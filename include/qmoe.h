@@ -168,6 +168,19 @@ QMOE_API int qmoe_kv_append(void* pool, const int32_t* slot_mapping, const void*
 QMOE_API int qmoe_kv_gather(const void* pool, const int32_t* slot_mapping, int n_rows, size_t row_bytes,
                    void* dst, void* stream);
 
+/*
+ * Decoder-side fused helpers (outside the north-star path; used by the Mixtral/Qwen serving
+ * plugin to cut per-layer launch counts).  bf16 only.
+ * qmoe_rmsnorm: out = rmsnorm(x [+ residual_add]) * weight (HF MixtralRMSNorm rounding);
+ *               when residual_add is given, sum_out = x + residual_add (bf16) is written too.
+ * qmoe_rope:    in-place rotate-half RoPE of q [T, n_heads, hd] and k [T, n_kv_heads, hd] (row
+ *               strides q_stride / k_stride elements) at positions[T], cos/sin tables fp32 [P, hd].
+ */
+QMOE_API int qmoe_rmsnorm(const void* x, const void* residual_add, const void* weight, float eps, int T, int d,
+                          void* out, void* sum_out, void* stream);
+QMOE_API int qmoe_rope(void* q, void* k, const int64_t* positions, const float* cos_table, const float* sin_table,
+                       int T, int n_heads, int n_kv_heads, int head_dim, int q_stride, int k_stride, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

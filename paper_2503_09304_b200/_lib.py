@@ -55,6 +55,8 @@ SIGNATURES = {
     "qmoe_cursor_advance": (_c_int, [_vp, _c_int, _vp, _vp]),
     "qmoe_kv_append": (_c_int, [_vp, _vp, _vp, _c_int, _c_size, _vp]),
     "qmoe_kv_gather": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),
+    "qmoe_rmsnorm": (_c_int, [_vp, _vp, _vp, ctypes.c_float, _c_int, _c_int, _vp, _vp, _vp]),
+    "qmoe_rope": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

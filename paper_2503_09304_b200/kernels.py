@@ -231,3 +231,33 @@ def kv_gather(pool: torch.Tensor, slot_mapping: torch.Tensor, out: torch.Tensor)
     lib = _lib.load()
     check(lib.qmoe_kv_gather(_ptr(pool), _ptr(slot_mapping), n, row_bytes, _ptr(out), _stream()), "qmoe_kv_gather")
     return out
+
+
+def rmsnorm(x: torch.Tensor, weight: torch.Tensor, eps: float, add: Optional[torch.Tensor] = None):
+    """rmsnorm(x [+ add]) * weight in one launch (bf16).  Returns out, or (out, x + add)."""
+    _need(x, "x", torch.bfloat16)
+    _need(weight, "weight", torch.bfloat16)
+    T, d = x.shape
+    out = torch.empty_like(x)
+    summed = None
+    if add is not None:
+        _need(add, "add", torch.bfloat16)
+        summed = torch.empty_like(x)
+    lib = _lib.load()
+    check(lib.qmoe_rmsnorm(_ptr(x), _ptr(add), _ptr(weight), float(eps), T, d, _ptr(out), _ptr(summed), _stream()),
+          "qmoe_rmsnorm")
+    return out if add is None else (out, summed)
+
+
+def rope_(qkv: torch.Tensor, positions: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, n_heads: int,
+          n_kv_heads: int, head_dim: int) -> None:
+    """In-place RoPE on the q and k parts of a packed [T, (H + 2*KV) * hd] qkv projection."""
+    _need(qkv, "qkv", torch.bfloat16)
+    _need(positions, "positions", torch.int64)
+    _need(cos, "cos", torch.float32)
+    _need(sin, "sin", torch.float32)
+    T, width = qkv.shape
+    k_ptr = qkv.data_ptr() + n_heads * head_dim * qkv.element_size()
+    lib = _lib.load()
+    check(lib.qmoe_rope(_ptr(qkv), k_ptr, _ptr(positions), _ptr(cos), _ptr(sin), T, n_heads, n_kv_heads, head_dim,
+                        width, width, _stream()), "qmoe_rope")

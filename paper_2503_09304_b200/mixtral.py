@@ -133,11 +133,8 @@ class DecoderMoEModel:
         cfg, L = self.cfg, self.layers[layer]
         H, KV, hd = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
         T = h.shape[0]
-        x = rms_norm(h, L.ln1, cfg.rms_eps)
+        x = K.rmsnorm(h, L.ln1, cfg.rms_eps)
         qkv = x @ L.w_qkv.T
-        q = qkv[:, : H * hd].view(T, H, hd)
-        k = qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd)
-        v = qkv[:, (H + KV) * hd:].view(T, KV, hd)
         # Per-iteration metadata (positions, slot mapping, block table, lengths) is identical in
         # every layer of a decode/prefill pass, so it is built once and reused across layers.
         key = tuple((m.seq.cache_handle, cache.count(m.seq.cache_handle, layer), m.n) for m in members)
@@ -166,7 +163,10 @@ class DecoderMoEModel:
                 meta["cu"] = torch.tensor(cu, dtype=torch.int32, device=self.device)
                 meta["max"] = max(n for (_, _, n) in key)
             self._meta, self._meta_key = meta, key
-        q, k = self._rope(q, meta["pos"]), self._rope(k, meta["pos"])
+        K.rope_(qkv, meta["pos"], self._cos, self._sin, H, KV, hd)
+        q = qkv[:, : H * hd].view(T, H, hd)
+        k = qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd)
+        v = qkv[:, (H + KV) * hd:].view(T, KV, hd)
         cache.scatter(layer, meta["slots"], torch.stack([k, v], 1))
         if decode:
             pool = cache.pool(layer)
@@ -175,8 +175,8 @@ class DecoderMoEModel:
         else:
             attn = self._fa_varlen(q, k, v, meta["cu"], meta["cu"], meta["max"], meta["max"],
                                    causal=True).reshape(T, H * hd)
-        h2 = h + attn @ L.w_o.T
-        return rms_norm(h2, L.ln2, cfg.rms_eps).contiguous(), h2.contiguous()
+        x_in, h2 = K.rmsnorm(attn @ L.w_o.T, L.ln2, cfg.rms_eps, add=h)  # h2 = h + o, x_in = norm2(h2)
+        return x_in, h2
 
     def route_batch(self, layer: int, x: torch.Tensor):
         return K.router(x, self.layers[layer].w_router, self.cfg.top_k, self.cfg.route_mode)
@@ -216,7 +216,7 @@ class DecoderMoEModel:
 
     def emit_batch(self, h: torch.Tensor, rows: list[int]) -> list[int]:
         hl = h.index_select(0, torch.tensor(rows, dtype=torch.long, device=self.device))
-        logits = (rms_norm(hl, self.final_norm, self.cfg.rms_eps) @ self.lm_head.T).float()
+        logits = (K.rmsnorm(hl.contiguous(), self.final_norm, self.cfg.rms_eps) @ self.lm_head.T).float()
         return torch.argmax(logits, dim=1).tolist()  # first maximal index: ties to the lowest id
 
     @staticmethod
