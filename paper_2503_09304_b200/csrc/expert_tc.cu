@@ -16,6 +16,8 @@
 // The TMEM double buffer lets the epilogue of tile i overlap the MMAs of tile i+1.
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "expert_common.cuh"
@@ -41,6 +43,7 @@ constexpr int kSplitRowsMax = 512;
 }  // namespace
 int down_splits(int xp_rows, int n_experts, int d, int F);
 float* splitk_buffer(FfnWorkspace* ws);
+bool use_cta_pair(int xp_rows);
 namespace {
 
 struct TcParams {
@@ -296,6 +299,209 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
   }
 }
 
+
+// ================================================================================================
+// CTA-pair variant (cta_group::2) for large batches: one M=256 x N=256 tile per CTA pair.  Each
+// CTA stages its 128 rows of A and its 128 rows of B (gate_up: CTA0 the gate rows, CTA1 the up
+// rows), so per-SM operand traffic per MMA drops by a third versus the 1-CTA kernel.  The leader
+// (cluster rank 0) claims tiles and publishes them to both CTAs' tile rings over DSMEM; both
+// CTAs' TMA loads complete on the leader's full barrier; the leader alone issues
+// tcgen05.mma.cta_group::2 and its commits multicast to both CTAs' smem-empty / TMEM-full
+// barriers; both CTAs' epilogue warps release the accumulator on the leader's TMEM-empty barrier.
+constexpr int kStages2 = 6;
+constexpr int kBM2 = 256;  // rows per pair tile (128 per CTA)
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+  constexpr int BN = 256;
+  constexpr int BN_OUT = (EPI == EPI_SWIGLU) ? BN / 2 : BN;
+  constexpr int kHalfA = 128 * BK * 2;         // 16 KB: this CTA's A rows
+  constexpr int kHalfB = (BN / 2) * BK * 2;    // 16 KB: this CTA's B rows
+  constexpr int kStageBytes = kHalfA + kHalfB;
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kBM2, BN);
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStages2], empty_bar[kStages2];
+  __shared__ __align__(8) uint64_t tfull_bar[kAccStages], tempty_bar[kAccStages];
+  __shared__ __align__(8) uint64_t ring_full[kTileRing], ring_empty[kTileRing];
+  __shared__ int ring_tile[kTileRing];
+  __shared__ uint32_t tmem_base_smem;
+  __shared__ TileMap map;
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int n_tiles_n = (p.N + BN_OUT - 1) / BN_OUT;
+  const int nkb = (p.K + BK - 1) / BK;
+
+  if (warp == 0) build_tile_map(map, p.offsets, p.e_begin, p.e_end, p.e_limit, kBM2, n_tiles_n);
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < kStages2; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < kAccStages; ++a) {
+      ptx::mbar_init(&tfull_bar[a], 1);
+      ptx::mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    for (int i = 0; i < kTileRing; ++i) {
+      ptx::mbar_init(&ring_full[i], 1);
+      ptx::mbar_init(&ring_empty[i], 10);  // leader: MMA + 4 epi; peer: producer + 4 epi
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_cg2<2 * BN>(&tmem_base_smem);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = tmem_base_smem;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmA);
+      ptx::tma_prefetch_desc(&tmB);
+      int stage = 0, slot = 0, last_e = -1;
+      uint32_t phase = 0, rphase = 0;
+      while (true) {
+        int tile;
+        if (leader) {
+          tile = ffn_claim(map, p.ws, p.flag, last_e);
+          ptx::mbar_wait_cluster(&ring_empty[slot], rphase ^ 1);
+          ring_tile[slot] = tile;
+          ptx::st_remote_u32(&ring_tile[slot], 1, (uint32_t)tile);
+          ptx::mbar_arrive(&ring_full[slot]);
+          ptx::mbar_arrive_remote(&ring_full[slot], 1);
+        } else {
+          ptx::mbar_wait_cluster(&ring_full[slot], rphase);
+          tile = ring_tile[slot];
+          ptx::mbar_arrive_remote(&ring_empty[slot], 0);
+        }
+        if (++slot == kTileRing) { slot = 0; rphase ^= 1; }
+        if (tile < 0) break;
+        int e, m0, n0;
+        map.locate(tile, kBM2, n_tiles_n, BN_OUT, e, m0, n0);
+        const int arow = m0 + (int)rank * 128;
+        // B rows of this CTA: gate_up -> CTA0 gate [n0, +128), CTA1 up F + [n0, +128);
+        // plain -> rows n0 + rank*128 of expert e.
+        const int brow = (EPI == EPI_SWIGLU) ? e * p.b_rows + (rank ? p.N : 0) + n0 : e * p.b_rows + n0 + (int)rank * 128;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait_cluster(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          uint8_t* sb = sa + kHalfA;
+          if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
+          ptx::tma_load_2d_cg2(&tmA, &full_bar[stage], sa, kb * BK, arow, ptx::kEvictNormal);
+          ptx::tma_load_2d_cg2(&tmB, &full_bar[stage], sb, kb * BK, brow, ptx::kEvictNormal);
+          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      int stage = 0, slot = 0, acc = 0;
+      uint32_t phase = 0, rphase = 0, aphase = 0;
+      while (true) {
+        ptx::mbar_wait_cluster(&ring_full[slot], rphase);
+        const int tile = ring_tile[slot];
+        ptx::mbar_arrive(&ring_empty[slot]);
+        if (++slot == kTileRing) { slot = 0; rphase ^= 1; }
+        if (tile < 0) break;
+        ptx::mbar_wait_cluster(&tempty_bar[acc], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem + stage * kStageBytes);
+          const uint32_t b_addr = a_addr + kHalfA;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            ptx::tc_mma_bf16_cg2(d_tmem, ptx::sw128_kmajor_desc(a_addr + k * 32), ptx::sw128_kmajor_desc(b_addr + k * 32),
+                                 kIdesc, (kb | k) != 0);
+          ptx::tc_commit_cg2(&empty_bar[stage], 0x3);  // both CTAs' smem slots free
+          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+        }
+        ptx::tc_commit_cg2(&tfull_bar[acc], 0x3);  // both CTAs' accumulators ready
+        if (++acc == kAccStages) { acc = 0; aphase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------------------------ epilogue (both CTAs)
+    const int ew = warp - kEpiWarp0;
+    int slot = 0, acc = 0;
+    uint32_t rphase = 0, aphase = 0;
+    while (true) {
+      ptx::mbar_wait_cluster(&ring_full[slot], rphase);
+      const int tile = ring_tile[slot];
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&ring_empty[slot]);
+        else ptx::mbar_arrive_remote(&ring_empty[slot], 0);
+      }
+      if (++slot == kTileRing) { slot = 0; rphase ^= 1; }
+      if (tile < 0) break;
+      int e, m0, n0;
+      map.locate(tile, kBM2, n_tiles_n, BN_OUT, e, m0, n0);
+      const int row = m0 + (int)rank * 128 + ew * 32 + lane;
+      const bool valid = row < p.offsets[e + 1];
+      __nv_bfloat16* dst_row = nullptr;
+      if (valid) {
+        const size_t orow = (EPI == EPI_SWIGLU) ? (size_t)row : (size_t)p.perm[row];
+        dst_row = p.out + orow * p.out_ld;
+      }
+      ptx::mbar_wait_cluster(&tfull_bar[acc], aphase);
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN_OUT; c += 32) {
+        uint32_t v[32];
+        ptx::tmem_ld32(t_row + c, v);
+        uint32_t packed[16];
+        if constexpr (EPI == EPI_SWIGLU) {
+          uint32_t u[32];
+          ptx::tmem_ld32(t_row + BN / 2 + c, u);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float g0 = __uint_as_float(v[2 * i]), g1 = __uint_as_float(v[2 * i + 1]);
+            const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+            packed[i] = pack_bf16(g0 / (1.f + __expf(-g0)) * u0, g1 / (1.f + __expf(-g1)) * u1);
+          }
+        } else {
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        }
+        if (valid && n0 + c < p.N) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst_row + n0 + c);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            d4[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&tempty_bar[acc]);
+        else ptx::mbar_arrive_remote(&tempty_bar[acc], 0);
+      }
+      if (++acc == kAccStages) { acc = 0; aphase ^= 1; }
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg2<2 * BN>(tmem_base);
+  }
+}
+
+constexpr int smem_bytes2() { return kStages2 * (128 * BK * 2 + 128 * BK * 2) + 1024; }
+
 // ---- host side --------------------------------------------------------------------------
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -357,6 +563,17 @@ int launch_tc(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cud
   return check_launch("qmoe_expert_ffn(tcgen05)");
 }
 
+template <int EPI>
+int launch_tc2(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_tc2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes2()));
+    attr_set = true;
+  }
+  ffn_tc2_kernel<EPI><<<(g_num_sms / 2) * 2, kThreads, smem_bytes2(), s>>>(a, b, p);
+  return check_launch("qmoe_expert_ffn(tcgen05 cta pair)");
+}
+
 }  // namespace
 
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
@@ -392,7 +609,8 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   p.N = F; p.K = d; p.b_rows = 2 * F;
   p.out = (__nv_bfloat16*)act_ws; p.out_ld = F;
   p.ws = ws + 0;
-  if ((st = launch_tc<BN, EPI_SWIGLU>(ta, tb, p, s))) return st;
+  const bool pair = use_cta_pair(xp_rows);
+  if ((st = pair ? launch_tc2<EPI_SWIGLU>(ta, tb, p, s) : launch_tc<BN, EPI_SWIGLU>(ta, tb, p, s))) return st;
   if ((st = ffn_finalize(ws + 0, nullptr, e_end, nullptr, s))) return st;
   // down: Y[perm[r], :d] = act[r] W2^T, only experts whose gate_up completed
   CUtensorMap ta2, tb2;
@@ -417,8 +635,19 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
     return check_launch("qmoe_expert_ffn(split-K reduce)");
   }
   p2.nsplit = 1;
-  if ((st = launch_tc<BN, EPI_DOWN>(ta2, tb2, p2, s))) return st;
+  if ((st = pair ? launch_tc2<EPI_DOWN>(ta2, tb2, p2, s) : launch_tc<BN, EPI_DOWN>(ta2, tb2, p2, s))) return st;
   return ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s);
+}
+
+// Large batches (many 256-row tiles per expert) use the CTA-pair kernel; QMOE_CTA_PAIR=0/1
+// forces either path (tests compare them).
+bool use_cta_pair(int xp_rows) {
+  static int forced = [] {
+    const char* v = getenv("QMOE_CTA_PAIR");
+    return v == nullptr ? -1 : atoi(v);
+  }();
+  if (forced >= 0) return forced == 1 && xp_rows > kSplitRowsMax;
+  return xp_rows >= 4096;
 }
 
 int down_splits(int xp_rows, int n_experts, int d, int F) {
