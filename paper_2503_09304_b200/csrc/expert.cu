@@ -15,7 +15,7 @@ __global__ void ffn_finalize_kernel(FfnWorkspace* ws, const int32_t* limit, int 
 }  // namespace
 
 int ffn_ws_reset(FfnWorkspace* ws, cudaStream_t s) {
-  QMOE_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(FfnWorkspace) * kFfnWorkspaceSlots, s));
+  QMOE_CUDA_TRY(cudaMemsetAsync(ws, 0, kFfnHeaderBytes, s));
   return QMOE_OK;
 }
 
@@ -27,7 +27,7 @@ int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cur
 }  // namespace qmoe
 
 extern "C" size_t qmoe_expert_ffn_workspace_bytes(int variant, int dtype, int d, int xp_rows) {
-  size_t n = sizeof(qmoe::FfnWorkspace) * qmoe::kFfnWorkspaceSlots;
+  size_t n = qmoe::kFfnHeaderBytes;
   if (variant == QMOE_EXPERT_SWIGLU && dtype == QMOE_BF16) n += qmoe::splitk_bytes(xp_rows, d);
   return n;
 }

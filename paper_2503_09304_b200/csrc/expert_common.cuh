@@ -14,6 +14,8 @@
 
 #include <limits.h>
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace qmoe {
@@ -26,6 +28,11 @@ struct alignas(128) FfnWorkspace {
 };
 
 constexpr int kFfnWorkspaceSlots = 2;
+// Workspace header: kFfnWorkspaceSlots claim slots, then one completion counter per expert (the
+// fused small-batch kernel's gate_up -> down dependency), then the split-K partials.
+constexpr int kFfnMaxExperts = 64;
+constexpr size_t kFfnHeaderBytes = sizeof(FfnWorkspace) * kFfnWorkspaceSlots + kFfnMaxExperts * sizeof(int);
+__host__ __device__ inline int* ffn_done(FfnWorkspace* ws) { return reinterpret_cast<int*>(ws + kFfnWorkspaceSlots); }
 
 struct TileMap {
   int e_first;              // absolute id of experts[0]
@@ -142,6 +149,18 @@ int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cur
 int expert_ffn_simt(int variant, int dtype, const void* xp, const int32_t* offsets, const int32_t* perm, int E,
                     int d, int F, const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, cudaStream_t s);
+// ---- host helpers of the tcgen05 paths (expert_tc.cu) -----------------------------------
+int tc_init_driver();  // cuTensorMapEncodeTiled entry point + SM count; QMOE_OK or error
+int tc_num_sms();
+// 2D bf16 row-major [rows, cols] -> tensor map with box {64 cols, box_rows}, 128B swizzle.
+int tc_make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// Small-batch path (expert_swap.cu): swap-AB tiles, gate_up and down in one persistent launch.
+bool use_swap_ab(int xp_rows, int n_experts, int d, int F);
+int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
+                    const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
+                    const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
+                    cudaStream_t s);
+
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                   const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int total_rows_hint,

@@ -18,6 +18,8 @@
 
 #include <stdlib.h>
 
+#include <cmath>
+
 #include <mutex>
 
 #include "expert_common.cuh"
@@ -43,7 +45,7 @@ constexpr int kSplitRowsMax = 512;
 }  // namespace
 int down_splits(int xp_rows, int n_experts, int d, int F);
 float* splitk_buffer(FfnWorkspace* ws);
-bool use_cta_pair(int xp_rows);
+bool use_cta_pair(int xp_rows, int n_experts);
 namespace {
 
 struct TcParams {
@@ -551,6 +553,16 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
   return QMOE_OK;
 }
 
+}  // namespace
+
+int tc_init_driver() { return init_driver(); }
+int tc_num_sms() { return g_num_sms; }
+int tc_make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  return make_map(m, base, rows, cols, box_rows);
+}
+
+namespace {
+
 template <int BN, int EPI>
 int launch_tc(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cudaStream_t s) {
   static bool attr_set = false;
@@ -586,6 +598,9 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   QMOE_REQUIRE(variant != QMOE_EXPERT_SWIGLU || F % 64 == 0, "qmoe_expert_ffn(bf16): F must be a multiple of 64");
   QMOE_REQUIRE(((uintptr_t)xp | (uintptr_t)w1 | (uintptr_t)y | (uintptr_t)(act_ws ? act_ws : y)) % 16 == 0,
                "qmoe_expert_ffn(bf16): buffers must be 16-byte aligned");
+  if (variant == QMOE_EXPERT_SWIGLU && use_swap_ab(xp_rows, E, d, F))
+    return expert_ffn_swap(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
+                           xp_rows, s);
   constexpr int BN = 256;
   if ((st = ffn_ws_reset(ws, s))) return st;
   TcParams p{};
@@ -609,7 +624,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   p.N = F; p.K = d; p.b_rows = 2 * F;
   p.out = (__nv_bfloat16*)act_ws; p.out_ld = F;
   p.ws = ws + 0;
-  const bool pair = use_cta_pair(xp_rows);
+  const bool pair = use_cta_pair(xp_rows, e_end - e_begin);
   if ((st = pair ? launch_tc2<EPI_SWIGLU>(ta, tb, p, s) : launch_tc<BN, EPI_SWIGLU>(ta, tb, p, s))) return st;
   if ((st = ffn_finalize(ws + 0, nullptr, e_end, nullptr, s))) return st;
   // down: Y[perm[r], :d] = act[r] W2^T, only experts whose gate_up completed
@@ -639,15 +654,21 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   return ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s);
 }
 
-// Large batches (many 256-row tiles per expert) use the CTA-pair kernel; QMOE_CTA_PAIR=0/1
-// forces either path (tests compare them).
-bool use_cta_pair(int xp_rows) {
+// Large batches use the CTA-pair kernel (M = 256 rows per tile) unless its row padding would
+// cost more than the 1-CTA kernel's (M = 128): with many fine-grained experts (Qwen: 60 experts,
+// ~550 rows each at 8k tokens) a 256-row tile wastes ~30% of the tensor work on padding rows.
+// The host does not know the per-expert counts (they stay on the device), so the padding is
+// estimated from the mean rows per covered expert.  QMOE_CTA_PAIR=0/1 forces either path.
+bool use_cta_pair(int xp_rows, int n_experts) {
   static int forced = [] {
     const char* v = getenv("QMOE_CTA_PAIR");
     return v == nullptr ? -1 : atoi(v);
   }();
   if (forced >= 0) return forced == 1 && xp_rows > kSplitRowsMax;
-  return xp_rows >= 4096;
+  if (xp_rows < 4096) return false;
+  const double r = (double)xp_rows / (n_experts > 0 ? n_experts : 1);
+  auto eff = [r](int m) { return r / (m * std::ceil(r / m)); };
+  return eff(256) >= eff(128) - 0.02;
 }
 
 int down_splits(int xp_rows, int n_experts, int d, int F) {
@@ -669,7 +690,7 @@ size_t splitk_bytes(int xp_rows, int d) {
 }
 
 float* splitk_buffer(FfnWorkspace* ws) {
-  return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + sizeof(FfnWorkspace) * kFfnWorkspaceSlots);
+  return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + kFfnHeaderBytes);
 }
 
 }  // namespace qmoe

@@ -3,12 +3,15 @@
 // Replaces MoEModel.route / route_many (reference model.py:115-134) and select_top_k /
 // softmax_over (model.py:71-80).  HBM-bound on X: each token row is read once; W_router (E x d)
 // stays L1/L2-resident and is reused across the TPC tokens a CTA owns (register blocking).
+#include <algorithm>
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace qmoe {
 namespace {
 
-constexpr int kWarps = 4;      // warps per CTA
+constexpr int kWarps = 8;      // warps per CTA
 constexpr int kExpChunk = 8;   // experts accumulated per pass over d
 constexpr int kMaxE = 64;
 
@@ -44,174 +47,361 @@ template <typename A> __device__ __forceinline__ A warp_sum(A v) {
 __device__ __forceinline__ float exp_acc(float v) { return expf(v); }
 __device__ __forceinline__ double exp_acc(double v) { return exp(v); }
 
-// One CTA owns TPC tokens; its kWarps warps split the hidden dimension (so a decode batch still
-// spreads over many CTAs), every lane keeps TPC x kExpChunk partial dot products in registers,
-// and all loads of one step (TPC token vectors + kExpChunk weight vectors) are issued before any
-// FMA so they are in flight together.  Partials are reduced across lanes (shuffles) and warps
-// (shared memory); then one thread per token does the top-k selection.
+template <typename A>
+__device__ __noinline__ void select_token(const A* lg, A* s_score, int tok, int E, int k, int mode, int lane,
+                                             int32_t* __restrict__ ids_out, A* __restrict__ w_out,
+                                             A* __restrict__ logits_out) {
+  const bool ok0 = lane < E, ok1 = lane + 32 < E;
+  const A l0 = ok0 ? lg[lane] : A(0), l1 = ok1 ? lg[lane + 32] : A(0);
+  if (logits_out != nullptr) {
+    if (ok0) logits_out[(size_t)tok * E + lane] = l0;
+    if (ok1) logits_out[(size_t)tok * E + lane + 32] = l1;
+  }
+  A s0 = l0, s1 = l1;  // value the top-k ranks on
+  if (mode == QMOE_ROUTE_SOFTMAX_TOPK) {
+    A m = ok0 ? l0 : l1;
+    if (ok1 && l1 > m) m = l1;
+    for (int o = 16; o > 0; o >>= 1) {
+      const A v = __shfl_xor_sync(0xffffffffu, m, o);
+      m = v > m ? v : m;
+    }
+    // lanes >= E contribute nothing; E >= 1 so lane 0 always holds a real expert
+    const A z0 = ok0 ? exp_acc(l0 - m) : A(0), z1 = ok1 ? exp_acc(l1 - m) : A(0);
+    const A tot = warp_sum(z0 + z1);
+    s0 = z0 / tot;
+    s1 = z1 / tot;
+    if (ok0) s_score[lane] = s0;
+    if (ok1) s_score[lane + 32] = s1;
+  }
+  // top-k by (score desc, id asc): k warp-wide argmax rounds (model.py:74 sorts by (-value, id)).
+  bool c0 = !ok0, c1 = !ok1;  // "taken" (or not an expert)
+#pragma unroll 1
+  for (int r = 0; r < k; ++r) {
+    int bid = -1;
+    A bv = A(0);
+    if (!c0) { bid = lane; bv = s0; }
+    if (!c1 && (bid < 0 || s1 > bv)) { bid = lane + 32; bv = s1; }
+    for (int o = 16; o > 0; o >>= 1) {
+      const A ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
+      if (oid >= 0 && (bid < 0 || ov > bv || (ov == bv && oid < bid))) { bv = ov; bid = oid; }
+    }
+    if (bid == lane) c0 = true;
+    if (bid == lane + 32) c1 = true;
+  }
+  const unsigned lo = __ballot_sync(0xffffffffu, ok0 && c0), hi = __ballot_sync(0xffffffffu, ok1 && c1);
+  if (lane != 0) return;
+  uint64_t chosen = (uint64_t)lo | ((uint64_t)hi << 32);
+  // ids ascending (model.py:75 / :129), weights in the same order.
+  int pick[8];
+  for (int j = 0; j < k; ++j) {
+    pick[j] = __ffsll((long long)chosen) - 1;
+    chosen &= chosen - 1;
+  }
+  A wv[8];
+  if (mode == QMOE_ROUTE_SOFTMAX_TOPK) {
+    for (int j = 0; j < k; ++j) wv[j] = s_score[pick[j]];
+  } else {
+    // softmax over the picked logits, summed in ascending id order (model.py:78-80)
+    A m = lg[pick[0]];
+    for (int j = 1; j < k; ++j) m = lg[pick[j]] > m ? lg[pick[j]] : m;
+    A tot = A(0);
+    for (int j = 0; j < k; ++j) {
+      wv[j] = exp_acc(lg[pick[j]] - m);
+      tot += wv[j];
+    }
+    for (int j = 0; j < k; ++j) wv[j] = wv[j] / tot;
+  }
+  for (int j = 0; j < k; ++j) {
+    ids_out[(size_t)tok * k + j] = pick[j];
+    w_out[(size_t)tok * k + j] = wv[j];
+  }
+}
+
+// One CTA owns TPC tokens, split into TPC/TPW groups of TPW tokens; each group gets kWarps/groups
+// warps laid out as (d slice) x (8-expert chunk).  Decode (TPC = 1): with few experts (Mixtral's 8)
+// all 8 warps split d, with many (Qwen's 60) each warp owns one chunk over the whole of d, so a
+// small batch still spreads over many warps.  Large batches: a warp owns TPW tokens over all of d
+// (few shuffles per byte of X, HBM-bound on X).  Every lane keeps TPW x kExpChunk partial dot
+// products in registers and issues all loads of a step (TPW token vectors + kExpChunk weight
+// vectors) before any FMA.  Partials are reduced across lanes (shuffles) and d slices (shared
+// memory, fixed slice order); then one warp per token does the selection with warp-wide argmax
+// rounds.  Requires ceil(E/8) <= warps per group (checked by the host dispatch).
 // VEC: true -> 16-byte vector loads (requires d % Vec<T>::N == 0 and aligned rows).
-template <typename T, int TPC, bool VEC>
+template <typename T, int TPC, int TPW, bool VEC>
 __global__ void __launch_bounds__(kWarps * 32)
 router_kernel(const T* __restrict__ x, const T* __restrict__ wr, int ntok, int d, int E, int k,
               int mode, int32_t* __restrict__ ids_out, typename AccOf<T>::type* __restrict__ w_out,
-              typename AccOf<T>::type* __restrict__ logits_out) {
+              typename AccOf<T>::type* __restrict__ logits_out, int rounds) {
   using A = typename AccOf<T>::type;
-  __shared__ A s_part[kWarps][TPC][kExpChunk];
+  constexpr int kGroups = TPC / TPW;
+  constexpr int kWpg = kWarps / kGroups;  // warps per token group
+  static_assert(kGroups * TPW == TPC && kWpg * kGroups == kWarps, "bad router tiling");
+  __shared__ A s_part[kWpg][TPC][kMaxE];
   __shared__ A s_logit[TPC][kMaxE];
+  __shared__ A s_score[TPC][kMaxE];
   const int warp = warp_id(), lane = lane_id();
-  const int tok0 = blockIdx.x * TPC;
   constexpr int N = VEC ? Vec<T>::N : 1;
-  // d range of this warp, in units of N elements
   const int nvec = d / N;
-  const int per_warp = (nvec + kWarps - 1) / kWarps;
-  const int v0 = warp * per_warp, v1 = min(nvec, v0 + per_warp);
-
-  // Few experts (E <= 16): the warps split d and every warp covers all experts.  Many experts
-  // (Qwen: 60): the warps take 8-expert chunks in parallel over the full d (no serial chunk loop).
-  const bool split_d = E <= 2 * kExpChunk;
-  const int c_begin = split_d ? 0 : warp * kExpChunk;
-  const int c_step = split_d ? kExpChunk : kWarps * kExpChunk;
-  const int w_v0 = split_d ? v0 : 0, w_v1 = split_d ? v1 : nvec;
-  for (int ec = c_begin; ec < E; ec += c_step) {
-    A acc[TPC][kExpChunk];
+  const int nchunk = (E + kExpChunk - 1) / kExpChunk;  // <= kWpg
+  const int dsplit = kWpg / nchunk;                     // >= 1
+  const int group = warp / kWpg, wig = warp % kWpg;
+  const int chunk = wig % nchunk, slice = wig / nchunk;
+  // `rounds` batches of TPC tokens per CTA: with many experts W_router (Qwen: 245 KB) is then
+  // re-read from L1 instead of from L2 for every 4 tokens.
+  for (int rnd = 0; rnd < rounds; ++rnd) {
+  const int tok0 = (blockIdx.x * rounds + rnd) * TPC;
+  if (tok0 >= ntok) break;
+  if (slice < dsplit) {
+    const int per = (nvec + dsplit - 1) / dsplit;
+    const int v0 = slice * per, v1 = min(nvec, v0 + per);
+    const int ec = chunk * kExpChunk;
+    const int gt0 = group * TPW;  // first token of this group within the CTA
+    A acc[TPW][kExpChunk];
 #pragma unroll
-    for (int t = 0; t < TPC; ++t)
+    for (int t = 0; t < TPW; ++t)
 #pragma unroll
       for (int j = 0; j < kExpChunk; ++j) acc[t][j] = A(0);
     const T* wrow[kExpChunk];
 #pragma unroll
     for (int j = 0; j < kExpChunk; ++j) wrow[j] = wr + (size_t)min(ec + j, E - 1) * d;  // clamp: no branch
-    const T* xrow[TPC];
+    const T* xrow[TPW];
 #pragma unroll
-    for (int t = 0; t < TPC; ++t) xrow[t] = x + (size_t)min(tok0 + t, ntok - 1) * d;
+    for (int t = 0; t < TPW; ++t) xrow[t] = x + (size_t)min(tok0 + gt0 + t, ntok - 1) * d;
 
-    for (int v = w_v0 + lane; v < w_v1; v += 32) {
-      A xv[TPC][N], wv[kExpChunk][N];
+#pragma unroll 2
+    for (int v = v0 + lane; v < v1; v += 32) {
+      A xv[TPW][N], wv[kExpChunk][N];
       if constexpr (VEC) {
         using U = typename Vec<T>::U;
-        U xu[TPC], wu[kExpChunk];
+        U xu[TPW], wu[kExpChunk];
 #pragma unroll
-        for (int t = 0; t < TPC; ++t) xu[t] = *reinterpret_cast<const U*>(xrow[t] + (size_t)v * N);
+        for (int t = 0; t < TPW; ++t) xu[t] = *reinterpret_cast<const U*>(xrow[t] + (size_t)v * N);
 #pragma unroll
         for (int j = 0; j < kExpChunk; ++j) wu[j] = __ldg(reinterpret_cast<const U*>(wrow[j] + (size_t)v * N));
 #pragma unroll
-        for (int t = 0; t < TPC; ++t) unpack<T, A>(xu[t], xv[t]);
+        for (int t = 0; t < TPW; ++t) unpack<T, A>(xu[t], xv[t]);
 #pragma unroll
         for (int j = 0; j < kExpChunk; ++j) unpack<T, A>(wu[j], wv[j]);
       } else {
 #pragma unroll
-        for (int t = 0; t < TPC; ++t) xv[t][0] = load_as<T, A>(xrow[t] + v);
+        for (int t = 0; t < TPW; ++t) xv[t][0] = load_as<T, A>(xrow[t] + v);
 #pragma unroll
         for (int j = 0; j < kExpChunk; ++j) wv[j][0] = load_as<T, A>(wrow[j] + v);
       }
 #pragma unroll
-      for (int t = 0; t < TPC; ++t)
+      for (int t = 0; t < TPW; ++t)
 #pragma unroll
         for (int j = 0; j < kExpChunk; ++j)
 #pragma unroll
           for (int q = 0; q < N; ++q) acc[t][j] += xv[t][q] * wv[j][q];
     }
-    if (split_d) {
 #pragma unroll
-      for (int t = 0; t < TPC; ++t)
+    for (int t = 0; t < TPW; ++t)
 #pragma unroll
-        for (int j = 0; j < kExpChunk; ++j) {
-          const A sum = warp_sum(acc[t][j]);
-          if (lane == 0) s_part[warp][t][j] = sum;
-        }
-      __syncthreads();
-      if (threadIdx.x < TPC * kExpChunk) {
-        const int t = threadIdx.x / kExpChunk, j = threadIdx.x % kExpChunk;
-        A sum = A(0);
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) sum += s_part[w][t][j];
-        if (ec + j < E) s_logit[t][ec + j] = sum;
+      for (int j = 0; j < kExpChunk; ++j) {
+        const A sum = warp_sum(acc[t][j]);
+        if (lane == 0 && ec + j < E) s_part[slice][gt0 + t][ec + j] = sum;
       }
-      __syncthreads();
-    } else {
-#pragma unroll
-      for (int t = 0; t < TPC; ++t)
-#pragma unroll
-        for (int j = 0; j < kExpChunk; ++j) {
-          const A sum = warp_sum(acc[t][j]);
-          if (lane == 0 && ec + j < E) s_logit[t][ec + j] = sum;
-        }
-    }
   }
-  if (!split_d) __syncthreads();
+  __syncthreads();
+  for (int i = threadIdx.x; i < TPC * E; i += kWarps * 32) {
+    const int t = i / E, e = i - t * E;
+    A sum = s_part[0][t][e];
+    for (int sl = 1; sl < dsplit; ++sl) sum += s_part[sl][t][e];
+    s_logit[t][e] = sum;
+  }
+  __syncthreads();
 
-  // Selection: thread t owns token tok0 + t.
-  if (threadIdx.x < TPC) {
-    const int tok = tok0 + threadIdx.x;
-    if (tok < ntok) {
-      const A* lg = s_logit[threadIdx.x];
-      if (logits_out != nullptr)
-        for (int e = 0; e < E; ++e) logits_out[(size_t)tok * E + e] = lg[e];
-      A score[kMaxE];  // value the top-k ranks on
-      if (mode == QMOE_ROUTE_SOFTMAX_TOPK) {
-        A m_all = lg[0];
-        for (int e = 1; e < E; ++e) m_all = lg[e] > m_all ? lg[e] : m_all;
-        A tot = A(0);
-        for (int e = 0; e < E; ++e) {
-          score[e] = exp_acc(lg[e] - m_all);
-          tot += score[e];
-        }
-        for (int e = 0; e < E; ++e) score[e] = score[e] / tot;
-      } else {
-        for (int e = 0; e < E; ++e) score[e] = lg[e];
-      }
-      // top-k by (score desc, id asc): scanning ascending ids with a strict '>' keeps the lower
-      // id on ties (model.py:74 sorts by (-value, id)).
-      uint64_t chosen = 0;
-      for (int r = 0; r < k; ++r) {
-        int best = -1;
-        A bv = A(0);
-        for (int e = 0; e < E; ++e) {
-          if ((chosen >> e) & 1ull) continue;
-          if (best < 0 || score[e] > bv) { best = e; bv = score[e]; }
-        }
-        chosen |= 1ull << best;
-      }
-      // ids ascending (model.py:75 / :129), weights in the same order.
-      int pick[8];
-      int n = 0;
-      for (int e = 0; e < E; ++e)
-        if ((chosen >> e) & 1ull) pick[n++] = e;
-      A wv[8];
-      if (mode == QMOE_ROUTE_SOFTMAX_TOPK) {
-        for (int j = 0; j < k; ++j) wv[j] = score[pick[j]];
-      } else {
-        A m = lg[pick[0]];
-        for (int j = 1; j < k; ++j) m = lg[pick[j]] > m ? lg[pick[j]] : m;
-        A tot = A(0);
-        for (int j = 0; j < k; ++j) {
-          wv[j] = exp_acc(lg[pick[j]] - m);
-          tot += wv[j];
-        }
-        for (int j = 0; j < k; ++j) wv[j] = wv[j] / tot;
-      }
-      for (int j = 0; j < k; ++j) {
-        ids_out[(size_t)tok * k + j] = pick[j];
-        w_out[(size_t)tok * k + j] = wv[j];
-      }
-    }
+  // Selection: warp w owns tokens tok0 + w, tok0 + w + kWarps, ...; lane l holds experts l, l + 32.
+#pragma unroll 1
+  for (int ti = warp; ti < TPC; ti += kWarps) {
+    const int tok = tok0 + ti;
+    if (tok >= ntok) break;
+    select_token<A>(s_logit[ti], s_score[ti], tok, E, k, mode, lane, ids_out, w_out, logits_out);
+  }
+  __syncthreads();  // s_part / s_logit / s_score are reused by the next round
   }
 }
 
-template <typename T, int TPC>
+
+template <typename T, int TPC, int TPW>
 int launch_router(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids,
                   void* w, void* logits, cudaStream_t s) {
   using A = typename AccOf<T>::type;
-  dim3 grid((T_ + TPC - 1) / TPC);
+  const int nchunk = (E + kExpChunk - 1) / kExpChunk;
+  const int rounds = nchunk > 2 && TPC > 1 ? 8 : 1;
+  dim3 grid((T_ + TPC * rounds - 1) / (TPC * rounds));
   const bool vec = (d % Vec<T>::N == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(wr) % 16 == 0);
   if (vec)
-    router_kernel<T, TPC, true><<<grid, kWarps * 32, 0, s>>>(
-        (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits);
+    router_kernel<T, TPC, TPW, true><<<grid, kWarps * 32, 0, s>>>(
+        (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits, rounds);
   else
-    router_kernel<T, TPC, false><<<grid, kWarps * 32, 0, s>>>(
-        (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits);
+    router_kernel<T, TPC, TPW, false><<<grid, kWarps * 32, 0, s>>>(
+        (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits, rounds);
   return check_launch("qmoe_router");
+}
+
+// ---- bf16, many tokens: the logits as a skinny GEMM on the tensor cores ------------------------
+// [T, d] x [d, E] with E <= 64 is HBM-bound on X (Qwen, T = 8k: 33 MB), but as fp32 FMAs it is
+// ~1 GFMA of CUDA-core work and the SIMT kernel re-reads W_router (245 KB) from L2 for every few
+// tokens.  Here a CTA owns 16 tokens x all experts; its 8 warps split K (warp w takes k16-step w of
+// every 128-wide chunk), chunks of X and W_router are staged by cp.async (4 stages, padded rows
+// for conflict-free ldmatrix) and multiplied with mma.sync m16n8k16 (bf16 in, fp32 accumulate;
+// the same products as the FMA path).  The 8 partial logit tiles are summed in warp order (fixed,
+// deterministic), then the logits go through the same selection as the SIMT kernel.  Small CTAs
+// keep every SM busy down to ~2k tokens.
+constexpr int kMmaTok = 16;
+constexpr int kMmaK = 128;
+constexpr int kLd = kMmaK + 8;  // bf16 per padded smem row
+constexpr int kMmaStages = 4;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int sz = pred ? 16 : 0;  // 0 -> zero-fill (rows past T or E)
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(const void* smem, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(sa));
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int NP>  // n-tile pairs: experts padded to 16 * NP
+__global__ void __launch_bounds__(256)
+router_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr, int ntok, int d, int E,
+                  int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
+                  float* __restrict__ logits_out) {
+  extern __shared__ __align__(16) __nv_bfloat16 sbuf[];  // kMmaStages x (X chunk, W chunk); reused below
+  const int warp = warp_id(), lane = lane_id();
+  const int tok0 = blockIdx.x * kMmaTok;
+  const int nk = d / kMmaK;
+  constexpr int wrows = 16 * NP;  // W rows staged
+  const int stage_elems = (kMmaTok + wrows) * kLd;
+  auto load = [&](int kc) {
+    if (kc < nk) {
+      __nv_bfloat16* sx = sbuf + (kc % kMmaStages) * stage_elems;
+      __nv_bfloat16* sw = sx + kMmaTok * kLd;
+      const int k0 = kc * kMmaK;
+      // (16 + wrows) rows x 16 pieces of 16 B over 256 threads
+      for (int piece = threadIdx.x; piece < (kMmaTok + wrows) * 16; piece += 256) {
+        const int r = piece >> 4, c = (piece & 15) * 8;
+        if (r < kMmaTok) {
+          const int t = tok0 + r;
+          cp_async16(sx + r * kLd + c, x + (size_t)min(t, ntok - 1) * d + k0 + c, t < ntok);
+        } else {
+          const int e = r - kMmaTok;
+          cp_async16(sw + e * kLd + c, wr + (size_t)min(e, E - 1) * d + k0 + c, e < E);
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group per chunk
+  };
+  float acc[2 * NP][4];
+#pragma unroll
+  for (int j = 0; j < 2 * NP; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMmaStages - 1; ++i) load(i);
+  for (int kc = 0; kc < nk; ++kc) {
+    load(kc + kMmaStages - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kMmaStages - 1) : "memory");  // chunk kc landed
+    __syncthreads();
+    const __nv_bfloat16* sx = sbuf + (kc % kMmaStages) * stage_elems;
+    const __nv_bfloat16* sw = sx + kMmaTok * kLd;
+    const int ks = warp;  // this warp's k16 step of the chunk
+    uint32_t a0, a1, a2, a3;
+    ldsm_x4(sx + (lane & 15) * kLd + ks * 16 + (lane >> 4) * 8, a0, a1, a2, a3);
+#pragma unroll
+    for (int np = 0; np < NP; ++np) {
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(sw + (16 * np + (lane >> 4) * 8 + (lane & 7)) * kLd + ks * 16 + ((lane >> 3) & 1) * 8, b0, b1, b2, b3);
+      mma_bf16_16816(acc[2 * np], a0, a1, a2, a3, b0, b1);
+      mma_bf16_16816(acc[2 * np + 1], a0, a1, a2, a3, b2, b3);
+    }
+    __syncthreads();  // stage kc % kMmaStages is refilled by the next iteration's load
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  // partial tiles [warp][16 tokens][64 experts], summed in warp order
+  float* s_part = reinterpret_cast<float*>(sbuf);
+  float* s_logit = s_part + 8 * kMmaTok * kMaxE;
+  float* s_score = s_logit + kMmaTok * kMaxE;
+  {
+    float* my = s_part + warp * kMmaTok * kMaxE;
+    const int r0 = lane >> 2;
+#pragma unroll
+    for (int j = 0; j < 2 * NP; ++j) {
+      const int e = 8 * j + 2 * (lane & 3);
+      my[r0 * kMaxE + e] = acc[j][0];
+      my[r0 * kMaxE + e + 1] = acc[j][1];
+      my[(r0 + 8) * kMaxE + e] = acc[j][2];
+      my[(r0 + 8) * kMaxE + e + 1] = acc[j][3];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMmaTok * kMaxE; i += 256) {
+    float v = s_part[i];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v += s_part[w * kMmaTok * kMaxE + i];
+    s_logit[i] = v;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int ti = warp; ti < kMmaTok; ti += 8) {
+    const int tok = tok0 + ti;
+    if (tok >= ntok) break;
+    select_token<float>(s_logit + ti * kMaxE, s_score + ti * kMaxE, tok, E, k, mode, lane, ids_out, w_out,
+                        logits_out);
+  }
+}
+
+template <int NP>
+int launch_router_mma_np(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
+                         void* logits, cudaStream_t s) {
+  static bool attr_set = false;
+  const int smem = std::max(kMmaStages * (kMmaTok + 16 * NP) * kLd * 2, (8 + 2) * kMmaTok * kMaxE * 4);
+  if (!attr_set) {
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(router_mma_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  router_mma_kernel<NP><<<(T_ + kMmaTok - 1) / kMmaTok, 256, smem, s>>>(
+      (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w, (float*)logits);
+  return check_launch("qmoe_router(mma)");
+}
+
+int launch_router_mma(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
+                      void* logits, cudaStream_t s) {
+  if (E <= 16) return launch_router_mma_np<1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  if (E <= 32) return launch_router_mma_np<2>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  return launch_router_mma_np<4>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+}
+
+// Few tokens (decode): one token per CTA, all 8 warps on it.  Many tokens: warps own tokens (2
+// each) when the experts fit one or two 8-expert chunks, else 4 tokens share the 8 warps.
+template <typename T>
+int dispatch_router(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
+                    void* logits, cudaStream_t s) {
+  const int nchunk = (E + kExpChunk - 1) / kExpChunk;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (T_ >= 256 && d % kMmaK == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+        reinterpret_cast<uintptr_t>(wr) % 16 == 0)
+      return launch_router_mma(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  }
+  if (T_ < 148 * 8) return launch_router<T, 1, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  if (nchunk == 1) return launch_router<T, 16, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  if (nchunk == 2) return launch_router<T, 8, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  if (nchunk <= 4) return launch_router<T, 4, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  return launch_router<T, 4, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
 }
 
 }  // namespace
@@ -229,18 +419,13 @@ extern "C" int qmoe_router(const void* x, const void* w_router, int T, int d, in
   if (T == 0) return QMOE_OK;
   QMOE_REQUIRE(x && w_router && ids_out && w_out, "qmoe_router: null pointer");
   cudaStream_t s = as_stream(stream);
-  // Few tokens (decode): one token per CTA maximises the CTA count; many tokens: 4 per CTA so
-  // every W_router load feeds 4 dot products.
-  const bool small = T < 148 * 8;
   switch (dtype) {
     case QMOE_BF16:
-      return small ? launch_router<__nv_bfloat16, 1>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s)
-                   : launch_router<__nv_bfloat16, 4>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s);
+      return dispatch_router<__nv_bfloat16>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s);
     case QMOE_F32:
-      return small ? launch_router<float, 1>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s)
-                   : launch_router<float, 4>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s);
+      return dispatch_router<float>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s);
     case QMOE_F64:
-      return launch_router<double, 1>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s);
+      return launch_router<double, 1, 1>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s);
     default:
       set_error("qmoe_router: unknown dtype %d", dtype);
       return QMOE_ERR_INVALID;

@@ -3,7 +3,9 @@ import sys, torch
 sys.path.insert(0, ".")
 from paper_2503_09304_b200 import kernels as K
 
-d, F, E, k = 4096, 14336, 8, 2
+import os
+SHAPES = {"mixtral": (4096, 14336, 8, 2, K.ROUTE_TOPK_SOFTMAX), "qwen": (2048, 1408, 60, 4, K.ROUTE_SOFTMAX_TOPK)}
+d, F, E, k, mode = SHAPES[os.environ.get("SHAPE", "mixtral")]
 g = torch.Generator(device="cuda").manual_seed(0)
 wr = (torch.randn((E, d), device="cuda", generator=g) / 64).bfloat16()
 gu = (torch.randn((E, 2 * F, d), device="cuda", generator=g) / 64).bfloat16()
@@ -29,11 +31,11 @@ def timeit(fn, iters=10):
 
 for T in [int(t) for t in sys.argv[1:]] or [32, 256, 1024, 4096, 8192, 16384]:
     x = torch.randn((T, d), device="cuda", generator=g).bfloat16()
-    ids, w = K.router(x, wr, k)
+    ids, w = K.router(x, wr, k, mode)
     perm, offsets, xp = K.permute(ids, E, x=x)
     y = torch.empty((T * k, d), dtype=torch.bfloat16, device="cuda")
     act = torch.empty((T * k, F), dtype=torch.bfloat16, device="cuda")
-    t_r = timeit(lambda: K.router(x, wr, k))
+    t_r = timeit(lambda: K.router(x, wr, k, mode))
     t_p = timeit(lambda: K.permute(ids, E, x=x))
     t_f = timeit(lambda: K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act))
     t_c = timeit(lambda: K.combine(y, w, x))
