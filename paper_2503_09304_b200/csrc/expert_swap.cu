@@ -27,6 +27,8 @@
 // complete their gate_up.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+
 #include "expert_common.cuh"
 #include "tc_ptx.cuh"
 
@@ -342,28 +344,29 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
   }
 }
 
-// Y[perm[r]] = bf16(sum_s part[s][r]) for the rows of experts [e_begin, stop); one warp per row.
+// Y[perm[r]] = bf16(sum_s part[s][r]) for the rows of experts [e_begin, stop), splits summed in
+// order (deterministic).  One thread per 8 columns of a row, so a decode batch (64 rows x 4096)
+// still spreads over ~128 CTAs.
 __global__ void __launch_bounds__(256) swap_reduce_kernel(const float* __restrict__ part, int nsplit, int part_rows,
                                                           int N, const int32_t* __restrict__ perm,
                                                           const int32_t* __restrict__ offsets, int e_begin,
                                                           const int32_t* __restrict__ stop,
                                                           __nv_bfloat16* __restrict__ y) {
   const int r0 = offsets[e_begin], r1 = offsets[*stop];
-  const int lane = threadIdx.x & 31;
-  for (int r = r0 + blockIdx.x * 8 + (threadIdx.x >> 5); r < r1; r += gridDim.x * 8) {
-    __nv_bfloat16* dst = y + (size_t)perm[r] * N;
-    for (int c = lane * 8; c < N; c += 256) {
-      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int s = 0; s < nsplit; ++s) {
-        const float4* src = reinterpret_cast<const float4*>(part + ((size_t)s * part_rows + r) * N + c);
-        const float4 u = __ldg(src), w = __ldg(src + 1);
-        a[0] += u.x; a[1] += u.y; a[2] += u.z; a[3] += u.w; a[4] += w.x; a[5] += w.y; a[6] += w.z; a[7] += w.w;
-      }
-      __nv_bfloat162 h[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
-      *reinterpret_cast<uint4*>(dst + c) = *reinterpret_cast<const uint4*>(h);
+  const int per_row = N / 8;
+  const long long total = (long long)(r1 - r0) * per_row;
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < total; i += (long long)gridDim.x * 256) {
+    const int r = r0 + (int)(i / per_row), c = (int)(i % per_row) * 8;
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int s = 0; s < nsplit; ++s) {
+      const float4* src = reinterpret_cast<const float4*>(part + ((size_t)s * part_rows + r) * N + c);
+      const float4 u = __ldg(src), w = __ldg(src + 1);
+      a[0] += u.x; a[1] += u.y; a[2] += u.z; a[3] += u.w; a[4] += w.x; a[5] += w.y; a[6] += w.z; a[7] += w.w;
     }
+    __nv_bfloat162 h[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) h[q] = __floats2bfloat162_rn(a[2 * q], a[2 * q + 1]);
+    *reinterpret_cast<uint4*>(y + (size_t)perm[r] * N + c) = *reinterpret_cast<const uint4*>(h);
   }
 }
 
@@ -441,7 +444,8 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
   if ((st = NT == 32 ? launch_swap<32>(maps, p, s) : launch_swap<64>(maps, p, s))) return st;
   if ((st = ffn_finalize(ws, nullptr, e_end, cursor_out, s))) return st;
   if (p.nsplit > 1) {
-    const int grid = xp_rows / 8 + 1 < 148 * 4 ? xp_rows / 8 + 1 : 148 * 4;
+    const long long work = (long long)xp_rows * (d / 8);
+    const int grid = (int)std::min<long long>((work + 255) / 256, 148 * 8);
     swap_reduce_kernel<<<grid, 256, 0, s>>>(p.part, p.nsplit, xp_rows, d, perm, offsets, e_begin, &ws[0].stop,
                                             (__nv_bfloat16*)y);
     return check_launch("qmoe_expert_ffn(swap-AB split-K reduce)");

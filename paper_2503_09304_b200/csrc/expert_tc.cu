@@ -665,7 +665,7 @@ bool use_cta_pair(int xp_rows, int n_experts) {
     return v == nullptr ? -1 : atoi(v);
   }();
   if (forced >= 0) return forced == 1 && xp_rows > kSplitRowsMax;
-  if (xp_rows < 4096) return false;
+  if (xp_rows < 1536) return false;  // measured crossover (Mixtral: pair faster from ~768 tokens)
   const double r = (double)xp_rows / (n_experts > 0 ? n_experts : 1);
   auto eff = [r](int m) { return r / (m * std::ceil(r / m)); };
   return eff(256) >= eff(128) - 0.02;
