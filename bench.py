@@ -40,6 +40,12 @@ D, F, E, TOPK = 4096, 14336, 8, 2
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+def local_device() -> int:
+    import torch
+
+    return int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count())
+
+
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -173,24 +179,30 @@ def run_reference_arm(args, rank: int, world: int) -> None:
 # ------------------------------------------------------------------------------------------------
 # GPU arm
 
-def make_layer(rank: int, world: int, device):
+def make_layer(rank: int, world: int, device, transport: str = "p2p", max_tokens: int = 8192):
     import torch
 
     from paper_2503_09304_b200.moe_block import SparseMoeBlock
 
     if world == 1:
         return SparseMoeBlock(D, F, E, TOPK, device=device).init_random(seed=1234)
-    from paper_2503_09304_b200.ep import ExpertParallelMoE
+    from paper_2503_09304_b200.ep import ExpertParallelMoE, PeerExpertParallelMoE
 
+    if transport == "p2p":
+        return PeerExpertParallelMoE(D, F, E, TOPK, rank, world, max_tokens=max_tokens,
+                                     device=device).init_random(seed=1234)
     return ExpertParallelMoE(D, F, E, TOPK, rank, world, device=device).init_random(seed=1234)
 
 
-def count_launches(T: int, world: int) -> int:
+def count_launches(T: int, world: int, transport: str = "p2p") -> int:
     """Our kernels per MoE-layer step: router 1; permute count+scatter(+gather) 2-3;
-    expert FFN gate_up + finalize + down + finalize 4; combine 1; EP adds the regroup gather and
-    the return scatter."""
+    expert FFN gate_up + finalize + down + finalize 4; combine 1.  EP over NCCL adds the regroup
+    gather and the return scatter; EP over peer memory replaces the permute's gather with the
+    dispatch kernel and adds two flag barriers."""
     from paper_2503_09304_b200.kernels import permute_launches
 
+    if world > 1 and transport == "p2p":
+        return 1 + permute_launches(T, TOPK, gather=False) + 1 + 2 + 4 + 1
     return 1 + permute_launches(T, TOPK) + 4 + 1 + (2 if world > 1 else 0)
 
 
@@ -213,16 +225,72 @@ def run_serving(args) -> dict:
     return out
 
 
+QWEN = (2048, 1408, 60, 4)  # Qwen1.5-MoE-A2.7B routed experts (BASELINE config 4)
+
+
+def run_qwen_layer(dev, flush, world: int) -> dict:
+    """BASELINE config 4: fine-grained experts (60, top-4, F=1408) — small per-expert M.  One MoE
+    layer step (router -> permute -> tcgen05 experts -> combine; routed experts only) at a prefill
+    batch (8192 tokens, ~546 rows per expert) and a decode batch (32 tokens, ~2 rows per expert),
+    L2 flushed before every step.  Roofline: tensor (large batch) / HBM weight streaming (decode)."""
+    import torch
+
+    from paper_2503_09304_b200 import kernels as K
+
+    d, F, E, k = QWEN
+    g = torch.Generator(device=dev).manual_seed(7)
+    wr = (torch.randn((E, d), device=dev, generator=g) * d ** -0.5).bfloat16()
+    gu = (torch.randn((E, 2 * F, d), device=dev, generator=g) * d ** -0.5).bfloat16()
+    dn = (torch.randn((E, d, F), device=dev, generator=g) * F ** -0.5).bfloat16()
+    peaks, _ = load_peaks()
+    out = {"shape": f"d={d} F={F} E={E} top-{k} (routed experts; softmax->top-k, no renorm)"}
+    for name, T in (("prefill", 8192), ("decode", 32)):
+        x = torch.randn((T, d), device=dev, generator=g).bfloat16()
+        y = torch.empty((T * k, d), dtype=torch.bfloat16, device=dev)
+        act = torch.empty((T * k, F), dtype=torch.bfloat16, device=dev)
+
+        def layer():
+            ids, w = K.router(x, wr, k, K.ROUTE_SOFTMAX_TOPK)
+            perm, offsets, xp = K.permute(ids, E, x=x)
+            K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act)
+            return K.combine(y, w, x), offsets
+
+        for _ in range(3):
+            _, offsets = layer()
+        torch.cuda.synchronize()
+        hit = int((offsets[1:] > offsets[:-1]).sum())
+        ts = []
+        for _ in range(10):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            layer()
+            b.record()
+            ts.append((a, b))
+        torch.cuda.synchronize()
+        ms = statistics.median(a.elapsed_time(b) for a, b in ts)
+        flops = 6.0 * T * k * d * F
+        wbytes = hit * 3 * d * F * 2
+        out[name] = {"tokens": T, "ms": ms, "tflops": flops / ms / 1e9, "weight_gbs": wbytes / ms / 1e6,
+                     "tensor_frac_sustained": flops / ms / 1e9 / float(peaks.get("bf16_tflops_sustained",
+                                                                                    peaks["bf16_tflops"])),
+                     "hbm_frac": wbytes / ms / 1e6 / float(peaks["hbm_gbs"]), "experts_hit": hit}
+        del x, y, act
+    del gu, dn
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, rank: int, world: int) -> None:
     import torch
     import torch.distributed as dist
 
     from paper_2503_09304_b200 import kernels as K
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", local_device())
     torch.cuda.set_device(dev)
     T = args.tokens
-    block = make_layer(rank, world, dev)
+    block = make_layer(rank, world, dev, args.ep_transport, args.tokens)
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
     x = torch.randn((T, D), device=dev, generator=g).to(torch.bfloat16)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
@@ -239,6 +307,16 @@ def run_ours(args, rank: int, world: int) -> None:
         ffn_events.append((s, e))
 
     K.expert_ffn = timed_ffn
+    orig_peer = K.expert_ffn_peer
+
+    def timed_ffn_peer(*a, **kw):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        orig_peer(*a, **kw)
+        e.record()
+        ffn_events.append((s, e))
+
+    K.expert_ffn_peer = timed_ffn_peer
 
     def barrier():
         if world > 1:
@@ -248,6 +326,8 @@ def run_ours(args, rank: int, world: int) -> None:
     for _ in range(args.warmup):
         block(x)
     barrier()
+    if world > 1 and args.ep_transport == "p2p" and block.barrier_failed():
+        raise RuntimeError("expert-parallel peer-memory barrier timed out")
     ffn_events.clear()
     sampler = ClockSampler(dev.index)
     step_ms = []
@@ -269,6 +349,7 @@ def run_ours(args, rank: int, world: int) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t)
     K.expert_ffn = orig
+    K.expert_ffn_peer = orig_peer
 
     # e2e through the public block API with HOST buffers: every step uploads its own pinned input,
     # runs SparseMoeBlock.forward and downloads its output.  Steps are pipelined the way a server
@@ -335,6 +416,7 @@ def run_ours(args, rank: int, world: int) -> None:
         dec.append((a, b))
     barrier()
     dec_ms = statistics.median(a.elapsed_time(b) for a, b in dec)
+    qwen = run_qwen_layer(dev, flush, world) if world == 1 else None
     serving = None
     if world == 1 and args.serve_duration > 0:
         del block, x, xd, flush
@@ -374,6 +456,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "config": {"workload": f"mixtral-8x7b-shaped MoE layer step: router->permute->tcgen05 SwiGLU experts->"
                                f"combine, d={D} F={F} E={E} top-{TOPK}, T={T} tokens/step/GPU",
                    "tokens_per_step_per_gpu": T, "parallelism": f"ep{world}" if world > 1 else "single",
+                   "ep_transport": (args.ep_transport if world > 1 else None),
                    "l2": "flushed (256 MiB write) before every timed step"},
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": T * D * 2 * world,
                 "d2h_bytes_per_step": T * D * 2 * world,
@@ -387,7 +470,8 @@ def run_ours(args, rank: int, world: int) -> None:
         "decode_step": {"tokens": args.decode_tokens, "ms": dec_ms,
                         "weight_gbs": hit_bytes / (dec_ms / 1e3) / 1e9,
                         "hbm_frac": hit_bytes / (dec_ms / 1e3) / 1e9 / float(peaks["hbm_gbs"])},
-        "gpu_launches": count_launches(T, world) * args.steps,
+        "qwen": qwen,
+        "gpu_launches": count_launches(T, world, args.ep_transport) * args.steps,
         "clocks": clocks,
         "cpu_baseline": cpu,
         "serving": serving,
@@ -404,6 +488,9 @@ def main():
     ap.add_argument("--tokens", type=int, default=8192)
     ap.add_argument("--decode-tokens", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ep-transport", choices=("p2p", "nccl"), default="p2p",
+                    help="N>1: token dispatch/combine over NVLink peer memory (fused into the dispatch kernel "
+                         "and the expert GEMM epilogue) or NCCL all-to-all-v")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--serve-rate", type=float, default=7.0)
     ap.add_argument("--serve-duration", type=float, default=20.0,
@@ -420,8 +507,10 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_device())
+        # NCCL on a real multi-GPU node; QMOE_DIST_BACKEND=gloo lets a 1-GPU box smoke-test the N>1
+        # code path with every rank on cuda:0 (numbers from such a run are not scaling numbers)
+        dist.init_process_group(os.environ.get("QMOE_DIST_BACKEND", "nccl"))
     run_ours(args, rank, world)
     if world > 1:
         import torch.distributed as dist

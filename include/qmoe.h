@@ -169,6 +169,47 @@ QMOE_API int qmoe_kv_gather(const void* pool, const int32_t* slot_mapping, int n
                    void* dst, void* stream);
 
 /*
+ * Expert parallelism over NVLink peer memory (no reference counterpart: the reference is a
+ * single process; BASELINE north_star asks for expert-parallel dispatch/combine
+ * across the GPUs of one node).  One process per GPU; peer buffers are exchanged once through
+ * CUDA IPC.  Per MoE layer: qmoe_permute (no gather) -> counts all-gather (host, the same E ints
+ * the scheduler's boundary timestamps need) -> qmoe_ep_dispatch -> qmoe_ep_barrier ->
+ * qmoe_expert_ffn_peer -> qmoe_ep_barrier -> qmoe_combine on the local slot buffer.
+ *
+ * qmoe_ipc_export: 64-byte cudaIpcMemHandle of the allocation containing ptr + ptr's offset in it.
+ * qmoe_ipc_import: map a peer's exported buffer (opened once per allocation, then cached).
+ */
+QMOE_API int qmoe_ipc_export(const void* ptr, void* handle_out, size_t* offset_out);
+QMOE_API int qmoe_ipc_import(const void* handle, size_t offset, void** ptr_out);
+/*
+ * Fused gather + all-to-all dispatch (replaces the Xp gather of qmoe_permute, the dispatch
+ * all-to-all and the owner-side regroup): the i-th pending row of expert e (queue order) is
+ * stored, over peer memory, to row dest_base[e] + i of rank dest_rank[e]'s receive buffer
+ * x_peers[dest_rank[e]], and ret_peers[dest_rank[e]][that row] = me << 24 | slot.
+ * dest_rank / dest_base: device int32[E]; x_peers / ret_peers: device arrays of world pointers.
+ */
+QMOE_API int qmoe_ep_dispatch(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k, int E,
+                              size_t row_bytes, int me, const int32_t* dest_rank, const int32_t* dest_base,
+                              void* const* x_peers, int32_t* const* ret_peers, void* stream);
+/*
+ * Stream-ordered device barrier over peer memory: flag_peers[g] = rank g's int32[world] flag
+ * array.  Releases `epoch` to every rank (system scope, after a system fence so this rank's
+ * earlier peer stores are visible) and waits until every rank released it to us.  After
+ * timeout_ns the wait gives up and writes 1 to error_out (device int32, optional) instead of hanging.
+ */
+QMOE_API int qmoe_ep_barrier(int32_t* const* flag_peers, int me, int world, int epoch, long long timeout_ns,
+                             int32_t* error_out, void* stream);
+/*
+ * Grouped SwiGLU expert FFN (bf16, tcgen05) over the rows a rank received: the combine
+ * all-to-all is fused into the down-projection epilogue, which stores output row r straight
+ * into row (ret[r] & 0xFFFFFF) of rank (ret[r] >> 24)'s slot buffer y_peers[ret[r] >> 24].
+ * Same tiling, preemption-free (whole expert range), workspace as qmoe_expert_ffn.
+ */
+QMOE_API int qmoe_expert_ffn_peer(const void* xp, const int32_t* offsets, const int32_t* ret, int E, int d, int F,
+                                  const void* gate_up, const void* down, int xp_rows, void* act_ws,
+                                  void* const* y_peers, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Decoder-side fused helpers (outside the north-star path; used by the Mixtral/Qwen serving
  * plugin to cut per-layer launch counts).  bf16 only.
  * qmoe_rmsnorm: out = rmsnorm(x [+ residual_add]) * weight (HF MixtralRMSNorm rounding);

@@ -57,6 +57,12 @@ SIGNATURES = {
     "qmoe_kv_gather": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),
     "qmoe_rmsnorm": (_c_int, [_vp, _vp, _vp, ctypes.c_float, _c_int, _c_int, _vp, _vp, _vp]),
     "qmoe_rope": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "qmoe_ipc_export": (_c_int, [_vp, _vp, ctypes.POINTER(_c_size)]),
+    "qmoe_ipc_import": (_c_int, [_vp, _c_size, ctypes.POINTER(_vp)]),
+    "qmoe_ep_dispatch": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_size, _c_int, _vp, _vp, _vp, _vp, _vp]),
+    "qmoe_ep_barrier": (_c_int, [_vp, _c_int, _c_int, _c_int, ctypes.c_longlong, _vp, _vp]),
+    "qmoe_expert_ffn_peer": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp,
+                                      _c_size, _vp]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

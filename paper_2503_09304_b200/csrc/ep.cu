@@ -1,0 +1,170 @@
+// Expert parallelism over NVLink peer memory (one process per GPU, one node).
+//
+// The NCCL path (ep.py, transport "nccl") moves tokens with two all-to-all-v collectives per MoE
+// layer plus a regroup gather and a return scatter.  This path fuses them into the producing and
+// consuming kernels instead, the B200-native way for an NVSwitch box where every peer is one
+// load/store away:
+//   dispatch  qmoe_ep_dispatch: one kernel gathers each routed row of the local tokens (expert-major
+//             queue order from qmoe_permute) and stores it straight into the OWNING rank's receive
+//             buffer at its final position (owner's local-expert-major order, source ranks in order,
+//             so the owner's grouped GEMM consumes it with no regroup), together with a 32-bit return
+//             address (source rank << 24 | source slot).
+//   combine   the grouped expert FFN's down-projection epilogue (qmoe_expert_ffn_peer) writes every
+//             output row directly into the source rank's slot buffer through that return address,
+//             tile by tile as the tensor cores finish it, so the return transfer overlaps the GEMM.
+//   ordering  qmoe_ep_barrier: a device-side flag barrier over peer memory (release/acquire at
+//             system scope), stream-ordered, no host round trip.
+// Peer buffers are exchanged once with CUDA IPC handles (qmoe_ipc_export / qmoe_ipc_import).
+#include <cudaTypedefs.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace qmoe {
+namespace {
+
+// dst_x[g] row (dest_base[e] + i) = x[perm[r] / k] for the i-th pending row r of expert e;
+// dst_ret[g][same row] = me << 24 | perm[r].  One warp per row, 16-byte vector copies.
+__global__ void __launch_bounds__(256) ep_dispatch_kernel(const uint8_t* __restrict__ x, const int32_t* __restrict__ perm,
+                                                          const int32_t* __restrict__ offsets, int k, int E,
+                                                          size_t row_bytes, int me,
+                                                          const int32_t* __restrict__ dest_rank,
+                                                          const int32_t* __restrict__ dest_base,
+                                                          void* const* __restrict__ x_peers,
+                                                          int32_t* const* __restrict__ ret_peers) {
+  __shared__ int s_off[65];
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) s_off[i] = offsets[i];
+  __syncthreads();
+  const int R = s_off[E];
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < R; r += warps) {
+    int lo = 0, hi = E - 1;  // expert owning queue position r: last e with s_off[e] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int e = lo;
+    const int slot = perm[r];
+    const int g = dest_rank[e];
+    const size_t row = (size_t)dest_base[e] + (r - s_off[e]);
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)(slot / k) * row_bytes);
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(x_peers[g]) + row * row_bytes);
+    for (size_t c = lane; c < row_bytes / 16; c += 32) dst[c] = __ldg(src + c);
+    if (lane == 0) ret_peers[g][row] = (me << 24) | slot;
+  }
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// flags[g] = this rank's view of rank g's last barrier epoch (flags live in each rank's memory,
+// flag_peers[g] = rank g's flag array).  Lane g releases `epoch` into rank g's slot `me`, then
+// waits for rank g's release into our slot g.  Times out (error_out = 1) instead of hanging.
+__global__ void ep_barrier_kernel(int32_t* const* flag_peers, int me, int world, int epoch, long long timeout_ns,
+                                  int32_t* error_out) {
+  const int g = threadIdx.x;
+  __threadfence_system();  // this rank's earlier peer stores (dispatch / epilogue) before the release
+  if (g < world) {
+    int32_t* remote = flag_peers[g] + me;
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(remote), "r"(epoch) : "memory");
+    const int32_t* mine = flag_peers[me] + g;
+    const uint64_t t0 = globaltimer_ns();
+    while (true) {
+      int v;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+      if (v - epoch >= 0) break;
+      if ((long long)(globaltimer_ns() - t0) > timeout_ns) {
+        if (error_out != nullptr) atomicExch(error_out, 1);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  __syncwarp();
+}
+
+PFN_cuMemGetAddressRange_v3020 g_range = nullptr;
+std::once_flag g_range_once;
+std::mutex g_ipc_mu;
+std::map<std::string, void*> g_opened;  // full 64-byte IPC handle -> mapped base
+
+}  // namespace
+}  // namespace qmoe
+
+extern "C" int qmoe_ipc_export(const void* ptr, void* handle_out, size_t* offset_out) {
+  using namespace qmoe;
+  QMOE_REQUIRE(ptr && handle_out && offset_out, "qmoe_ipc_export: null pointer");
+  std::call_once(g_range_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  });
+  QMOE_REQUIRE(g_range != nullptr, "qmoe_ipc_export: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (g_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) {
+    set_error("qmoe_ipc_export: cuMemGetAddressRange failed");
+    return QMOE_ERR_CUDA;
+  }
+  cudaIpcMemHandle_t h;
+  QMOE_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = reinterpret_cast<uintptr_t>(ptr) - static_cast<uintptr_t>(base);
+  return QMOE_OK;
+}
+
+extern "C" int qmoe_ipc_import(const void* handle, size_t offset, void** ptr_out) {
+  using namespace qmoe;
+  QMOE_REQUIRE(handle && ptr_out, "qmoe_ipc_import: null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  const std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
+  std::lock_guard<std::mutex> lock(g_ipc_mu);
+  auto it = g_opened.find(key);
+  void* base = nullptr;
+  if (it != g_opened.end()) {
+    base = it->second;
+  } else {
+    QMOE_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    g_opened[key] = base;
+  }
+  *ptr_out = static_cast<uint8_t*>(base) + offset;
+  return QMOE_OK;
+}
+
+extern "C" int qmoe_ep_dispatch(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k, int E,
+                                size_t row_bytes, int me, const int32_t* dest_rank, const int32_t* dest_base,
+                                void* const* x_peers, int32_t* const* ret_peers, void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(T >= 0 && k >= 1 && E >= 1 && E <= 64, "qmoe_ep_dispatch: bad sizes T=%d k=%d E=%d", T, k, E);
+  QMOE_REQUIRE(me >= 0 && me < 256, "qmoe_ep_dispatch: rank %d outside [0, 256)", me);
+  QMOE_REQUIRE(T * k < (1 << 24), "qmoe_ep_dispatch: %d slots exceed the 24-bit return address", T * k);
+  QMOE_REQUIRE(row_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0,
+               "qmoe_ep_dispatch: rows must be 16-byte multiples and aligned");
+  if (T == 0) return QMOE_OK;
+  QMOE_REQUIRE(x && perm && offsets && dest_rank && dest_base && x_peers && ret_peers, "qmoe_ep_dispatch: null pointer");
+  const int rows = T * k;
+  const int grid = rows / 8 + 1 < 148 * 4 ? rows / 8 + 1 : 148 * 4;
+  ep_dispatch_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint8_t*>(x), perm, offsets, k, E,
+                                                          row_bytes, me, dest_rank, dest_base, x_peers, ret_peers);
+  return check_launch("qmoe_ep_dispatch");
+}
+
+extern "C" int qmoe_ep_barrier(int32_t* const* flag_peers, int me, int world, int epoch, long long timeout_ns,
+                               int32_t* error_out, void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(world >= 1 && world <= 32 && me >= 0 && me < world, "qmoe_ep_barrier: bad rank %d / world %d", me,
+               world);
+  QMOE_REQUIRE(flag_peers != nullptr, "qmoe_ep_barrier: null flag table");
+  ep_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(flag_peers, me, world, epoch, timeout_ns, error_out);
+  return check_launch("qmoe_ep_barrier");
+}

@@ -32,11 +32,11 @@ extern "C" size_t qmoe_expert_ffn_workspace_bytes(int variant, int dtype, int d,
   return n;
 }
 
-extern "C" int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int32_t* offsets,
+static int expert_ffn_entry(int variant, int dtype, const void* xp, const int32_t* offsets,
                                const int32_t* perm, int E, int d, int F, const void* w1, const void* w2,
                                int e_begin, int e_end, int xp_rows, void* act_ws, void* y,
                                const volatile int32_t* preempt_flag, int32_t* cursor_out, void* workspace,
-                               size_t workspace_bytes, void* stream) {
+                               size_t workspace_bytes, void* const* y_peers, void* stream) {
   using namespace qmoe;
   QMOE_REQUIRE(variant == QMOE_EXPERT_TANH_AFFINE || variant == QMOE_EXPERT_SWIGLU,
                "qmoe_expert_ffn: unknown variant %d", variant);
@@ -57,6 +57,8 @@ extern "C" int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int
     if (st) return st;
     return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
   }
+  QMOE_REQUIRE(y_peers == nullptr || (dtype == QMOE_BF16 && variant == QMOE_EXPERT_SWIGLU),
+               "qmoe_expert_ffn_peer: peer-memory outputs need the bf16 SwiGLU path");
   switch (dtype) {
     case QMOE_F64:
     case QMOE_F32:
@@ -64,9 +66,27 @@ extern "C" int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int
                              preempt_flag, cursor_out, ws, s);
     case QMOE_BF16:
       return expert_ffn_tc(variant, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, preempt_flag,
-                           cursor_out, ws, xp_rows, s);
+                           cursor_out, ws, xp_rows, y_peers, s);
     default:
       set_error("qmoe_expert_ffn: unknown dtype %d", dtype);
       return QMOE_ERR_INVALID;
   }
+}
+
+extern "C" int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int32_t* offsets,
+                               const int32_t* perm, int E, int d, int F, const void* w1, const void* w2,
+                               int e_begin, int e_end, int xp_rows, void* act_ws, void* y,
+                               const volatile int32_t* preempt_flag, int32_t* cursor_out, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  return expert_ffn_entry(variant, dtype, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, xp_rows, act_ws, y,
+                          preempt_flag, cursor_out, workspace, workspace_bytes, nullptr, stream);
+}
+
+extern "C" int qmoe_expert_ffn_peer(const void* xp, const int32_t* offsets, const int32_t* ret, int E, int d, int F,
+                                    const void* gate_up, const void* down, int xp_rows, void* act_ws,
+                                    void* const* y_peers, void* workspace, size_t workspace_bytes, void* stream) {
+  QMOE_REQUIRE(y_peers != nullptr, "qmoe_expert_ffn_peer: y_peers is null");
+  return expert_ffn_entry(QMOE_EXPERT_SWIGLU, QMOE_BF16, xp, offsets, ret, E, d, F, gate_up, down, 0, E, xp_rows,
+                          act_ws, const_cast<void*>(static_cast<const void*>(y_peers)), nullptr, nullptr, workspace,
+                          workspace_bytes, y_peers, stream);
 }

@@ -140,6 +140,15 @@ __device__ __forceinline__ int ffn_claim(const TileMap& m, FfnWorkspace* ws, con
   return e < stop ? t : -1;
 }
 
+// Destination row of a down-projection output: row v of the local slot buffer, or — expert
+// parallel over NVLink peer memory (qmoe_expert_ffn_peer) — row (v & 0xFFFFFF) of the slot
+// buffer of rank (v >> 24), whose base address is peers[v >> 24].
+template <typename T>
+__device__ __forceinline__ T* out_row(T* base, void* const* peers, int32_t v, size_t ld) {
+  if (peers != nullptr) return reinterpret_cast<T*>(peers[(uint32_t)v >> 24]) + (size_t)(v & 0xFFFFFF) * ld;
+  return base + (size_t)v * ld;
+}
+
 int ffn_ws_reset(FfnWorkspace* ws, cudaStream_t s);
 // Extra workspace the bf16 SwiGLU path needs for split-K partials of the down projection.
 size_t splitk_bytes(int xp_rows, int d);
@@ -159,11 +168,11 @@ bool use_swap_ab(int xp_rows, int n_experts, int d, int F);
 int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                    cudaStream_t s);
+                    void* const* y_peers, cudaStream_t s);
 
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                   const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int total_rows_hint,
-                  cudaStream_t s);
+                  void* const* y_peers, cudaStream_t s);
 
 }  // namespace qmoe

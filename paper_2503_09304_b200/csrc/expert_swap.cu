@@ -55,6 +55,7 @@ struct SwapParams {
   __nv_bfloat16* y;
   float* part;
   int nsplit, kb_per_split, part_rows;
+  void* const* peers;  // expert parallel over peer memory: per-rank slot buffers (see out_row)
 };
 
 template <int NT>
@@ -320,7 +321,7 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (j < n && ok) p.y[(size_t)p.perm[m0 + c + j] * p.d + col] = __float2bfloat16_rn(__uint_as_float(v[j]));
+              if (j < n && ok) out_row(p.y, p.peers, p.perm[m0 + c + j], p.d)[col] = __float2bfloat16_rn(__uint_as_float(v[j]));
           }
         }
       }
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(256) swap_reduce_kernel(const float* __restric
                                                           int N, const int32_t* __restrict__ perm,
                                                           const int32_t* __restrict__ offsets, int e_begin,
                                                           const int32_t* __restrict__ stop,
-                                                          __nv_bfloat16* __restrict__ y) {
+                                                          __nv_bfloat16* __restrict__ y, void* const* peers) {
   const int r0 = offsets[e_begin], r1 = offsets[*stop];
   const int per_row = N / 8;
   const long long total = (long long)(r1 - r0) * per_row;
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(256) swap_reduce_kernel(const float* __restric
     __nv_bfloat162 h[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) h[q] = __floats2bfloat162_rn(a[2 * q], a[2 * q + 1]);
-    *reinterpret_cast<uint4*>(y + (size_t)perm[r] * N + c) = *reinterpret_cast<const uint4*>(h);
+    *reinterpret_cast<uint4*>(out_row(y, peers, perm[r], N) + c) = *reinterpret_cast<const uint4*>(h);
   }
 }
 
@@ -413,7 +414,7 @@ bool use_swap_ab(int xp_rows, int n_experts, int d, int F) {
 int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                    cudaStream_t s) {
+                    void* const* y_peers, cudaStream_t s) {
   int st;
   if ((st = ffn_ws_reset(ws, s))) return st;
   // Token tile: 32 rows when experts see ~1-24 rows on average (decode), else 64.
@@ -435,6 +436,7 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
   p.done = ffn_done(ws);
   p.act = (__nv_bfloat16*)act_ws;
   p.y = (__nv_bfloat16*)y;
+  p.peers = y_peers;
   const int nkb2 = (F + kBK - 1) / kBK;
   const int want = swap_splits(F);
   p.kb_per_split = (nkb2 + want - 1) / want;
@@ -447,7 +449,7 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
     const long long work = (long long)xp_rows * (d / 8);
     const int grid = (int)std::min<long long>((work + 255) / 256, 148 * 8);
     swap_reduce_kernel<<<grid, 256, 0, s>>>(p.part, p.nsplit, xp_rows, d, perm, offsets, e_begin, &ws[0].stop,
-                                            (__nv_bfloat16*)y);
+                                            (__nv_bfloat16*)y, y_peers);
     return check_launch("qmoe_expert_ffn(swap-AB split-K reduce)");
   }
   return QMOE_OK;

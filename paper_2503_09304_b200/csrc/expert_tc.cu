@@ -65,6 +65,7 @@ struct TcParams {
   int kb_per_split;
   float* part;        // [nsplit][part_rows][N] fp32 partials
   int part_rows;
+  void* const* peers;  // down projection: per-rank slot buffers (expert parallel over peer memory)
 };
 
 template <int BN>
@@ -214,8 +215,8 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if constexpr (EPI == EPI_DOWN_PART) {
           part_row = p.part + ((size_t)split * p.part_rows + row) * p.N;
         } else {
-          const size_t orow = (EPI == EPI_SWIGLU) ? (size_t)row : (size_t)p.perm[row];
-          dst_row = p.out + orow * p.out_ld;
+          dst_row = (EPI == EPI_SWIGLU) ? p.out + (size_t)row * p.out_ld
+                                        : out_row(p.out, p.peers, p.perm[row], p.out_ld);
         }
       }
       ptx::mbar_wait(&tfull_bar[acc], aphase);
@@ -283,11 +284,11 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
                                                             int N, const int32_t* __restrict__ perm,
                                                             const int32_t* __restrict__ offsets, int e_begin,
                                                             const int32_t* __restrict__ stop,
-                                                            __nv_bfloat16* __restrict__ y) {
+                                                            __nv_bfloat16* __restrict__ y, void* const* peers) {
   const int r0 = offsets[e_begin], r1 = offsets[*stop];
   const int lane = threadIdx.x & 31;
   for (int r = r0 + blockIdx.x * 8 + (threadIdx.x >> 5); r < r1; r += gridDim.x * 8) {
-    __nv_bfloat16* dst = y + (size_t)perm[r] * N;
+    __nv_bfloat16* dst = out_row(y, peers, perm[r], N);
     for (int c = lane * 8; c < N; c += 256) {
       float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       for (int s = 0; s < nsplit; ++s) {
@@ -452,8 +453,8 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const bool valid = row < p.offsets[e + 1];
       __nv_bfloat16* dst_row = nullptr;
       if (valid) {
-        const size_t orow = (EPI == EPI_SWIGLU) ? (size_t)row : (size_t)p.perm[row];
-        dst_row = p.out + orow * p.out_ld;
+        dst_row = (EPI == EPI_SWIGLU) ? p.out + (size_t)row * p.out_ld
+                                      : out_row(p.out, p.peers, p.perm[row], p.out_ld);
       }
       ptx::mbar_wait_cluster(&tfull_bar[acc], aphase);
       ptx::tc_fence_after();
@@ -591,7 +592,7 @@ int launch_tc2(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cu
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                   const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                  cudaStream_t s) {
+                  void* const* y_peers, cudaStream_t s) {
   int st = init_driver();
   if (st) return st;
   QMOE_REQUIRE(d % 64 == 0, "qmoe_expert_ffn(bf16): d must be a multiple of 64 (d=%d)", d);
@@ -600,7 +601,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
                "qmoe_expert_ffn(bf16): buffers must be 16-byte aligned");
   if (variant == QMOE_EXPERT_SWIGLU && use_swap_ab(xp_rows, E, d, F))
     return expert_ffn_swap(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
-                           xp_rows, s);
+                           xp_rows, y_peers, s);
   constexpr int BN = 256;
   if ((st = ffn_ws_reset(ws, s))) return st;
   TcParams p{};
@@ -609,6 +610,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   p.offsets = offsets;
   p.perm = perm;
   p.flag = flag;
+  p.peers = y_peers;
   CUtensorMap ta, tb;
   if (variant == QMOE_EXPERT_TANH_AFFINE) {
     if ((st = make_map(&ta, xp, xp_rows, d, BM)) || (st = make_map(&tb, w1, (uint64_t)E * d, d, BN / 2))) return st;
@@ -646,7 +648,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
     if ((st = ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s))) return st;
     const int grid = xp_rows / 8 + 1 < 148 * 4 ? xp_rows / 8 + 1 : 148 * 4;
     splitk_reduce_kernel<<<grid, 256, 0, s>>>(p2.part, p2.nsplit, xp_rows, d, perm, offsets, e_begin, &ws[1].stop,
-                                               (__nv_bfloat16*)y);
+                                               (__nv_bfloat16*)y, y_peers);
     return check_launch("qmoe_expert_ffn(split-K reduce)");
   }
   p2.nsplit = 1;

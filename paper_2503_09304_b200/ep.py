@@ -139,3 +139,111 @@ class ExpertParallelMoE(torch.nn.Module):
             ops.scatter_rows(y_back, perm[:R].contiguous(), y)
         res = None if residual is None else residual.reshape(-1, d).contiguous()
         return ops.combine(y, w, res).reshape(shape)
+
+
+class PeerExpertParallelMoE(ExpertParallelMoE):
+    """The same expert-parallel block with the two all-to-alls replaced by peer-memory stores
+    (csrc/ep.cu): a dispatch kernel writes every routed row straight into its owner's receive
+    buffer in the owner's local-expert-major order, and the grouped GEMM's down-projection epilogue
+    writes every output row straight into its source rank's slot buffer, tile by tile.  Device flag
+    barriers over peer memory order the phases (no host round trip, no NCCL on the data path).
+    Receive / slot / flag buffers are allocated once for `max_tokens` tokens per rank and exchanged
+    through CUDA IPC (`connect`, collective)."""
+
+    def __init__(self, hidden_size: int, intermediate_size: int, num_experts: int, top_k: int, rank: int,
+                 world: int, max_tokens: int, device: Optional[torch.device] = None,
+                 dtype: torch.dtype = torch.bfloat16, group=None, ops=K, route_mode: int = K.ROUTE_TOPK_SOFTMAX,
+                 barrier_timeout_s: float = 30.0, host_barrier: bool = False):
+        super().__init__(hidden_size, intermediate_size, num_experts, top_k, rank, world, device=device, dtype=dtype,
+                         group=group, ops=ops, route_mode=route_mode)
+        if dtype != torch.bfloat16:
+            raise ValueError("the peer-memory transport runs the bf16 tcgen05 path")
+        self.max_tokens = max_tokens
+        cap = world * max_tokens * top_k  # worst case: every routed row of every rank lands here
+        dev = self.device
+        self.x_recv = torch.empty((cap, hidden_size), dtype=dtype, device=dev)
+        self.ret = torch.empty(cap, dtype=torch.int32, device=dev)
+        self.y = torch.empty((max_tokens * top_k, hidden_size), dtype=dtype, device=dev)
+        self.flags = torch.zeros(world, dtype=torch.int32, device=dev)
+        self.error = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.act = torch.empty((cap, intermediate_size), dtype=dtype, device=dev)
+        self.epoch = 0
+        self.timeout_s = barrier_timeout_s
+        # host_barrier: order the phases with a stream sync + process-group barrier instead of the
+        # device flag barrier (debugging aid: isolates the data path from the flag protocol)
+        self.host_barrier = host_barrier
+        self._peer_tables = None
+
+    def _comm_device(self):
+        backend = dist.get_backend(self.group)
+        return torch.device("cpu") if backend == "gloo" else self.device
+
+    def connect(self) -> None:
+        """Exchange CUDA IPC handles of the receive / return / slot / flag buffers (collective)."""
+        bufs = (self.x_recv, self.ret, self.y, self.flags)
+        mine = [K.ipc_export(t) for t in bufs]
+        torch.cuda.synchronize(self.device)  # buffers (zeroed flags) materialised before peers map them
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=self.group)
+        tables = []
+        for i, t in enumerate(bufs):
+            ptrs = [t.data_ptr() if g == self.rank else K.ipc_import(*allh[g][i]) for g in range(self.world)]
+            tables.append(torch.tensor(ptrs, dtype=torch.int64, device=self.device))
+        self._peer_tables = tables
+        dist.barrier(group=self.group)
+
+    def dispatch_tables(self, allc: list[list[int]]) -> tuple[list[int], list[int]]:
+        """For this rank's rows of expert e: the owning rank and the first receive row there.
+        Owner g lays rows out by its local experts (ascending), then source rank, then queue order."""
+        E, b, me = self.E, self.bounds, self.rank
+        dest_rank, dest_base = [0] * E, [0] * E
+        for g in range(self.world):
+            base = 0
+            for e in range(b[g], b[g + 1]):
+                dest_rank[e] = g
+                dest_base[e] = base + sum(allc[s][e] for s in range(me))
+                base += sum(allc[s][e] for s in range(self.world))
+        return dest_rank, dest_base
+
+    @torch.no_grad()
+    def forward(self, hidden_states: torch.Tensor, residual: Optional[torch.Tensor] = None) -> torch.Tensor:
+        ops, E, k, d = self.ops, self.E, self.k, self.d
+        shape = hidden_states.shape
+        x = hidden_states.reshape(-1, d).contiguous()
+        T = x.shape[0]
+        if T > self.max_tokens:
+            raise ValueError(f"{T} tokens exceed max_tokens={self.max_tokens}")
+        if self._peer_tables is None:
+            self.connect()
+        x_peers, ret_peers, y_peers, flag_peers = self._peer_tables
+        ids, w = ops.router(x, self.w_router, k, self.route_mode)
+        perm, offsets, _ = ops.permute(ids, E)
+        off = offsets.tolist()
+        allc = self.exchange_counts([off[e + 1] - off[e] for e in range(E)])
+        dest_rank, dest_base = self.dispatch_tables(allc)
+        tab = torch.tensor([dest_rank, dest_base], dtype=torch.int32).to(self.device, non_blocking=True)
+        ops.ep_dispatch(x, perm, offsets, k, self.rank, tab[0], tab[1], x_peers, ret_peers)
+        self._barrier(flag_peers)
+        loc = [0]
+        for e in range(self.e_lo, self.e_hi):
+            loc.append(loc[-1] + sum(allc[s][e] for s in range(self.world)))
+        R = loc[-1]
+        if R:
+            loc_off = torch.tensor(loc, dtype=torch.int32).to(self.device, non_blocking=True)
+            ops.expert_ffn_peer(self.x_recv[:R], loc_off, self.ret[:R], self.gate_up, self.down, y_peers,
+                                act_ws=self.act[:R])
+        self._barrier(flag_peers)
+        res = None if residual is None else residual.reshape(-1, d).contiguous()
+        return ops.combine(self.y[: T * k], w, res).reshape(shape)
+
+    def _barrier(self, flag_peers) -> None:
+        self.epoch += 1
+        if self.host_barrier:
+            torch.cuda.current_stream(self.device).synchronize()
+            dist.barrier(group=self.group)
+        else:
+            self.ops.ep_barrier(flag_peers, self.rank, self.world, self.epoch, self.error, self.timeout_s)
+
+    def barrier_failed(self) -> bool:
+        """True if any device barrier timed out (syncs)."""
+        return bool(int(self.error.item()))

@@ -8,6 +8,7 @@ exception classes.  Nothing here synchronises the host.
 
 from __future__ import annotations
 
+import ctypes
 from typing import Optional
 
 import torch
@@ -261,3 +262,66 @@ def rope_(qkv: torch.Tensor, positions: torch.Tensor, cos: torch.Tensor, sin: to
     lib = _lib.load()
     check(lib.qmoe_rope(_ptr(qkv), k_ptr, _ptr(positions), _ptr(cos), _ptr(sin), T, n_heads, n_kv_heads, head_dim,
                         width, width, _stream()), "qmoe_rope")
+
+
+# ------------------------------------------------------------------ expert parallel over peer memory
+
+def ipc_export(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t in it)."""
+    _need(t, "t")
+    handle = ctypes.create_string_buffer(64)
+    off = ctypes.c_size_t(0)
+    lib = _lib.load()
+    check(lib.qmoe_ipc_export(_ptr(t), handle, ctypes.byref(off)), "qmoe_ipc_export")
+    return handle.raw, int(off.value)
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    """Device address of a peer process's exported buffer (mapped once per allocation)."""
+    out = ctypes.c_void_p(0)
+    lib = _lib.load()
+    check(lib.qmoe_ipc_import(ctypes.create_string_buffer(handle, 64), offset, ctypes.byref(out)), "qmoe_ipc_import")
+    return int(out.value)
+
+
+def ep_dispatch(x: torch.Tensor, perm: torch.Tensor, offsets: torch.Tensor, k: int, me: int, dest_rank: torch.Tensor,
+                dest_base: torch.Tensor, x_peers: torch.Tensor, ret_peers: torch.Tensor) -> None:
+    """Store every pending routed row of x into its owner's receive buffer (see qmoe.h)."""
+    _need(x, "x")
+    for name, t in (("perm", perm), ("offsets", offsets), ("dest_rank", dest_rank), ("dest_base", dest_base)):
+        _need(t, name, torch.int32)
+    _need(x_peers, "x_peers", torch.int64)
+    _need(ret_peers, "ret_peers", torch.int64)
+    T, d = x.shape
+    lib = _lib.load()
+    check(lib.qmoe_ep_dispatch(_ptr(x), _ptr(perm), _ptr(offsets), T, k, offsets.shape[0] - 1, d * x.element_size(),
+                               me, _ptr(dest_rank), _ptr(dest_base), _ptr(x_peers), _ptr(ret_peers), _stream()),
+          "qmoe_ep_dispatch")
+
+
+def ep_barrier(flag_peers: torch.Tensor, me: int, world: int, epoch: int, error: Optional[torch.Tensor] = None,
+               timeout_s: float = 10.0) -> None:
+    """Stream-ordered device barrier over peer memory (flag_peers: int64 device [world])."""
+    _need(flag_peers, "flag_peers", torch.int64)
+    lib = _lib.load()
+    check(lib.qmoe_ep_barrier(_ptr(flag_peers), me, world, epoch, int(timeout_s * 1e9), _ptr(error), _stream()),
+          "qmoe_ep_barrier")
+
+
+def expert_ffn_peer(xp: torch.Tensor, offsets: torch.Tensor, ret: torch.Tensor, gate_up: torch.Tensor,
+                    down: torch.Tensor, y_peers: torch.Tensor, act_ws: Optional[torch.Tensor] = None) -> None:
+    """Grouped SwiGLU experts over received rows; outputs go straight to their source ranks."""
+    _need(xp, "xp", torch.bfloat16)
+    _need(offsets, "offsets", torch.int32)
+    _need(ret, "ret", torch.int32)
+    _need(y_peers, "y_peers", torch.int64)
+    E, twoF, d = gate_up.shape
+    F = twoF // 2
+    rows = xp.shape[0]
+    if act_ws is None:
+        act_ws = torch.empty((max(rows, 1), F), dtype=xp.dtype, device=xp.device)
+    lib = _lib.load()
+    nbytes = lib.qmoe_expert_ffn_workspace_bytes(EXPERT_SWIGLU, _lib.QMOE_BF16, d, rows)
+    ws = workspace(nbytes, "ffn", xp.device)
+    check(lib.qmoe_expert_ffn_peer(_ptr(xp), _ptr(offsets), _ptr(ret), E, d, F, _ptr(gate_up), _ptr(down), rows,
+                                   _ptr(act_ws), _ptr(y_peers), _ptr(ws), nbytes, _stream()), "qmoe_expert_ffn_peer")

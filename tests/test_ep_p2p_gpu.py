@@ -1,0 +1,117 @@
+"""Expert parallelism over peer memory (csrc/ep.cu), world size 2, on ONE B200: two processes share
+cuda:0 and map each other's receive / slot / flag buffers through CUDA IPC exactly as two GPUs of
+an NVSwitch box would: the dispatch kernel stores rows into the peer's receive buffer, the expert
+GEMM epilogue stores outputs into the peer's slot buffer, and stream-ordered device flag barriers
+(system-scope release/acquire on the peer's flags) order the phases.  gloo carries only the
+host-side handle exchange and the per-layer counts all-gather.  Every rank's layer output must
+match the single-process SparseMoeBlock on the same weights (same rows per expert, same order).
+The large case (> 512 received rows, 128/256-row tcgen05 tiles, several buffers in separate
+allocations) is the one that caught an IPC-handle cache keyed on a handle prefix."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+D, F, E, K, SEED = 512, 1024, 8, 2, 11
+TOKENS = {0: [24, 7, 40], 1: [31, 0, 9]}  # per rank, per forward call (uneven; one empty batch)
+BIG = {0: [700, 64], 1: [513, 600]}      # > 512 received rows: the 128/256-row tcgen05 tiles
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _inputs(rank, call, T):
+    g = torch.Generator().manual_seed(1000 * rank + call)
+    return torch.randn((T, D), generator=g).bfloat16()
+
+
+def _worker(rank, world, port, q, transport):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2503_09304_b200.ep import ExpertParallelMoE, PeerExpertParallelMoE
+
+        tokens = BIG if transport == "p2p-big" else TOKENS
+        if transport.startswith("p2p"):
+            blk = PeerExpertParallelMoE(D, F, E, K, rank, world, max_tokens=1024, device=torch.device("cuda", 0),
+                                        barrier_timeout_s=60.0).init_random(SEED)
+        else:  # the all-to-all-v transport; gloo stands in for NCCL (two ranks cannot share a GPU in NCCL)
+            blk = ExpertParallelMoE(D, F, E, K, rank, world, device=torch.device("cuda", 0)).init_random(SEED)
+            blk.barrier_failed = lambda: False
+        outs = []
+        for call, T in enumerate(tokens[rank]):
+            x = _inputs(rank, call, T).cuda()
+            outs.append(blk(x, residual=x).float().cpu().numpy())
+        torch.cuda.synchronize()
+        q.put((rank, outs, blk.barrier_failed(), None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # noqa: BLE001 - report to the parent instead of hanging it
+        q.put((rank, None, None, repr(exc)))
+
+
+@pytest.mark.parametrize("transport", ["p2p", "p2p-big", "alltoall"])
+def test_expert_parallel_matches_single_process(cuda, transport):
+    from paper_2503_09304_b200.moe_block import SparseMoeBlock
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, transport)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    errors = [e for (_, _, _, e) in got if e]
+    assert not errors, errors
+    ref_blk = SparseMoeBlock(D, F, E, K, device=cuda).init_random(SEED)
+    tokens = BIG if transport == "p2p-big" else TOKENS
+    for rank, outs, failed, _ in got:
+        assert not failed, f"rank {rank}: a device barrier timed out"
+        for call, T in enumerate(tokens[rank]):
+            x = _inputs(rank, call, T).cuda()
+            if T == 0:
+                assert outs[call].shape == (0, D)
+                continue
+            ref = (ref_blk(x.view(1, T, D)).view(T, D).float() + x.float()).cpu().numpy()
+            got_o = outs[call]
+            rel = np.linalg.norm(got_o - ref) / np.linalg.norm(ref)
+            assert rel < 1e-2, (rank, call, rel)
+
+
+def test_device_flag_barrier_two_concurrent_ranks(cuda):
+    """qmoe_ep_barrier with two 'ranks' on two streams of one process (both resident at once):
+    60 epochs complete with no timeout and every flag ends at the last epoch; a rank whose peer
+    never arrives times out into the error word instead of hanging."""
+    from paper_2503_09304_b200 import kernels as Kn
+
+    flags = [torch.zeros(2, dtype=torch.int32, device=cuda) for _ in range(2)]
+    table = torch.tensor([f.data_ptr() for f in flags], dtype=torch.int64, device=cuda)
+    err = torch.zeros(1, dtype=torch.int32, device=cuda)
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    torch.cuda.synchronize()
+    for epoch in range(1, 61):
+        for me in range(2):
+            with torch.cuda.stream(streams[me]):
+                Kn.ep_barrier(table, me, 2, epoch, err, timeout_s=20.0)
+    torch.cuda.synchronize()
+    assert int(err) == 0
+    assert [f.tolist() for f in flags] == [[60, 60], [60, 60]]
+    Kn.ep_barrier(table, 0, 2, 61, err, timeout_s=0.2)  # rank 1 never arrives
+    torch.cuda.synchronize()
+    assert int(err) == 1
