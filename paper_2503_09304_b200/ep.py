@@ -55,6 +55,23 @@ def regroup_index(counts: list[list[int]], e_lo: int, e_hi: int) -> tuple[list[i
     return idx, offsets
 
 
+def dispatch_tables(allc: list[list[int]], bounds: list[int], me: int) -> tuple[list[int], list[int]]:
+    """Peer-memory dispatch: for source rank `me`'s rows of expert e, the owning rank and the first
+    receive row there.  Owner g lays its receive buffer out by local expert (ascending), then source
+    rank, then queue order -- the order regroup_index produces for the all-to-all transport -- so the
+    grouped GEMM consumes it directly.  allc[s][e] = rows of expert e that rank s sends."""
+    world = len(allc)
+    E = bounds[-1]
+    dest_rank, dest_base = [0] * E, [0] * E
+    for g in range(world):
+        base = 0
+        for e in range(bounds[g], bounds[g + 1]):
+            dest_rank[e] = g
+            dest_base[e] = base + sum(allc[s][e] for s in range(me))
+            base += sum(allc[s][e] for s in range(world))
+    return dest_rank, dest_base
+
+
 class ExpertParallelMoE(torch.nn.Module):
     """Mixtral-style sparse MoE block with experts sharded over the process group."""
 
@@ -193,17 +210,7 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
         dist.barrier(group=self.group)
 
     def dispatch_tables(self, allc: list[list[int]]) -> tuple[list[int], list[int]]:
-        """For this rank's rows of expert e: the owning rank and the first receive row there.
-        Owner g lays rows out by its local experts (ascending), then source rank, then queue order."""
-        E, b, me = self.E, self.bounds, self.rank
-        dest_rank, dest_base = [0] * E, [0] * E
-        for g in range(self.world):
-            base = 0
-            for e in range(b[g], b[g + 1]):
-                dest_rank[e] = g
-                dest_base[e] = base + sum(allc[s][e] for s in range(me))
-                base += sum(allc[s][e] for s in range(self.world))
-        return dest_rank, dest_base
+        return dispatch_tables(allc, self.bounds, self.rank)
 
     @torch.no_grad()
     def forward(self, hidden_states: torch.Tensor, residual: Optional[torch.Tensor] = None) -> torch.Tensor:

@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2503_09304_b200.ep import ExpertParallelMoE, expert_bounds, regroup_index
+from paper_2503_09304_b200.ep import ExpertParallelMoE, dispatch_tables, expert_bounds, regroup_index
 
 
 class CpuOps:
@@ -131,3 +131,29 @@ def test_regroup_index_orders_by_local_expert_then_source():
     # received: src0 -> e2:0 rows, e3:3 rows [0,1,2]; src1 -> e2:1 row [3], e3:1 row [4]
     assert idx == [3, 0, 1, 2, 4]
     assert off == [0, 1, 5]
+
+
+@pytest.mark.parametrize("world,E", [(2, 8), (4, 8), (8, 60), (3, 5)])
+def test_peer_dispatch_tables_match_regroup_order(world, E):
+    """The peer-memory transport writes rows straight to their final receive position: for every
+    owner, the (source, expert) blocks tile [0, received rows) exactly, in the same local-expert-major
+    then source-rank order that regroup_index gives the all-to-all transport."""
+    rng = np.random.default_rng(world * 100 + E)
+    counts = rng.integers(0, 9, size=(world, E)).tolist()
+    counts[0][0] = 0  # an empty (source, expert) block
+    b = expert_bounds(E, world)
+    for g in range(world):
+        # position of every received row, keyed (expert, source, i)
+        pos = {}
+        for s in range(world):
+            dest_rank, dest_base = dispatch_tables(counts, b, s)
+            for e in range(b[g], b[g + 1]):
+                assert dest_rank[e] == g
+                for i in range(counts[s][e]):
+                    pos[(e, s, i)] = dest_base[e] + i
+        total = sum(counts[s][e] for s in range(world) for e in range(b[g], b[g + 1]))
+        assert sorted(pos.values()) == list(range(total))
+        order = [key for key, _ in sorted(pos.items(), key=lambda kv: kv[1])]
+        assert order == sorted(order)  # expert, then source, then queue order
+        idx, off = regroup_index(counts, b[g], b[g + 1])
+        assert off[-1] == total
