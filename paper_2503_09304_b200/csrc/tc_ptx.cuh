@@ -138,15 +138,20 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// Wait with cluster-scope acquire (barriers that receive remote arrivals).
+// Wait with cluster-scope acquire (barriers that receive remote arrivals).  The spin polls with a
+// relaxed try_wait; one acquire try_wait (which then succeeds at once) follows, because an acquire
+// try_wait makes ptxas emit an L1 invalidate (CCTL.IVALL) on every spin iteration.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t"
       ".reg .pred p;\n\t"
       "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAITC_%=;\n\t"
+      "WAITA_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITA_%=;\n\t"
       "}" ::"r"(addr),
       "r"(parity)
       : "memory");
