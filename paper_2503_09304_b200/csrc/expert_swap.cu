@@ -9,7 +9,7 @@
 // most of their MMA work and 1/3 of their L2 traffic on padding rows, and the two launches
 // (gate_up, then down) each leave a partial last wave on a 148-SM part.  Here:
 //   * swap-AB: the weights are the MMA's M = 128 side (A, from HBM through TMA), the tokens the
-//     N = NT side (B, NT in {32, 64} rows from L2).  D[128 weight rows x NT tokens] lives in TMEM.
+//     N = NT side (B, NT in {32, 64, 128} rows from L2).  D[128 weight rows x NT tokens] lives in TMEM.
 //   * gate_up unit = (expert, 128 F columns, token tile): two MMAs per K step (gate rows and up
 //     rows of the same 128 columns) into two accumulators, so every epilogue thread holds g and u
 //     of one column and writes SiLU(g)*u for its tokens to act.
@@ -62,7 +62,10 @@ template <int NT>
 struct SwapCfg {
   static constexpr int kABytes = kWRows * kBK * 2;  // 16 KB: one 128-row weight K block
   static constexpr int kBBytes = NT * kBK * 2;      // one NT-row token K block
-  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
+  // down-projection K blocks per stage: 2 keeps 32 KB of weights per stage for small token tiles;
+  // NT = 128 stages one (48 KB stages, 4 in flight)
+  static constexpr int kKB2 = NT <= 64 ? 2 : 1;
+  static constexpr int kStageBytes = 2 * kABytes + kKB2 * kBBytes;
   static constexpr int kStages = (200 * 1024) / kStageBytes;
   static constexpr int kSmem = kStages * kStageBytes + 1024;
   static constexpr uint32_t kTmemCols = 4 * NT;  // 2 accumulator stages x (gate, up) x NT
@@ -194,8 +197,8 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
         } else {
           const int kb0 = split * p.kb_per_split, kb1 = min(nkb2, kb0 + p.kb_per_split);
           const int w_row = e * p.d + n0;
-          for (int kb = kb0; kb < kb1; kb += 2) {
-            const bool two = kb + 1 < kb1;
+          for (int kb = kb0; kb < kb1; kb += C::kKB2) {
+            const bool two = C::kKB2 == 2 && kb + 1 < kb1;
             ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * C::kStageBytes;
             ptx::mbar_arrive_expect_tx(&full_bar[stage], (two ? 2 : 1) * (C::kABytes + C::kBBytes));
@@ -246,8 +249,8 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
           int e, m0, n0, split;
           map2.locate(t - N1, NT, nt2 * p.nsplit, kWRows, e, m0, n0, p.nsplit, &split);
           const int kb0 = split * p.kb_per_split, kb1 = min(nkb2, kb0 + p.kb_per_split);
-          for (int kb = kb0; kb < kb1; kb += 2) {
-            const int nh = kb + 1 < kb1 ? 2 : 1;
+          for (int kb = kb0; kb < kb1; kb += C::kKB2) {
+            const int nh = C::kKB2 == 2 && kb + 1 < kb1 ? 2 : 1;
             ptx::mbar_wait(&full_bar[stage], phase);
             ptx::tc_fence_after();
             const uint32_t a = ptx::smem_u32(smem + stage * C::kStageBytes);
@@ -405,10 +408,10 @@ bool use_swap_ab(int xp_rows, int n_experts, int d, int F) {
     const char* v = getenv("QMOE_SWAP_AB");
     return v == nullptr ? -1 : atoi(v);
   }();
+  (void)F;
   if (d % kWRows != 0 || F % kBK != 0 || n_experts < 1 || n_experts > kFfnMaxExperts) return false;
-  const bool fits = xp_rows <= kSwapRowsMax || swap_splits(F) == 1;
-  if (forced >= 0) return forced == 1 && fits;
-  return fits && xp_rows <= 64 * n_experts;
+  if (forced >= 0) return forced == 1;
+  return xp_rows <= 64 * n_experts;
 }
 
 int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
@@ -417,9 +420,9 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
                     void* const* y_peers, cudaStream_t s) {
   int st;
   if ((st = ffn_ws_reset(ws, s))) return st;
-  // Token tile: 32 rows when experts see ~1-24 rows on average (decode), else 64.
+  // Token tile: 32 rows when experts see ~1-24 rows on average (decode), 64 up to ~64, else 128.
   const double mean_rows = (double)xp_rows / (E > 0 ? E : 1);
-  const int NT = mean_rows <= 24.0 ? 32 : 64;
+  const int NT = mean_rows <= 24.0 ? 32 : (mean_rows <= 64.0 ? 64 : 128);
   CUtensorMap maps[4];
   if ((st = tc_make_map(&maps[0], xp, xp_rows, d, NT)) || (st = tc_make_map(&maps[1], w1, (uint64_t)E * 2 * F, d, kWRows)) ||
       (st = tc_make_map(&maps[2], act_ws, xp_rows, F, NT)) || (st = tc_make_map(&maps[3], w2, (uint64_t)E * d, F, kWRows)))
@@ -438,12 +441,14 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
   p.y = (__nv_bfloat16*)y;
   p.peers = y_peers;
   const int nkb2 = (F + kBK - 1) / kBK;
-  const int want = swap_splits(F);
+  const int want = xp_rows <= kSwapRowsMax ? swap_splits(F) : 1;  // partials sized for <= 512 rows
   p.kb_per_split = (nkb2 + want - 1) / want;
   p.nsplit = (nkb2 + p.kb_per_split - 1) / p.kb_per_split;  // every split non-empty
   p.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + kFfnHeaderBytes);
   p.part_rows = xp_rows;
-  if ((st = NT == 32 ? launch_swap<32>(maps, p, s) : launch_swap<64>(maps, p, s))) return st;
+  if ((st = NT == 32 ? launch_swap<32>(maps, p, s)
+                     : (NT == 64 ? launch_swap<64>(maps, p, s) : launch_swap<128>(maps, p, s))))
+    return st;
   if ((st = ffn_finalize(ws, nullptr, e_end, cursor_out, s))) return st;
   if (p.nsplit > 1) {
     const long long work = (long long)xp_rows * (d / 8);

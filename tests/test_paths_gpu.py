@@ -1,0 +1,73 @@
+"""Every bf16 expert-FFN code path, forced through the QMOE_SWAP_AB / QMOE_CTA_PAIR switches (read
+once per process, so each configuration runs in its own interpreter), against the torch fp32
+restatement of HF MixtralExperts on the same bf16 inputs: swap-AB with 32/64/128-row token tiles,
+the 1-CTA 128-row tcgen05 kernel and the CTA-pair 256-row kernel, plus a preempted launch and its
+resume on each path (bit-identical to the uninterrupted launch)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import json, sys
+import torch
+sys.path.insert(0, sys.argv[1])
+from paper_2503_09304_b200 import kernels as K
+res = []
+for (T, d, F, E, k) in json.loads(sys.argv[2]):
+    g = torch.Generator().manual_seed(T * 7 + E)
+    x = torch.randn((T, d), generator=g).bfloat16().cuda()
+    wr = (torch.randn((E, d), generator=g) / d ** 0.5).bfloat16().cuda()
+    gu = (torch.randn((E, 2 * F, d), generator=g) / d ** 0.5).bfloat16().cuda()
+    dn = (torch.randn((E, d, F), generator=g) / F ** 0.5).bfloat16().cuda()
+    ids, w = K.router(x, wr, k)
+    perm, offsets, xp = K.permute(ids, E, x=x)
+    y = torch.zeros((T * k, d), dtype=torch.bfloat16, device="cuda")
+    K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y)
+    oc = offsets.cpu().tolist()
+    ref = torch.zeros((T * k, d), device="cuda")
+    for e in range(E):
+        a, b = oc[e], oc[e + 1]
+        if a < b:
+            h = xp[a:b].float() @ gu[e].float().T
+            act = (torch.nn.functional.silu(h[:, :F]) * h[:, F:]).bfloat16().float()
+            ref[perm[a:b].long()] = act @ dn[e].float().T
+    rel = ((y.float() - ref).norm() / ref.norm()).item()
+    # preempt at the first boundary >= 3, resume from the cursor: must equal the full launch
+    flag = torch.full((1,), 3, dtype=torch.int32, device="cuda")
+    cur = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    y2 = torch.zeros_like(y)
+    K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y2, preempt_flag=flag, cursor_out=cur)
+    c = int(cur)
+    first = next((e for e in range(3, E) if oc[e + 1] > oc[e]), E)
+    done = perm[: oc[c]].long()
+    part_ok = c == first and torch.equal(y2[done], y[done])
+    K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y2, e_begin=c)
+    res.append({"shape": [T, d, F, E, k], "rel": rel, "stop": c, "want_stop": first, "partial_ok": part_ok,
+                "resume_identical": torch.equal(y2, y)})
+print(json.dumps(res))
+"""
+
+SHAPES = [(16, 1024, 2048, 8, 2), (160, 1024, 2048, 8, 2), (700, 1024, 2048, 8, 2), (1200, 512, 1408, 8, 2),
+          (2500, 512, 1024, 8, 2)]
+
+
+@pytest.mark.parametrize("env", [{"QMOE_SWAP_AB": "1"}, {"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "0"},
+                                 {"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "1"}],
+                         ids=["swap-ab", "tc-1cta", "tc-pair"])
+def test_forced_expert_path(cuda, env):
+    shapes = SHAPES if env.get("QMOE_SWAP_AB") == "1" else [s for s in SHAPES if s[0] * s[4] > 512]
+    out = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), json.dumps(shapes)], capture_output=True, text=True,
+                         env={**os.environ, **env}, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    for r in json.loads(out.stdout.strip().splitlines()[-1]):
+        assert r["rel"] < 1e-2, r
+        assert r["stop"] == r["want_stop"] and r["partial_ok"], r
+        assert r["resume_identical"], r
