@@ -400,8 +400,8 @@ int swap_splits(int F) {
 
 }  // namespace
 
-// Small batches: at most ~64 routed rows per expert on average (Mixtral decode up to 256 tokens,
-// Qwen up to ~1k tokens).  K-split down units need the split-K workspace, which is sized for at
+// Small batches: at most ~80 routed rows per expert on average (Mixtral decode up to 320 tokens,
+// Qwen up to ~1.2k tokens).  K-split down units need the split-K workspace, which is sized for at
 // most kSwapRowsMax rows (qmoe_expert_ffn_workspace_bytes).  QMOE_SWAP_AB=0/1 forces the choice.
 bool use_swap_ab(int xp_rows, int n_experts, int d, int F) {
   static int forced = [] {
@@ -411,7 +411,9 @@ bool use_swap_ab(int xp_rows, int n_experts, int d, int F) {
   (void)F;
   if (d % kWRows != 0 || F % kBK != 0 || n_experts < 1 || n_experts > kFfnMaxExperts) return false;
   if (forced >= 0) return forced == 1;
-  return xp_rows <= 64 * n_experts;
+  // measured crossover: Qwen (60 experts) 1k tokens (~68 rows per expert) is faster here, Mixtral
+  // 512 tokens (~128 per expert) on the 128/256-row tcgen05 tiles
+  return xp_rows <= 80 * n_experts;
 }
 
 int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
