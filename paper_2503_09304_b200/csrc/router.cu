@@ -11,7 +11,6 @@
 namespace qmoe {
 namespace {
 
-constexpr int kWarps = 8;      // warps per CTA
 constexpr int kExpChunk = 8;   // experts accumulated per pass over d
 constexpr int kMaxE = 64;
 
@@ -128,7 +127,7 @@ __device__ __noinline__ void select_token(const A* lg, A* s_score, int tok, int 
 // memory, fixed slice order); then one warp per token does the selection with warp-wide argmax
 // rounds.  Requires ceil(E/8) <= warps per group (checked by the host dispatch).
 // VEC: true -> 16-byte vector loads (requires d % Vec<T>::N == 0 and aligned rows).
-template <typename T, int TPC, int TPW, bool VEC>
+template <typename T, int TPC, int TPW, bool VEC, int kWarps = 8>
 __global__ void __launch_bounds__(kWarps * 32)
 router_kernel(const T* __restrict__ x, const T* __restrict__ wr, int ntok, int d, int E, int k,
               int mode, int32_t* __restrict__ ids_out, typename AccOf<T>::type* __restrict__ w_out,
@@ -225,7 +224,7 @@ router_kernel(const T* __restrict__ x, const T* __restrict__ wr, int ntok, int d
 }
 
 
-template <typename T, int TPC, int TPW>
+template <typename T, int TPC, int TPW, int NW = 8>
 int launch_router(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids,
                   void* w, void* logits, cudaStream_t s) {
   using A = typename AccOf<T>::type;
@@ -235,10 +234,10 @@ int launch_router(const void* x, const void* wr, int T_, int d, int E, int k, in
   const bool vec = (d % Vec<T>::N == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(wr) % 16 == 0);
   if (vec)
-    router_kernel<T, TPC, TPW, true><<<grid, kWarps * 32, 0, s>>>(
+    router_kernel<T, TPC, TPW, true, NW><<<grid, NW * 32, 0, s>>>(
         (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits, rounds);
   else
-    router_kernel<T, TPC, TPW, false><<<grid, kWarps * 32, 0, s>>>(
+    router_kernel<T, TPC, TPW, false, NW><<<grid, NW * 32, 0, s>>>(
         (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits, rounds);
   return check_launch("qmoe_router");
 }
@@ -397,7 +396,8 @@ int dispatch_router(const void* x, const void* wr, int T_, int d, int E, int k, 
         reinterpret_cast<uintptr_t>(wr) % 16 == 0)
       return launch_router_mma(x, wr, T_, d, E, k, mode, ids, w, logits, s);
   }
-  if (T_ < 148 * 8) return launch_router<T, 1, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  // decode: 16 warps on one token halve the dependent load rounds over d (Qwen: 8 chunks x 2 slices)
+  if (T_ < 148 * 8) return launch_router<T, 1, 1, 16>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
   if (nchunk == 1) return launch_router<T, 16, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
   if (nchunk == 2) return launch_router<T, 8, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
   if (nchunk <= 4) return launch_router<T, 4, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
