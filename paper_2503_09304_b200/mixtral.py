@@ -106,6 +106,7 @@ class DecoderMoEModel:
         self._cos, self._sin = emb.cos(), emb.sin()
         self._stop = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._meta, self._meta_key = None, None
+        self._shared_T, self._shared_off, self._shared_ident = -1, None, None
 
     # ------------------------------------------------------------------ cache geometry
     def kv_row_shape(self):
@@ -205,13 +206,19 @@ class DecoderMoEModel:
             L = self.layers[layer]
             T = x.shape[0]
             Fs = self.cfg.shared_ffn_dim
-            offsets = torch.tensor([0, T], dtype=torch.int32, device=self.device)
-            ident = torch.arange(T, dtype=torch.int32, device=self.device)
+            # one-expert problem over all T rows; cached per T so no per-layer H2D copy (a pageable
+            # torch.tensor(..., device=cuda) waits for the stream, i.e. for the grouped GEMM)
+            if self._shared_T != T:
+                self._shared_off = torch.arange(0, 2 * T, T, dtype=torch.int32, device=self.device)
+                self._shared_ident = torch.arange(T, dtype=torch.int32, device=self.device)
+                self._shared_T = T
+            offsets, ident = self._shared_off, self._shared_ident
             ys = torch.empty_like(x)
             act = K.workspace(T * Fs * 2, "act_shared", self.device).view(self.dtype)[: T * Fs].view(T, Fs)
             K.expert_ffn(K.EXPERT_SWIGLU, x, offsets, ident, L.sh_gate_up, L.sh_down, ys, act_ws=act)
-            gate = torch.sigmoid(x.float() @ L.sh_gate.float().T)
-            res = (res.float() + gate * ys.float()).to(self.dtype)
+            # res + sigmoid(g . x) * shared(x) as a one-slot combine (HF Qwen2MoeSparseMoeBlock)
+            gate = torch.sigmoid((x @ L.sh_gate.T).float())
+            res = K.combine(ys, gate, res)
         return K.combine(y, w, res)
 
     def emit_batch(self, h: torch.Tensor, rows: list[int]) -> list[int]:

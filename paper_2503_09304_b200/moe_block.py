@@ -94,7 +94,8 @@ class SparseMoeBlock(nn.Module):
     def _shared(self, x: torch.Tensor) -> torch.Tensor:
         T = x.shape[0]
         dev = x.device
-        offsets = torch.tensor([0, T], dtype=torch.int32, device=dev)
+        offsets = (torch.arange(0, 2 * T, T, dtype=torch.int32, device=dev) if T  # [0, T] without an H2D sync
+                   else torch.zeros(2, dtype=torch.int32, device=dev))
         perm = torch.arange(T, dtype=torch.int32, device=dev)
         ys = torch.empty_like(x)
         K.expert_ffn(K.EXPERT_SWIGLU, x, offsets, perm, self.shared_expert.gate_up_proj, self.shared_expert.down_proj,
@@ -115,8 +116,8 @@ class SparseMoeBlock(nn.Module):
                      act_ws=act)
         res = None if residual is None else residual.reshape(-1, d).contiguous()
         if self.shared_ffn_dim:
-            gate = torch.sigmoid((x.float() @ self.shared_expert_gate.weight.float().T))
-            shared = (self._shared(x).float() * gate).to(x.dtype)
-            res = shared if res is None else (res.float() + shared.float()).to(x.dtype)
+            # res + sigmoid(g . x) * shared(x): a one-slot combine on the shared expert's output
+            gate = torch.sigmoid((x @ self.shared_expert_gate.weight.T).float()).contiguous()
+            res = K.combine(self._shared(x), gate, res)
         self.last_routing = (ids, w)
         return K.combine(y, w, res).reshape(shape)

@@ -5,11 +5,12 @@ import torch
 from paper_2503_09304_b200.core import Phase, Priority, SchedulerDirective, batch_form, sequence_new
 from paper_2503_09304_b200.engine import InferenceEngine, VirtualClock, WallClock
 from paper_2503_09304_b200.kvcache import UnifiedDynamicCache
-from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, DecoderMoEModel
+from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, QWEN15_MOE_A27B, DecoderMoEModel
 
-m = DecoderMoEModel(MIXTRAL_8X7B)
+cfg = QWEN15_MOE_A27B if "qwen" in sys.argv[1:] else MIXTRAL_8X7B
+m = DecoderMoEModel(cfg)
 for dp in (False, True):
-    cache = UnifiedDynamicCache(32, m.kv_row_shape(), m.kv_dtype, m.device, m.kv_entry_bytes(), 64e9, **m.kv_page_kwargs)
+    cache = UnifiedDynamicCache(cfg.num_layers, m.kv_row_shape(), m.kv_dtype, m.device, m.kv_entry_bytes(), 64e9, **m.kv_page_kwargs)
     eng = InferenceEngine(m, cache, WallClock(), max_batch_size=32, device_preempt=dp)
     seqs = []
     for i in range(32):
@@ -21,11 +22,15 @@ for dp in (False, True):
     out = eng.execute(batch_form(seqs, Phase.PREFILL, 32, eng.next_batch_id()), seqs, cont)
     for s in seqs:
         s.generated.append(out.tokens[s.id]); s.advance_phase(Phase.DECODE)
-    ts = []
+    ts, gs = [], []
     for it in range(12):
         torch.cuda.synchronize(); t = time.perf_counter()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
         out = eng.execute(batch_form(seqs, Phase.DECODE, 32, eng.next_batch_id()), seqs, cont)
-        ts.append((time.perf_counter() - t) * 1e3)
+        b.record(); torch.cuda.synchronize()
+        ts.append((time.perf_counter() - t) * 1e3); gs.append(a.elapsed_time(b))
         for s in seqs:
             s.generated.append(out.tokens[s.id])
-    print(f"device_preempt={dp}: decode iteration ms {sorted(ts)[len(ts)//2]:.2f} (all {[round(x,1) for x in ts]})", flush=True)
+    print(f"{cfg.name} device_preempt={dp}: decode iteration ms {sorted(ts)[len(ts)//2]:.2f} "
+          f"(GPU span {sorted(gs)[len(gs)//2]:.2f})", flush=True)
