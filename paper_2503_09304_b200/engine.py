@@ -37,7 +37,7 @@ import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Union
 
-from .core import (Batch, Checkpoint, EngineReport, MemberProgress, Phase, SchedulerDirective, Sequence,
+from .core import (Batch, BatchProgress, Checkpoint, EngineReport, MemberProgress, Phase, SchedulerDirective, Sequence,
                    SimulationError, Stage, StateCorruptionError, batch_form)
 from .model import MemberRows
 
@@ -331,7 +331,7 @@ class InferenceEngine:
             members.append(MemberRows(seq, row, len(toks)))
             row += len(toks)
         st = _State(list(sequences), members, row)
-        st.progress = tuple(MemberProgress(s.id, s.priority, s.phase, len(s.generated)) for s in sequences)
+        st.progress = BatchProgress(MemberProgress(s.id, s.priority, s.phase, len(s.generated)) for s in sequences)
         ckpts = [s.checkpoint for s in sequences]
         if ckpts[0] is None:
             st.h = self.model.embed_batch([t for toks in inputs for t in toks])
