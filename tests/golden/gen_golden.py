@@ -79,8 +79,9 @@ class RandomPreempt:
                 else SchedulerDirective.CONTINUE)
 
 
-def record_run(trace, model_config, scheduler, mbs, policy=None, policy_spec=None):
-    """Run the reference with logging hooks; returns a JSON-able dict."""
+def record_run(trace, model_config, scheduler, mbs, policy=None, policy_spec=None, model_factory=None):
+    """Run the reference with logging hooks; returns a JSON-able dict.  model_factory (optional)
+    swaps in a routing-replay stub after construction."""
     log = []
     base_policy = policy if policy is not None else (POLICIES[scheduler] if scheduler in POLICIES else None)
 
@@ -93,6 +94,8 @@ def record_run(trace, model_config, scheduler, mbs, policy=None, policy_spec=Non
     if scheduler != "baseline":
         kwargs["policy"] = logged_policy
     sim = Simulation(trace, model_config=model_config, scheduler=scheduler, max_batch_size=mbs, **kwargs)
+    if model_factory is not None:
+        sim.model = sim.engine.model = model_factory(model_config)
     sch = sim.scheduler
     g = sch.get_next_batch
 
@@ -204,6 +207,54 @@ def gen_logs():
         print("log", *r)
 
 
+class ReplayStub(MoEModel):
+    """Reference-side routing-replay stub: the reference's own
+    engine, scheduler, driver and virtual clock run unchanged; route / route_many / emit_token
+    return the B200 run's recorded expert ids and tokens in call order and assert the call
+    (layer, token count) matches, so any schedule divergence surfaces at once."""
+
+    def __init__(self, cfg, routes, emits):
+        super().__init__(cfg)
+        self._routes, self._emits = list(routes), list(emits)
+        self._r = self._e = 0
+
+    def _next(self, layer, n):
+        rl, rn, ids = self._routes[self._r]
+        self._r += 1
+        assert (rl, rn) == (layer, n), f"replay diverged at route call {self._r - 1}: {(rl, rn)} vs {(layer, n)}"
+        return [{e: 1.0 / len(row) for e in row} for row in ids]
+
+    def route(self, h, layer):
+        return self._next(layer, 1)[0]
+
+    def route_many(self, H, layer):
+        return self._next(layer, len(H))
+
+    def emit_token(self, h):
+        t = self._emits[self._e]
+        self._e += 1
+        return t
+
+
+def gen_b200_ref():
+    """The reference's decision log for the B200 Mixtral-8x7B-shaped virtual-clock run recorded by
+    tools/record_virtual_run.py (logs/mixtral_b200_run.json.gz): same trace, same expert ids and
+    tokens replayed through the unmodified reference -> logs/mixtral_b200_ref.json.gz."""
+    from moesim.workload import TraceRecord
+
+    src = OUT / "logs" / "mixtral_b200_run.json.gz"
+    with gzip.open(src, "rt") as fh:
+        run = json.load(fh)
+    cfg = ModelConfig(**run["model"])
+    trace = [TraceRecord(i, a, Priority.from_tag(p), pl, mn, sd) for i, a, p, pl, mn, sd in run["trace"]]
+    rec = record_run(trace, cfg, run["scheduler"], run["max_batch_size"],
+                     model_factory=lambda c: ReplayStub(c, run["routes"], run["emits"]))
+    rec["source"] = "reference moesim replaying " + run["source"]
+    del rec["routes"], rec["emits"]  # identical to the run's by construction
+    write_json_gz(rec, OUT / "logs" / "mixtral_b200_ref.json.gz")
+    print("b200 ref log", len(rec["log"]), "events", rec["preemptions"], "preemptions", rec["makespan_ms"])
+
+
 def gen_tiny_layer():
     """Capture real router inputs of trace A's first prefill batch, then run the reference's
     router / queues / experts / combine on them."""
@@ -288,6 +339,11 @@ def gen_param_digests():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["b200"]:  # only the reference replay of the committed B200 run
+        gen_b200_ref()
+        sys.exit(0)
     gen_param_digests()
     gen_tiny_layer()
     gen_logs()
+    if (OUT / "logs" / "mixtral_b200_run.json.gz").exists():
+        gen_b200_ref()

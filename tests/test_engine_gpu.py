@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 import torch
 
+from conftest import ROOT
 from replay import load_log, policy_for, trace_of
 from oracle import moe_oracle as om
 from paper_2503_09304_b200.core import Phase, Priority, SchedulerDirective, Stage, batch_form, sequence_new
@@ -239,3 +240,30 @@ def test_device_flag_preemption_is_transparent_in_wall_clock_mode(cuda, name):
     res = sim.run()
     assert res.probes.preemptions > 0
     assert {str(k): s.generated for k, s in sorted(res.sequences.items())} == rec["tokens"]
+
+
+def test_b200_mixtral_virtual_run_is_reproducible(cuda):
+    """Re-run the recorded 32-layer Mixtral-8x7B-shaped virtual-clock trace on the B200 path: the
+    expert ids, tokens and decision log equal the committed recording, whose log the reference
+    reproduces bit for bit (test_decision_log.py::test_b200_mixtral_run_decision_log_matches_reference)."""
+    import gc
+    import importlib.util
+
+    from replay import load_log
+    from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, DecoderMoEModel
+
+    spec = importlib.util.spec_from_file_location("record_virtual_run", ROOT / "tools" / "record_virtual_run.py")
+    rv = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(rv)
+    want = load_log("mixtral_b200_run")
+    model = DecoderMoEModel(MIXTRAL_8X7B)
+    try:
+        got = rv.record(model)
+    finally:
+        del model
+        gc.collect()
+        torch.cuda.empty_cache()
+    assert got["routes"] == want["routes"]
+    assert got["emits"] == want["emits"]
+    assert [list(e) for e in got["log"]] == [list(e) for e in want["log"]]
+    assert got["makespan_ms"] == want["makespan_ms"]
