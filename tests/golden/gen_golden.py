@@ -236,13 +236,14 @@ class ReplayStub(MoEModel):
         return t
 
 
-def gen_b200_ref():
-    """The reference's decision log for the B200 Mixtral-8x7B-shaped virtual-clock run recorded by
-    tools/record_virtual_run.py (logs/mixtral_b200_run.json.gz): same trace, same expert ids and
-    tokens replayed through the unmodified reference -> logs/mixtral_b200_ref.json.gz."""
+def gen_b200_ref(name="mixtral"):
+    """The reference's decision log for a B200 virtual-clock run recorded by
+    tools/record_virtual_run.py (logs/<name>_b200_run.json.gz, Mixtral- or Qwen-shaped): same
+    trace, same expert ids and tokens replayed through the unmodified reference ->
+    logs/<name>_b200_ref.json.gz."""
     from moesim.workload import TraceRecord
 
-    src = OUT / "logs" / "mixtral_b200_run.json.gz"
+    src = OUT / "logs" / f"{name}_b200_run.json.gz"
     with gzip.open(src, "rt") as fh:
         run = json.load(fh)
     cfg = ModelConfig(**run["model"])
@@ -251,8 +252,8 @@ def gen_b200_ref():
                      model_factory=lambda c: ReplayStub(c, run["routes"], run["emits"]))
     rec["source"] = "reference moesim replaying " + run["source"]
     del rec["routes"], rec["emits"]  # identical to the run's by construction
-    write_json_gz(rec, OUT / "logs" / "mixtral_b200_ref.json.gz")
-    print("b200 ref log", len(rec["log"]), "events", rec["preemptions"], "preemptions", rec["makespan_ms"])
+    write_json_gz(rec, OUT / "logs" / f"{name}_b200_ref.json.gz")
+    print(name, "b200 ref log", len(rec["log"]), "events", rec["preemptions"], "preemptions", rec["makespan_ms"])
 
 
 def gen_tiny_layer():
@@ -339,11 +340,13 @@ def gen_param_digests():
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] == ["b200"]:  # only the reference replay of the committed B200 run
-        gen_b200_ref()
+    if sys.argv[1:2] == ["b200"]:  # only the reference replay of committed B200 runs
+        for name in sys.argv[2:] or ["mixtral", "qwen"]:
+            gen_b200_ref(name)
         sys.exit(0)
     gen_param_digests()
     gen_tiny_layer()
     gen_logs()
-    if (OUT / "logs" / "mixtral_b200_run.json.gz").exists():
-        gen_b200_ref()
+    for name in ("mixtral", "qwen"):
+        if (OUT / "logs" / f"{name}_b200_run.json.gz").exists():
+            gen_b200_ref(name)

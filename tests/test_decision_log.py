@@ -37,15 +37,17 @@ def test_decision_log_matches_reference(name):
     assert [[r.seq_id, r.first_token_ms, r.finish_ms] for r in res.records] == rec["records"]
 
 
-def test_b200_mixtral_run_decision_log_matches_reference():
+@pytest.mark.parametrize("name", ["mixtral", "qwen"])
+def test_b200_run_decision_log_matches_reference(name):
     """Big-shape decision-log parity (parity matrix row 2).  The B200 path
     (32-layer Mixtral-8x7B-shaped decoder, random-init bf16, real tcgen05 kernels, virtual clock)
     produced logs/mixtral_b200_run.json.gz (tools/record_virtual_run.py); the UNMODIFIED reference
     replayed the same trace with that run's expert ids and tokens and produced
     logs/mixtral_b200_ref.json.gz (tests/golden/gen_golden.py b200).  Selections, every report's
     virtual timestamp and directive, per-expert queue contents, preemption cursors, token routing
-    and job records must be identical."""
-    run, ref = load_log("mixtral_b200_run"), load_log("mixtral_b200_ref")
+    and job records must be identical.  Also for the 24-layer Qwen1.5-MoE-A2.7B shape (60 experts,
+    top-4, softmax->top-k routing), where the ratchet gives thousands of expert-boundary preemptions."""
+    run, ref = load_log(f"{name}_b200_run"), load_log(f"{name}_b200_ref")
     assert run["trace"] == ref["trace"]
     if run["log"] != ref["log"]:
         i, x, y = first_divergence(run["log"], ref["log"])
@@ -56,10 +58,11 @@ def test_b200_mixtral_run_decision_log_matches_reference():
     assert run["records"] == ref["records"]
 
 
-def test_b200_mixtral_run_replays_through_this_host_path():
+@pytest.mark.parametrize("name", ["mixtral", "qwen"])
+def test_b200_run_replays_through_this_host_path(name):
     """The same recorded ids/tokens through this repo's own engine + scheduler (routing-replay
     double) reproduce the run's log: the host control path alone accounts for the decisions."""
-    rec = load_log("mixtral_b200_run")
+    rec = load_log(f"{name}_b200_run")
     sim = Simulation(trace_of(rec), model=ReplayModel(rec), scheduler=rec["scheduler"],
                      max_batch_size=rec["max_batch_size"], policy=policy_for(rec), record_log=True)
     res = sim.run()

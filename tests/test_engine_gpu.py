@@ -242,21 +242,23 @@ def test_device_flag_preemption_is_transparent_in_wall_clock_mode(cuda, name):
     assert {str(k): s.generated for k, s in sorted(res.sequences.items())} == rec["tokens"]
 
 
-def test_b200_mixtral_virtual_run_is_reproducible(cuda):
-    """Re-run the recorded 32-layer Mixtral-8x7B-shaped virtual-clock trace on the B200 path: the
-    expert ids, tokens and decision log equal the committed recording, whose log the reference
-    reproduces bit for bit (test_decision_log.py::test_b200_mixtral_run_decision_log_matches_reference)."""
+@pytest.mark.parametrize("name", ["mixtral", "qwen"])
+def test_b200_virtual_run_is_reproducible(cuda, name):
+    """Re-run the recorded virtual-clock trace of the 32-layer Mixtral-8x7B-shaped / 24-layer
+    Qwen1.5-MoE-shaped decoder on the B200 path: the expert ids, tokens and decision log equal the
+    committed recording, whose log the reference reproduces bit for bit
+    (test_decision_log.py::test_b200_run_decision_log_matches_reference)."""
     import gc
     import importlib.util
 
     from replay import load_log
-    from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, DecoderMoEModel
+    from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, QWEN15_MOE_A27B, DecoderMoEModel
 
     spec = importlib.util.spec_from_file_location("record_virtual_run", ROOT / "tools" / "record_virtual_run.py")
     rv = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(rv)
-    want = load_log("mixtral_b200_run")
-    model = DecoderMoEModel(MIXTRAL_8X7B)
+    want = load_log(f"{name}_b200_run")
+    model = DecoderMoEModel(QWEN15_MOE_A27B if name == "qwen" else MIXTRAL_8X7B)
     try:
         got = rv.record(model)
     finally:

@@ -8,7 +8,7 @@ reference simulator (a routing-replay stub model) and records
 own decision log; tests/test_decision_log.py checks the two logs are identical, and
 tests/test_engine_gpu.py re-runs this recording and checks the B200 path reproduces it.
 
-    python tools/record_virtual_run.py tests/golden/logs/mixtral_b200_run.json.gz
+    python tools/record_virtual_run.py tests/golden/logs/mixtral_b200_run.json.gz [qwen]
 """
 from __future__ import annotations
 
@@ -23,7 +23,7 @@ sys.path.insert(0, str(ROOT))
 
 import torch  # noqa: E402
 
-from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, DecoderMoEModel  # noqa: E402
+from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, QWEN15_MOE_A27B, DecoderMoEModel  # noqa: E402
 from paper_2503_09304_b200.sim import Simulation  # noqa: E402
 from paper_2503_09304_b200.workload import WorkloadSpec, trace_for_rate  # noqa: E402
 
@@ -89,7 +89,7 @@ def record(model: DecoderMoEModel, scheduler: str = "qllm") -> dict:
 
 def main():
     out = Path(sys.argv[1])
-    model = DecoderMoEModel(MIXTRAL_8X7B)
+    model = DecoderMoEModel(QWEN15_MOE_A27B if "qwen" in sys.argv[2:] else MIXTRAL_8X7B)
     rec = record(model)
     out.parent.mkdir(parents=True, exist_ok=True)
     with gzip.open(out, "wt", encoding="utf-8") as fh:
