@@ -177,6 +177,7 @@ class InferenceEngine:
         self._pinned_off = None
         self._flags = None
         self._flag_slot = 0
+        self._on_expert_reports = None
 
     def next_batch_id(self) -> int:
         self._batch_counter += 1
@@ -198,7 +199,11 @@ class InferenceEngine:
         return batch
 
     # ------------------------------------------------------------------------------------------
-    def execute(self, batch: Batch, sequences: list[Sequence], on_report: ReportCallback) -> IterationOutcome:
+    def execute(self, batch: Batch, sequences: list[Sequence], on_report: ReportCallback,
+                on_expert_reports: Optional[Callable[[list[EngineReport]], Optional[int]]] = None) -> IterationOutcome:
+        """on_expert_reports (optional): answers the expert-boundary reports of one grouped launch
+        in order and returns the index of the first PREEMPT (wall-clock device-preempt path)."""
+        self._on_expert_reports = on_expert_reports
         if [s.id for s in sequences] != batch.members:
             raise SimulationError("sequence list does not match batch members")
         st = self._init_state(sequences)
@@ -301,18 +306,36 @@ class InferenceEngine:
         self.stats["expert_launches"] += 1
         self._off_ready.synchronize()  # waits for the permute only; the GEMM keeps running
         off = self._pinned_off.tolist()
-        for e in range(E):
-            n = off[e + 1] - off[e]
-            if n == 0:
-                continue
-            self._charge(self.cost.expert_cost(n))
-            if self._on_report(batch, st, layer, e, on_report) is PREEMPT:
-                # raise "stop at the first boundary >= e+1" while the kernel runs: an async H2D
-                # write on a side stream (copy engine), so expert e always completes
-                self._sig_src[slot] = e + 1
-                with torch.cuda.stream(self._sig_stream):
-                    flag.copy_(self._sig_src[slot:slot + 1], non_blocking=True)
-                return stop_dev, True
+        stop = None
+        # batched answers only on a wall clock (charges are no-ops there; a virtual clock charges
+        # experts one by one up to the preempting report, engine.py:215 in the reference)
+        if self._on_expert_reports is not None and not getattr(self.clock, "virtual", True):
+            hit, reports = [], []
+            for e in range(E):
+                n = off[e + 1] - off[e]
+                if n:
+                    self._charge(self.cost.expert_cost(n))
+                    hit.append(e)
+                    reports.append(self._report(batch, Stage.EXPERTS, layer, st, expert_id=e))
+            i = self._on_expert_reports(reports)
+            if i is not None:
+                stop = hit[i] + 1
+        else:
+            for e in range(E):
+                n = off[e + 1] - off[e]
+                if n == 0:
+                    continue
+                self._charge(self.cost.expert_cost(n))
+                if self._on_report(batch, st, layer, e, on_report) is PREEMPT:
+                    stop = e + 1
+                    break
+        if stop is not None:
+            # raise "stop at the first boundary >= stop" while the kernel runs: an async H2D write
+            # on a side stream (copy engine), so the reported expert always completes
+            self._sig_src[slot] = stop
+            with torch.cuda.stream(self._sig_stream):
+                flag.copy_(self._sig_src[slot:slot + 1], non_blocking=True)
+            return stop_dev, True
         return stop_dev, False
 
     def _on_report(self, batch, st, layer, expert, on_report):

@@ -217,7 +217,8 @@ class DecoderMoEModel:
             act = K.workspace(T * Fs * 2, "act_shared", self.device).view(self.dtype)[: T * Fs].view(T, Fs)
             K.expert_ffn(K.EXPERT_SWIGLU, x, offsets, ident, L.sh_gate_up, L.sh_down, ys, act_ws=act)
             # res + sigmoid(g . x) * shared(x) as a one-slot combine (HF Qwen2MoeSparseMoeBlock)
-            gate = torch.sigmoid((x @ L.sh_gate.T).float())
+            # the gate logit g . x is a one-expert router call (fp32 accumulate, no cuBLAS setup per layer)
+            gate = torch.sigmoid(K.router(x, L.sh_gate, 1, want_logits=True)[2])
             res = K.combine(ys, gate, res)
         return K.combine(y, w, res)
 

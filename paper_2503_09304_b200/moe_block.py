@@ -117,7 +117,7 @@ class SparseMoeBlock(nn.Module):
         res = None if residual is None else residual.reshape(-1, d).contiguous()
         if self.shared_ffn_dim:
             # res + sigmoid(g . x) * shared(x): a one-slot combine on the shared expert's output
-            gate = torch.sigmoid((x @ self.shared_expert_gate.weight.T).float()).contiguous()
+            gate = torch.sigmoid(K.router(x, self.shared_expert_gate.weight, 1, want_logits=True)[2])
             res = K.combine(self._shared(x), gate, res)
         self.last_routing = (ids, w)
         return K.combine(y, w, res).reshape(shape)
