@@ -65,6 +65,7 @@ combine_bf16_kernel(const __nv_bfloat16* __restrict__ y, const float* __restrict
   const int nv = d >> 3;  // uint4 per row
   const int per = (nv + parts - 1) / parts;
   const int v_end = min(nv, (part + 1) * per);
+#pragma unroll 2
   for (int v = part * per + lane; v < v_end; v += 32) {
     float acc[8];
     if (residual != nullptr) {
