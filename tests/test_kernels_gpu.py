@@ -209,7 +209,8 @@ def _swiglu_ref(xp, offsets, perm, gate_up, down, T, k, e_hi=None):
 @pytest.mark.parametrize("T,d,F,E,k", [(64, 1024, 2048, 8, 2), (1000, 512, 1408, 60, 4), (8, 4096, 14336, 8, 2),
                                        (2048, 4096, 14336, 8, 2), (1, 4096, 14336, 8, 2), (64, 2048, 1408, 60, 4),
                                        (256, 1024, 1024, 2, 1), (3, 512, 1024, 16, 2), (128, 2048, 1408, 60, 4),
-                                       (32, 4096, 14336, 8, 2), (200, 768, 640, 5, 2)])
+                                       (32, 4096, 14336, 8, 2), (200, 768, 640, 5, 2), (40, 512, 576, 4, 2),
+                                       (300, 384, 192, 3, 1)])
 def test_expert_swiglu_bf16_tcgen05_against_torch_fp32(cuda, T, d, F, E, k):
     """T*k <= 512 routed rows take the swap-AB single-launch kernel (expert_swap.cu, incl. multi
     token tiles per expert, empty experts, K-split down), larger batches the 128/256-row tiles."""
