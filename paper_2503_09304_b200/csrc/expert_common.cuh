@@ -149,6 +149,47 @@ __device__ __forceinline__ T* out_row(T* base, void* const* peers, int32_t v, si
   return base + (size_t)v * ld;
 }
 
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Single-launch gate_up + down kernels (expert_swap.cu, expert_fused.cu).  Claim the next unit:
+// gate_up units [0, N1) under the expert-boundary stop protocol of ffn_claim, then down units
+// [N1, N1 + N2).  Returns the global unit index or -1.
+__device__ __forceinline__ int two_phase_claim(const TileMap& m1, int N2, FfnWorkspace* ws, const volatile int32_t* flag,
+                                          int& last_e) {
+  const int N1 = m1.total;
+  while (true) {
+    const int t = atomicAdd(&ws->next, 1);
+    if (t >= N1) return t - N1 < N2 ? t : -1;
+    int local;
+    const int e = m1.expert_of(t, local);
+    if (flag != nullptr && e != last_e) {
+      const int s = *flag;
+      if (s > 0) {
+        int cand = local == 0 ? e : e + 1;
+        if (cand < s) cand = s;
+        atomicMax(&ws->stop_inv, INT_MAX - cand);
+      }
+    }
+    last_e = e;
+    const int stop = INT_MAX - ld_acquire(&ws->stop_inv);
+    if (e < stop) return t;
+    // every later gate_up unit belongs to an expert >= e >= stop: skip straight to the down units
+    atomicMax(&ws->next, N1);
+  }
+}
+
+// Down unit of expert e: true once all gate_up units of e stored their act rows, false if e can
+// no longer complete (the stop fell at or below it).
+__device__ __forceinline__ bool expert_ready(const int* done, int e, int need, const FfnWorkspace* ws) {
+  while (true) {
+    if (ld_acquire(done + e) >= need) return true;
+    if (INT_MAX - ld_acquire(&ws->stop_inv) <= e) return false;
+    __nanosleep(64);
+  }
+}
+
 int ffn_ws_reset(FfnWorkspace* ws, cudaStream_t s);
 // Extra workspace the bf16 SwiGLU path needs for split-K partials of the down projection.
 size_t splitk_bytes(int xp_rows, int d);
@@ -169,6 +210,13 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
                     void* const* y_peers, cudaStream_t s);
+
+// Mid-size batches (expert_fused.cu): 128 x 256 tiles, gate_up and down in one persistent launch.
+bool use_fused_tc();
+int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
+                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
+                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
+                     void* const* y_peers, cudaStream_t s);
 
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,

@@ -1,0 +1,295 @@
+// Grouped SwiGLU expert FFN with gate_up AND down in ONE persistent launch, 128 x 256 tcgen05
+// tiles (1 CTA per SM) -- the mid-size-batch / fine-grained-expert path.
+//
+// Replaces the reference's per-expert drain (engine.py:204-215 -> model.py:141-145) for the
+// north-star SwiGLU expert (HF MixtralExperts / Qwen2MoeExperts).
+//
+// The two-launch path (expert_tc.cu) ends the gate_up launch with a partial last wave, pays a
+// launch + prologue, and ends the down launch with another partial wave.  Here one unit counter
+// covers all gate_up tiles (expert-major, the reference's drain order) then all down tiles, and a
+// down tile of expert e waits on a per-expert completion counter (release/acquire, then an
+// async-proxy fence before TMA reads act) -- the protocol of the swap-AB kernel (expert_swap.cu),
+// with token rows on the MMA's M side:
+//   gate_up tile = (expert, 128 token rows, 128 F columns): B stacks the gate rows over the up rows
+//                  of those columns, so accumulator columns [0,128) = gate, [128,256) = up and the
+//                  epilogue writes SiLU(g)*u to act;
+//   down tile    = (expert, 128 token rows, 256 output columns), rows scattered to token slots
+//                  (or, expert parallel over peer memory, to the source rank's slot buffer).
+// Preemption: the device flag is read by gate_up claimers (expert_common.cuh); down tiles run for
+// exactly the experts below the stop.
+#include <cudaTypedefs.h>
+
+#include <stdlib.h>
+
+#include "expert_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace qmoe {
+namespace {
+
+constexpr int kBM = 128, kBN = 256, kBKf = 64;
+constexpr int kStagesF = 4;
+constexpr int kRingF = 4;
+constexpr int kThreadsF = 256;
+constexpr int kEpiF = 4;
+constexpr int kABytesF = kBM * kBKf * 2;                 // 16 KB
+constexpr int kStageBytesF = kABytesF + kBN * kBKf * 2;  // 48 KB
+constexpr int kSmemF = kStagesF * kStageBytesF + 1024;
+
+struct FusedParams {
+  int d, F;
+  int e_begin, e_end;
+  const int32_t* offsets;
+  const int32_t* perm;
+  const volatile int32_t* flag;
+  FfnWorkspace* ws;
+  int* done;
+  __nv_bfloat16* act;
+  __nv_bfloat16* y;
+  void* const* peers;
+};
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(kThreadsF, 1)
+ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
+                 const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW2,
+                 FusedParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStagesF], empty_bar[kStagesF];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t ring_full[kRingF], ring_empty[kRingF];
+  __shared__ int ring_tile[kRingF];
+  __shared__ uint32_t tmem_base_smem;
+  __shared__ TileMap map1, map2;
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kBM, kBN);
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt1 = (p.F + kBN / 2 - 1) / (kBN / 2);  // 128 act columns per gate_up tile
+  const int nt2 = (p.d + kBN - 1) / kBN;            // 256 output columns per down tile
+  const int nkb1 = (p.d + kBKf - 1) / kBKf, nkb2 = (p.F + kBKf - 1) / kBKf;
+
+  if (warp == 0) build_tile_map(map1, p.offsets, p.e_begin, p.e_end, nullptr, kBM, nt1);
+  if (warp == 3) build_tile_map(map2, p.offsets, p.e_begin, p.e_end, nullptr, kBM, nt2);
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < kStagesF; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull_bar[a], 1);
+      ptx::mbar_init(&tempty_bar[a], 4);
+    }
+    for (int i = 0; i < kRingF; ++i) {
+      ptx::mbar_init(&ring_full[i], 1);
+      ptx::mbar_init(&ring_empty[i], 1 + 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<2 * kBN>(&tmem_base_smem);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = tmem_base_smem;
+  const int N1 = map1.total, N2 = map2.total;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmX);
+      ptx::tma_prefetch_desc(&tmW1);
+      ptx::tma_prefetch_desc(&tmAct);
+      ptx::tma_prefetch_desc(&tmW2);
+      int stage = 0, slot = 0, last_e = -1;
+      uint32_t phase = 0, rphase = 0;
+      while (true) {
+        const int t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
+        int e = 0, m0 = 0, n0 = 0;
+        if (t >= N1) {
+          map2.locate(t - N1, kBM, nt2, kBN, e, m0, n0);
+          if (!expert_ready(p.done, e, map1.m_tiles[e - map1.e_first] * nt1 * 4, p.ws)) continue;
+          fence_proxy_async_global();  // act rows written by generic stores, read below by TMA
+        } else if (t >= 0) {
+          map1.locate(t, kBM, nt1, kBN / 2, e, m0, n0);
+        }
+        ptx::mbar_wait(&ring_empty[slot], rphase ^ 1);
+        ring_tile[slot] = t;
+        ptx::mbar_arrive(&ring_full[slot]);
+        if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+        if (t < 0) break;
+        const bool up = t < N1;
+        const CUtensorMap* ta = up ? &tmX : &tmAct;
+        const CUtensorMap* tb = up ? &tmW1 : &tmW2;
+        // B rows: gate_up -> gate [n0, +128) over up F + [n0, +128); down -> [n0, +256)
+        const int brow0 = up ? e * 2 * p.F + n0 : e * p.d + n0;
+        const int brow1 = up ? brow0 + p.F : brow0 + kBN / 2;
+        const int nkb = up ? nkb1 : nkb2;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytesF;
+          ptx::mbar_arrive_expect_tx(&full_bar[stage], kStageBytesF);
+          ptx::tma_load_2d(ta, &full_bar[stage], sa, kb * kBKf, m0, ptx::kEvictNormal);
+          ptx::tma_load_2d(tb, &full_bar[stage], sa + kABytesF, kb * kBKf, brow0, ptx::kEvictNormal);
+          ptx::tma_load_2d(tb, &full_bar[stage], sa + kABytesF + (kBN / 2) * 128, kb * kBKf, brow1,
+                           ptx::kEvictNormal);
+          if (++stage == kStagesF) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0, slot = 0, acc = 0;
+      uint32_t phase = 0, rphase = 0, aphase = 0;
+      while (true) {
+        ptx::mbar_wait(&ring_full[slot], rphase);
+        const int t = ring_tile[slot];
+        ptx::mbar_arrive(&ring_empty[slot]);
+        if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+        if (t < 0) break;
+        const int nkb = t < N1 ? nkb1 : nkb2;
+        ptx::mbar_wait(&tempty_bar[acc], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kBN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem + stage * kStageBytesF);
+          const uint32_t b_addr = a_addr + kABytesF;
+#pragma unroll
+          for (int k = 0; k < kBKf / 16; ++k)
+            ptx::tc_mma_bf16(d_tmem, ptx::sw128_kmajor_desc(a_addr + k * 32), ptx::sw128_kmajor_desc(b_addr + k * 32),
+                             kIdesc, (kb | k) != 0);
+          ptx::tc_commit(&empty_bar[stage]);
+          if (++stage == kStagesF) { stage = 0; phase ^= 1; }
+        }
+        ptx::tc_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kEpiF) {
+    // ------------------------------------------------------------------ epilogue
+    const int ew = warp - kEpiF;  // TMEM lanes [32*ew, 32*ew+32) = token rows of the tile
+    int slot = 0, acc = 0;
+    uint32_t rphase = 0, aphase = 0;
+    while (true) {
+      ptx::mbar_wait(&ring_full[slot], rphase);
+      const int t = ring_tile[slot];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&ring_empty[slot]);
+      if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+      if (t < 0) break;
+      const bool up = t < N1;
+      int e, m0, n0;
+      if (up) map1.locate(t, kBM, nt1, kBN / 2, e, m0, n0);
+      else map2.locate(t - N1, kBM, nt2, kBN, e, m0, n0);
+      const int row = m0 + ew * 32 + lane;
+      const bool valid = row < p.offsets[e + 1];
+      __nv_bfloat16* dst = nullptr;
+      if (valid) dst = up ? p.act + (size_t)row * p.F : out_row(p.y, p.peers, p.perm[row], p.d);
+      const int ncols = up ? p.F : p.d;
+      ptx::mbar_wait(&tfull_bar[acc], aphase);
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * kBN;
+      const int out_cols = up ? kBN / 2 : kBN;
+#pragma unroll 1
+      for (int c = 0; c < out_cols; c += 32) {
+        uint32_t v[32];
+        uint32_t packed[16];
+        ptx::tmem_ld32(t_row + c, v);
+        if (up) {
+          uint32_t u[32];
+          ptx::tmem_ld32(t_row + kBN / 2 + c, u);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float g0 = __uint_as_float(v[2 * i]), g1 = __uint_as_float(v[2 * i + 1]);
+            const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+            packed[i] = pack2(g0 / (1.f + __expf(-g0)) * u0, g1 / (1.f + __expf(-g1)) * u1);
+          }
+        } else {
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) packed[i] = pack2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        }
+        if (valid && n0 + c < ncols) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + n0 + c);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            d4[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+      if (up) {
+        // publish this warp's act rows to the down tiles of expert e (read by TMA: async proxy)
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.done + e, 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<2 * kBN>(tmem_base);
+  }
+}
+
+}  // namespace
+
+// The single-launch path for the 1-CTA tile shape (mid-size batches and fine-grained experts);
+// QMOE_FUSED=0/1 forces it off/on (tests compare the paths).
+bool use_fused_tc() {
+  static int forced = [] {
+    const char* v = getenv("QMOE_FUSED");
+    return v == nullptr ? -1 : atoi(v);
+  }();
+  return forced != 0;
+}
+
+int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
+                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
+                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
+                     void* const* y_peers, cudaStream_t s) {
+  int st;
+  if ((st = ffn_ws_reset(ws, s))) return st;
+  CUtensorMap maps[4];
+  if ((st = tc_make_map(&maps[0], xp, xp_rows, d, kBM)) ||
+      (st = tc_make_map(&maps[1], w1, (uint64_t)E * 2 * F, d, kBN / 2)) ||
+      (st = tc_make_map(&maps[2], act_ws, xp_rows, F, kBM)) ||
+      (st = tc_make_map(&maps[3], w2, (uint64_t)E * d, F, kBN / 2)))
+    return st;
+  FusedParams p{};
+  p.d = d;
+  p.F = F;
+  p.e_begin = e_begin;
+  p.e_end = e_end;
+  p.offsets = offsets;
+  p.perm = perm;
+  p.flag = flag;
+  p.ws = ws;
+  p.done = ffn_done(ws);
+  p.act = (__nv_bfloat16*)act_ws;
+  p.y = (__nv_bfloat16*)y;
+  p.peers = y_peers;
+  static bool attr_set = false;
+  if (!attr_set) {
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemF));
+    attr_set = true;
+  }
+  ffn_fused_kernel<<<tc_num_sms(), kThreadsF, kSmemF, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  if ((st = check_launch("qmoe_expert_ffn(tcgen05 single launch)"))) return st;
+  return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
+}
+
+}  // namespace qmoe

@@ -71,46 +71,6 @@ struct SwapCfg {
   static constexpr uint32_t kTmemCols = 4 * NT;  // 2 accumulator stages x (gate, up) x NT
 };
 
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-// Claim the next unit: gate_up units [0, N1) under the expert-boundary stop protocol of
-// ffn_claim, then down units [N1, N1 + N2).  Returns the global unit index or -1.
-__device__ __forceinline__ int swap_claim(const TileMap& m1, int N2, FfnWorkspace* ws, const volatile int32_t* flag,
-                                          int& last_e) {
-  const int N1 = m1.total;
-  while (true) {
-    const int t = atomicAdd(&ws->next, 1);
-    if (t >= N1) return t - N1 < N2 ? t : -1;
-    int local;
-    const int e = m1.expert_of(t, local);
-    if (flag != nullptr && e != last_e) {
-      const int s = *flag;
-      if (s > 0) {
-        int cand = local == 0 ? e : e + 1;
-        if (cand < s) cand = s;
-        atomicMax(&ws->stop_inv, INT_MAX - cand);
-      }
-    }
-    last_e = e;
-    const int stop = INT_MAX - ld_acquire(&ws->stop_inv);
-    if (e < stop) return t;
-    // every later gate_up unit belongs to an expert >= e >= stop: skip straight to the down units
-    atomicMax(&ws->next, N1);
-  }
-}
-
-// Down unit of expert e: true once all gate_up units of e stored their act rows, false if e can
-// no longer complete (the stop fell at or below it).
-__device__ __forceinline__ bool expert_ready(const int* done, int e, int need, const FfnWorkspace* ws) {
-  while (true) {
-    if (ld_acquire(done + e) >= need) return true;
-    if (INT_MAX - ld_acquire(&ws->stop_inv) <= e) return false;
-    __nanosleep(64);
-  }
-}
-
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.f + __expf(-g)) * u; }
 
 template <int NT>
@@ -168,7 +128,7 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
       int stage = 0, slot = 0, last_e = -1;
       uint32_t phase = 0, rphase = 0;
       while (true) {
-        int t = swap_claim(map1, N2, p.ws, p.flag, last_e);
+        int t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
         int e = 0, m0 = 0, n0 = 0, split = 0;
         if (t >= N1) {
           map2.locate(t - N1, NT, nt2 * p.nsplit, kWRows, e, m0, n0, p.nsplit, &split);

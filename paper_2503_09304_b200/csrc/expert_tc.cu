@@ -621,12 +621,15 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
     if ((st = launch_tc<BN, EPI_TANH>(ta, tb, p, s))) return st;
     return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
   }
+  const bool pair = use_cta_pair(xp_rows, e_end - e_begin);
+  if (!pair && down_splits(xp_rows, e_end - e_begin, d, F) == 1 && use_fused_tc())
+    return expert_ffn_fused(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
+                            xp_rows, y_peers, s);
   // gate_up: act[r, :F] = SiLU(x W1^T) * (x W3^T), expert order rows
   if ((st = make_map(&ta, xp, xp_rows, d, BM)) || (st = make_map(&tb, w1, (uint64_t)E * 2 * F, d, BN / 2))) return st;
   p.N = F; p.K = d; p.b_rows = 2 * F;
   p.out = (__nv_bfloat16*)act_ws; p.out_ld = F;
   p.ws = ws + 0;
-  const bool pair = use_cta_pair(xp_rows, e_end - e_begin);
   if ((st = pair ? launch_tc2<EPI_SWIGLU>(ta, tb, p, s) : launch_tc<BN, EPI_SWIGLU>(ta, tb, p, s))) return st;
   if ((st = ffn_finalize(ws + 0, nullptr, e_end, nullptr, s))) return st;
   // down: Y[perm[r], :d] = act[r] W2^T, only experts whose gate_up completed

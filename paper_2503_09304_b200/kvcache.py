@@ -64,7 +64,9 @@ class UnifiedDynamicCache:
         need = -(-upto // self.page_size)
         while len(pages) < need:
             if not self._free:
-                self._grow(self._n_pages * 2)
+                # grow by half: the copy keeps old and new pools alive at once, and a doubling of
+                # a multi-GB pool next to a 93 GB model runs out of HBM
+                self._grow(self._n_pages + max(1, self._n_pages // 2))
             pages.append(self._free.pop())
 
     def slots(self, handle: int, start: int, n: int) -> list[int]:

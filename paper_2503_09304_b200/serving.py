@@ -6,6 +6,7 @@ arrivals, 20% LS) seeded per rate exactly like the reference runner (cli.py:172-
 
 from __future__ import annotations
 
+import gc
 import time
 from dataclasses import replace
 from typing import Optional
@@ -41,6 +42,8 @@ def serve_once(model, trace, scheduler: str, max_batch_size: int = 32, slo_ms: f
         "engine": res.engine_stats,
     }
     del sim, res
+    gc.collect()  # the run's KV page pools sit in reference cycles; free them before the next run
+    torch.cuda.empty_cache()
     return out
 
 

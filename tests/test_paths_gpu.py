@@ -50,8 +50,10 @@ for (T, d, F, E, k) in json.loads(sys.argv[2]):
     done = perm[: oc[c]].long()
     part_ok = c == first and torch.equal(y2[done], y[done])
     K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y2, e_begin=c)
+    import hashlib
     res.append({"shape": [T, d, F, E, k], "rel": rel, "stop": c, "want_stop": first, "partial_ok": part_ok,
-                "resume_identical": torch.equal(y2, y)})
+                "resume_identical": torch.equal(y2, y),
+                "sha": hashlib.sha1(y.view(torch.int16).cpu().numpy().tobytes()).hexdigest()})
 print(json.dumps(res))
 """
 
@@ -59,15 +61,29 @@ SHAPES = [(16, 1024, 2048, 8, 2), (160, 1024, 2048, 8, 2), (700, 1024, 2048, 8, 
           (2500, 512, 1024, 8, 2)]
 
 
-@pytest.mark.parametrize("env", [{"QMOE_SWAP_AB": "1"}, {"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "0"},
-                                 {"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "1"}],
-                         ids=["swap-ab", "tc-1cta", "tc-pair"])
-def test_forced_expert_path(cuda, env):
-    shapes = SHAPES if env.get("QMOE_SWAP_AB") == "1" else [s for s in SHAPES if s[0] * s[4] > 512]
+def _run(env, shapes):
     out = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), json.dumps(shapes)], capture_output=True, text=True,
                          env={**os.environ, **env}, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
-    for r in json.loads(out.stdout.strip().splitlines()[-1]):
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    for r in res:
         assert r["rel"] < 1e-2, r
         assert r["stop"] == r["want_stop"] and r["partial_ok"], r
         assert r["resume_identical"], r
+    return res
+
+
+@pytest.mark.parametrize("env", [{"QMOE_SWAP_AB": "1"}, {"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "0"},
+                                 {"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "1"}],
+                         ids=["swap-ab", "tc-1cta-single-launch", "tc-pair"])
+def test_forced_expert_path(cuda, env):
+    _run(env, SHAPES if env.get("QMOE_SWAP_AB") == "1" else [s for s in SHAPES if s[0] * s[4] > 512])
+
+
+def test_single_launch_equals_two_launches(cuda):
+    """The 1-CTA single-launch kernel (expert_fused.cu) computes every tile exactly like the
+    two-launch 1-CTA path (same tiles, same MMA order, same epilogue): outputs are bit-identical."""
+    shapes = [s for s in SHAPES if s[0] * s[4] > 512]
+    one = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "0"}, shapes)
+    two = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "0", "QMOE_FUSED": "0"}, shapes)
+    assert [r["sha"] for r in one] == [r["sha"] for r in two]
