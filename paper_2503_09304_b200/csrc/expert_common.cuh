@@ -211,12 +211,13 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
                     void* const* y_peers, cudaStream_t s);
 
-// Mid-size batches (expert_fused.cu): 128 x 256 tiles, gate_up and down in one persistent launch.
+// Mid-size and large batches (expert_fused.cu): 128 x 256 (1 CTA) or 256 x 256 (CTA pair) tiles,
+// gate_up and down in one persistent launch.
 bool use_fused_tc();
 int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                      const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                     void* const* y_peers, cudaStream_t s);
+                     void* const* y_peers, bool pair, cudaStream_t s);
 
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,

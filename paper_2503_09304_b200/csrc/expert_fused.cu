@@ -245,6 +245,229 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
   }
 }
 
+// ================================================================================================
+// CTA-pair (cta_group::2) variant: 256 token rows x 256 B rows per tile, one tile per cluster of 2.
+// Same protocol as ffn_tc2_kernel (expert_tc.cu): the leader claims tiles (two_phase_claim) and
+// publishes them to both CTAs' rings over DSMEM, both CTAs' TMA loads complete on the leader's
+// barrier, the leader issues tcgen05.mma.cta_group::2 with multicast commits.  A down tile of
+// expert e is published only once the leader saw every gate_up tile of e complete (8 epilogue
+// warps per pair tile arrive); the peer re-acquires the counter before its async-proxy fence.
+constexpr int kStagesP = 6;
+constexpr int kHalfP = 128 * kBKf * 2;  // 16 KB: this CTA's A rows, and separately its B rows
+constexpr int kStageBytesP = 2 * kHalfP;
+constexpr int kSmemP = kStagesP * kStageBytesP + 1024;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsF, 1)
+ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
+                      const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW2,
+                      FusedParams p) {
+  constexpr int kBMp = 256;
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kBMp, kBN);
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStagesP], empty_bar[kStagesP];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t ring_full[kRingF], ring_empty[kRingF];
+  __shared__ int ring_tile[kRingF];
+  __shared__ uint32_t tmem_base_smem;
+  __shared__ TileMap map1, map2;
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int nt1 = (p.F + kBN / 2 - 1) / (kBN / 2), nt2 = (p.d + kBN - 1) / kBN;
+  const int nkb1 = (p.d + kBKf - 1) / kBKf, nkb2 = (p.F + kBKf - 1) / kBKf;
+
+  if (warp == 0) build_tile_map(map1, p.offsets, p.e_begin, p.e_end, nullptr, kBMp, nt1);
+  if (warp == 3) build_tile_map(map2, p.offsets, p.e_begin, p.e_end, nullptr, kBMp, nt2);
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < kStagesP; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull_bar[a], 1);
+      ptx::mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    for (int i = 0; i < kRingF; ++i) {
+      ptx::mbar_init(&ring_full[i], 1);
+      ptx::mbar_init(&ring_empty[i], 10);  // leader: MMA + 4 epi; peer: producer + 4 epi
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_cg2<2 * kBN>(&tmem_base_smem);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = tmem_base_smem;
+  const int N1 = map1.total, N2 = map2.total;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmX);
+      ptx::tma_prefetch_desc(&tmW1);
+      ptx::tma_prefetch_desc(&tmAct);
+      ptx::tma_prefetch_desc(&tmW2);
+      int stage = 0, slot = 0, last_e = -1;
+      uint32_t phase = 0, rphase = 0;
+      while (true) {
+        int t;
+        int e = 0, m0 = 0, n0 = 0;
+        if (leader) {
+          t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
+          if (t >= N1) {
+            map2.locate(t - N1, kBMp, nt2, kBN, e, m0, n0);
+            if (!expert_ready(p.done, e, map1.m_tiles[e - map1.e_first] * nt1 * 8, p.ws)) continue;
+            fence_proxy_async_global();
+          }
+          ptx::mbar_wait_cluster(&ring_empty[slot], rphase ^ 1);
+          ring_tile[slot] = t;
+          ptx::st_remote_u32(&ring_tile[slot], 1, (uint32_t)t);
+          ptx::mbar_arrive(&ring_full[slot]);
+          ptx::mbar_arrive_remote(&ring_full[slot], 1);
+        } else {
+          ptx::mbar_wait_cluster(&ring_full[slot], rphase);
+          t = ring_tile[slot];
+          ptx::mbar_arrive_remote(&ring_empty[slot], 0);
+          if (t >= N1) {
+            map2.locate(t - N1, kBMp, nt2, kBN, e, m0, n0);
+            (void)ld_acquire(p.done + e);  // the leader saw it complete; acquire it here too
+            fence_proxy_async_global();
+          }
+        }
+        if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+        if (t < 0) break;
+        const bool up = t < N1;
+        if (up) map1.locate(t, kBMp, nt1, kBN / 2, e, m0, n0);
+        const CUtensorMap* ta = up ? &tmX : &tmAct;
+        const CUtensorMap* tb = up ? &tmW1 : &tmW2;
+        const int arow = m0 + (int)rank * 128;
+        // this CTA's 128 B rows: gate_up -> CTA0 gate [n0, +128), CTA1 up F + [n0, +128);
+        // down -> rows n0 + rank*128 of expert e
+        const int brow = up ? e * 2 * p.F + (rank ? p.F : 0) + n0 : e * p.d + n0 + (int)rank * 128;
+        const int nkb = up ? nkb1 : nkb2;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait_cluster(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytesP;
+          if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytesP);
+          ptx::tma_load_2d_cg2(ta, &full_bar[stage], sa, kb * kBKf, arow, ptx::kEvictNormal);
+          ptx::tma_load_2d_cg2(tb, &full_bar[stage], sa + kHalfP, kb * kBKf, brow, ptx::kEvictNormal);
+          if (++stage == kStagesP) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      int stage = 0, slot = 0, acc = 0;
+      uint32_t phase = 0, rphase = 0, aphase = 0;
+      while (true) {
+        ptx::mbar_wait_cluster(&ring_full[slot], rphase);
+        const int t = ring_tile[slot];
+        ptx::mbar_arrive(&ring_empty[slot]);
+        if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+        if (t < 0) break;
+        const int nkb = t < N1 ? nkb1 : nkb2;
+        ptx::mbar_wait_cluster(&tempty_bar[acc], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kBN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem + stage * kStageBytesP);
+          const uint32_t b_addr = a_addr + kHalfP;
+#pragma unroll
+          for (int k = 0; k < kBKf / 16; ++k)
+            ptx::tc_mma_bf16_cg2(d_tmem, ptx::sw128_kmajor_desc(a_addr + k * 32),
+                                 ptx::sw128_kmajor_desc(b_addr + k * 32), kIdesc, (kb | k) != 0);
+          ptx::tc_commit_cg2(&empty_bar[stage], 0x3);
+          if (++stage == kStagesP) { stage = 0; phase ^= 1; }
+        }
+        ptx::tc_commit_cg2(&tfull_bar[acc], 0x3);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kEpiF) {
+    // ------------------------------------------------------------------ epilogue (both CTAs)
+    const int ew = warp - kEpiF;
+    int slot = 0, acc = 0;
+    uint32_t rphase = 0, aphase = 0;
+    while (true) {
+      ptx::mbar_wait_cluster(&ring_full[slot], rphase);
+      const int t = ring_tile[slot];
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&ring_empty[slot]);
+        else ptx::mbar_arrive_remote(&ring_empty[slot], 0);
+      }
+      if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+      if (t < 0) break;
+      const bool up = t < N1;
+      int e, m0, n0;
+      if (up) map1.locate(t, kBMp, nt1, kBN / 2, e, m0, n0);
+      else map2.locate(t - N1, kBMp, nt2, kBN, e, m0, n0);
+      const int row = m0 + (int)rank * 128 + ew * 32 + lane;
+      const bool valid = row < p.offsets[e + 1];
+      __nv_bfloat16* dst = nullptr;
+      if (valid) dst = up ? p.act + (size_t)row * p.F : out_row(p.y, p.peers, p.perm[row], p.d);
+      const int ncols = up ? p.F : p.d;
+      ptx::mbar_wait_cluster(&tfull_bar[acc], aphase);
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * kBN;
+      const int out_cols = up ? kBN / 2 : kBN;
+#pragma unroll 1
+      for (int c = 0; c < out_cols; c += 32) {
+        uint32_t v[32];
+        uint32_t packed[16];
+        ptx::tmem_ld32(t_row + c, v);
+        if (up) {
+          uint32_t u[32];
+          ptx::tmem_ld32(t_row + kBN / 2 + c, u);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float g0 = __uint_as_float(v[2 * i]), g1 = __uint_as_float(v[2 * i + 1]);
+            const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+            packed[i] = pack2(g0 / (1.f + __expf(-g0)) * u0, g1 / (1.f + __expf(-g1)) * u1);
+          }
+        } else {
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) packed[i] = pack2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        }
+        if (valid && n0 + c < ncols) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + n0 + c);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            d4[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&tempty_bar[acc]);
+        else ptx::mbar_arrive_remote(&tempty_bar[acc], 0);
+      }
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+      if (up) {
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.done + e, 1);
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg2<2 * kBN>(tmem_base);
+  }
+}
+
 }  // namespace
 
 // The single-launch path for the 1-CTA tile shape (mid-size batches and fine-grained experts);
@@ -260,10 +483,11 @@ bool use_fused_tc() {
 int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                      const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                     void* const* y_peers, cudaStream_t s) {
+                     void* const* y_peers, bool pair, cudaStream_t s) {
   int st;
   if ((st = ffn_ws_reset(ws, s))) return st;
   CUtensorMap maps[4];
+  // A boxes: 128 token rows (each CTA of a pair loads its own 128); B boxes: 128 weight rows
   if ((st = tc_make_map(&maps[0], xp, xp_rows, d, kBM)) ||
       (st = tc_make_map(&maps[1], w1, (uint64_t)E * 2 * F, d, kBN / 2)) ||
       (st = tc_make_map(&maps[2], act_ws, xp_rows, F, kBM)) ||
@@ -285,9 +509,13 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
   static bool attr_set = false;
   if (!attr_set) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemF));
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_fused_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemP));
     attr_set = true;
   }
-  ffn_fused_kernel<<<tc_num_sms(), kThreadsF, kSmemF, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  if (pair)
+    ffn_fused_pair_kernel<<<(tc_num_sms() / 2) * 2, kThreadsF, kSmemP, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  else
+    ffn_fused_kernel<<<tc_num_sms(), kThreadsF, kSmemF, s>>>(maps[0], maps[1], maps[2], maps[3], p);
   if ((st = check_launch("qmoe_expert_ffn(tcgen05 single launch)"))) return st;
   return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
 }

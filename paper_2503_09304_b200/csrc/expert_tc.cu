@@ -622,9 +622,9 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
     return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
   }
   const bool pair = use_cta_pair(xp_rows, e_end - e_begin);
-  if (!pair && down_splits(xp_rows, e_end - e_begin, d, F) == 1 && use_fused_tc())
+  if (down_splits(xp_rows, e_end - e_begin, d, F) == 1 && use_fused_tc())
     return expert_ffn_fused(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
-                            xp_rows, y_peers, s);
+                            xp_rows, y_peers, pair, s);
   // gate_up: act[r, :F] = SiLU(x W1^T) * (x W3^T), expert order rows
   if ((st = make_map(&ta, xp, xp_rows, d, BM)) || (st = make_map(&tb, w1, (uint64_t)E * 2 * F, d, BN / 2))) return st;
   p.N = F; p.K = d; p.b_rows = 2 * F;

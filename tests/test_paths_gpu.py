@@ -80,10 +80,11 @@ def test_forced_expert_path(cuda, env):
     _run(env, SHAPES if env.get("QMOE_SWAP_AB") == "1" else [s for s in SHAPES if s[0] * s[4] > 512])
 
 
-def test_single_launch_equals_two_launches(cuda):
-    """The 1-CTA single-launch kernel (expert_fused.cu) computes every tile exactly like the
-    two-launch 1-CTA path (same tiles, same MMA order, same epilogue): outputs are bit-identical."""
+@pytest.mark.parametrize("pair", ["0", "1"], ids=["1cta", "cta-pair"])
+def test_single_launch_equals_two_launches(cuda, pair):
+    """The single-launch kernels (expert_fused.cu, 1-CTA and CTA pair) compute every tile exactly
+    like the two-launch paths (same tiles, same MMA order, same epilogue): bit-identical outputs."""
     shapes = [s for s in SHAPES if s[0] * s[4] > 512]
-    one = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "0"}, shapes)
-    two = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "0", "QMOE_FUSED": "0"}, shapes)
+    one = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": pair}, shapes)
+    two = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": pair, "QMOE_FUSED": "0"}, shapes)
     assert [r["sha"] for r in one] == [r["sha"] for r in two]
