@@ -70,6 +70,14 @@ extern "C" {
 #define QMOE_EXPERT_TANH_AFFINE 0 /* y = tanh(A_e x + b_e)          (model.py:141-145)        */
 #define QMOE_EXPERT_SWIGLU 1      /* y = W2_e (SiLU(W1_e x) * W3_e x) (HF MixtralExperts)      */
 
+/* ---- bf16 SwiGLU kernel paths (qmoe_expert_ffn_path) ----------------------------------- */
+#define QMOE_PATH_UNSUPPORTED 0       /* d or F not a multiple of 64                              */
+#define QMOE_PATH_SWAP_AB 1           /* decode-size batches: swap-AB, gate_up+down in one launch  */
+#define QMOE_PATH_FUSED_1CTA 2        /* 128x256 tcgen05 tiles, gate_up+down in one launch         */
+#define QMOE_PATH_FUSED_PAIR 3        /* 256x256 CTA-pair tiles, gate_up+down in one launch        */
+#define QMOE_PATH_TWO_LAUNCH_1CTA 4   /* 128x256 tiles, one launch per projection (split-K small)  */
+#define QMOE_PATH_TWO_LAUNCH_PAIR 5   /* 256x256 CTA-pair tiles, one launch per projection         */
+
 QMOE_API int qmoe_version(void);
 QMOE_API const char* qmoe_status_string(int status);
 /* Text of the last error raised on the calling thread (CUDA error string or validation msg). */
@@ -124,6 +132,28 @@ QMOE_API int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int32
                     int e_begin, int e_end, int xp_rows, void* act_ws, void* y,
                     const volatile int32_t* preempt_flag, int32_t* cursor_out, void* workspace,
                     size_t workspace_bytes, void* stream);
+
+/*
+ * Kernel path qmoe_expert_ffn takes for a bf16 SwiGLU launch over all E experts of xp_rows routed
+ * rows (QMOE_PATH_*).  Host-only, no device work.
+ */
+QMOE_API int qmoe_expert_ffn_path(int d, int F, int E, int xp_rows);
+/*
+ * Grouped bf16 SwiGLU experts reading the token rows straight from X (no gathered Xp): the i-th
+ * row of expert e is X[perm[offsets[e] + i] / k], loaded by the GEMM's producer warp with TMA
+ * tile::gather4 (4 arbitrary rows per instruction) -- the permute's row gather fused into the
+ * A-operand load.  Only for the single-launch tcgen05 paths (QMOE_PATH_FUSED_1CTA / _PAIR for
+ * xp_rows = T*k); other paths return QMOE_ERR_UNSUPPORTED (callers gather with qmoe_permute).
+ * Measured on B200 it is ~2x SLOWER than qmoe_permute's gather + qmoe_expert_ffn (32 gather4
+ * instructions per 64-wide K step per CTA saturate the TMA issue path, where the Xp tile is one
+ * instruction), so the host paths do not use it; it serves callers that cannot afford the
+ * T*k*d Xp buffer.
+ * Same outputs, preemption flag, cursor and workspace as qmoe_expert_ffn (xp_rows = T*k).
+ */
+QMOE_API int qmoe_expert_ffn_gather(const void* x, int T, int k, const int32_t* offsets, const int32_t* perm, int E,
+                                    int d, int F, const void* gate_up, const void* down, int e_begin, int e_end,
+                                    void* act_ws, void* y, const volatile int32_t* preempt_flag, int32_t* cursor_out,
+                                    void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Combine (replaces InferenceEngine._finish_layer, engine.py:330-365, and MoEModel.combine,

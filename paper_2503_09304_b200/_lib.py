@@ -34,6 +34,13 @@ QMOE_ROUTE_SOFTMAX_TOPK = 1
 QMOE_EXPERT_TANH_AFFINE = 0
 QMOE_EXPERT_SWIGLU = 1
 
+QMOE_PATH_UNSUPPORTED = 0
+QMOE_PATH_SWAP_AB = 1
+QMOE_PATH_FUSED_1CTA = 2
+QMOE_PATH_FUSED_PAIR = 3
+QMOE_PATH_TWO_LAUNCH_1CTA = 4
+QMOE_PATH_TWO_LAUNCH_PAIR = 5
+
 _c_int = ctypes.c_int
 _c_size = ctypes.c_size_t
 _vp = ctypes.c_void_p
@@ -57,6 +64,9 @@ SIGNATURES = {
     "qmoe_kv_gather": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),
     "qmoe_rmsnorm": (_c_int, [_vp, _vp, _vp, ctypes.c_float, _c_int, _c_int, _vp, _vp, _vp]),
     "qmoe_rope": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "qmoe_expert_ffn_path": (_c_int, [_c_int, _c_int, _c_int, _c_int]),
+    "qmoe_expert_ffn_gather": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int,
+                                        _c_int, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
     "qmoe_ipc_export": (_c_int, [_vp, _vp, ctypes.POINTER(_c_size)]),
     "qmoe_ipc_import": (_c_int, [_vp, _c_size, ctypes.POINTER(_vp)]),
     "qmoe_ep_dispatch": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_size, _c_int, _vp, _vp, _vp, _vp, _vp]),

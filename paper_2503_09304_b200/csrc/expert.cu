@@ -90,3 +90,39 @@ extern "C" int qmoe_expert_ffn_peer(const void* xp, const int32_t* offsets, cons
                           act_ws, const_cast<void*>(static_cast<const void*>(y_peers)), nullptr, nullptr, workspace,
                           workspace_bytes, y_peers, stream);
 }
+
+extern "C" int qmoe_expert_ffn_path(int d, int F, int E, int xp_rows) { return qmoe::expert_ffn_path(d, F, E, xp_rows); }
+
+extern "C" int qmoe_expert_ffn_gather(const void* x, int T, int k, const int32_t* offsets, const int32_t* perm, int E,
+                                      int d, int F, const void* gate_up, const void* down, int e_begin, int e_end,
+                                      void* act_ws, void* y, const volatile int32_t* preempt_flag,
+                                      int32_t* cursor_out, void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(T >= 0 && k >= 1 && k <= 8 && E >= 1 && E <= 64 && d >= 1 && F >= 1,
+               "qmoe_expert_ffn_gather: bad sizes T=%d k=%d E=%d d=%d F=%d", T, k, E, d, F);
+  QMOE_REQUIRE(0 <= e_begin && e_begin <= e_end && e_end <= E, "qmoe_expert_ffn_gather: bad expert range [%d, %d)",
+               e_begin, e_end);
+  const int rows = T * k;
+  QMOE_REQUIRE(workspace != nullptr &&
+                   workspace_bytes >= qmoe_expert_ffn_workspace_bytes(QMOE_EXPERT_SWIGLU, QMOE_BF16, d, rows),
+               "qmoe_expert_ffn_gather: workspace too small");
+  FfnWorkspace* ws = reinterpret_cast<FfnWorkspace*>(workspace);
+  cudaStream_t s = as_stream(stream);
+  if (rows == 0 || e_begin == e_end) {
+    int st = ffn_ws_reset(ws, s);
+    if (st) return st;
+    return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
+  }
+  QMOE_REQUIRE(x && offsets && perm && gate_up && down && act_ws && y, "qmoe_expert_ffn_gather: null pointer");
+  QMOE_REQUIRE(((uintptr_t)x | (uintptr_t)gate_up | (uintptr_t)y | (uintptr_t)act_ws) % 16 == 0,
+               "qmoe_expert_ffn_gather: buffers must be 16-byte aligned");
+  const int path = expert_ffn_path(d, F, E, rows);
+  if (path != QMOE_PATH_FUSED_1CTA && path != QMOE_PATH_FUSED_PAIR) {
+    set_error("qmoe_expert_ffn_gather: path %d has no fused row gather (use qmoe_permute's gather)", path);
+    return QMOE_ERR_UNSUPPORTED;
+  }
+  int st = tc_init_driver();
+  if (st) return st;
+  return expert_ffn_fused(nullptr, offsets, perm, E, d, F, gate_up, down, e_begin, e_end, act_ws, y, preempt_flag,
+                          cursor_out, ws, rows, nullptr, path == QMOE_PATH_FUSED_PAIR, x, T, k, s);
+}

@@ -217,7 +217,9 @@ bool use_fused_tc();
 int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                      const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                     void* const* y_peers, bool pair, cudaStream_t s);
+                     void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s);
+// Which bf16 SwiGLU kernel qmoe_expert_ffn runs for this shape (QMOE_PATH_* in qmoe.h).
+int expert_ffn_path(int d, int F, int E, int xp_rows);
 
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,

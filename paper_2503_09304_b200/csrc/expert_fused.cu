@@ -47,7 +47,19 @@ struct FusedParams {
   __nv_bfloat16* act;
   __nv_bfloat16* y;
   void* const* peers;
+  int k;       // top-k: gate_up A rows are x[perm[r] / k] when gather != 0
+  int gather;  // 1: gate_up A tiles are gathered from X by the producer warp (TMA tile::gather4)
 };
+
+// Token rows of one 128-row A tile for the gather: lane l owns rows [4l, 4l+4) of the tile; rows
+// past the expert's queue read token 0 (their results are never stored).
+__device__ __forceinline__ void gather_rows4(const FusedParams& p, int m0, int row_end, int lane, int (&g)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int r = m0 + 4 * lane + j;
+    g[j] = r < row_end ? p.perm[r] / p.k : 0;
+  }
+}
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -98,49 +110,65 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
   const int N1 = map1.total, N2 = map2.total;
 
   if (warp == 0) {
-    // ------------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------------ TMA producer (warp-wide:
+    // lane 0 claims and issues the tile loads; in gather mode all 32 lanes issue tile::gather4)
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmX);
       ptx::tma_prefetch_desc(&tmW1);
       ptx::tma_prefetch_desc(&tmAct);
       ptx::tma_prefetch_desc(&tmW2);
-      int stage = 0, slot = 0, last_e = -1;
-      uint32_t phase = 0, rphase = 0;
-      while (true) {
-        const int t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
-        int e = 0, m0 = 0, n0 = 0;
-        if (t >= N1) {
-          map2.locate(t - N1, kBM, nt2, kBN, e, m0, n0);
-          if (!expert_ready(p.done, e, map1.m_tiles[e - map1.e_first] * nt1 * 4, p.ws)) continue;
-          fence_proxy_async_global();  // act rows written by generic stores, read below by TMA
-        } else if (t >= 0) {
-          map1.locate(t, kBM, nt1, kBN / 2, e, m0, n0);
+    }
+    int stage = 0, slot = 0, last_e = -1;
+    uint32_t phase = 0, rphase = 0;
+    while (true) {
+      int t = -1;
+      if (lane == 0) {
+        while (true) {
+          t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
+          if (t >= N1) {
+            int e2, m2, n2;
+            map2.locate(t - N1, kBM, nt2, kBN, e2, m2, n2);
+            if (!expert_ready(p.done, e2, map1.m_tiles[e2 - map1.e_first] * nt1 * 4, p.ws)) continue;
+            fence_proxy_async_global();  // act rows written by generic stores, read below by TMA
+          }
+          break;
         }
         ptx::mbar_wait(&ring_empty[slot], rphase ^ 1);
         ring_tile[slot] = t;
         ptx::mbar_arrive(&ring_full[slot]);
-        if (++slot == kRingF) { slot = 0; rphase ^= 1; }
-        if (t < 0) break;
-        const bool up = t < N1;
-        const CUtensorMap* ta = up ? &tmX : &tmAct;
-        const CUtensorMap* tb = up ? &tmW1 : &tmW2;
-        // B rows: gate_up -> gate [n0, +128) over up F + [n0, +128); down -> [n0, +256)
-        const int brow0 = up ? e * 2 * p.F + n0 : e * p.d + n0;
-        const int brow1 = up ? brow0 + p.F : brow0 + kBN / 2;
-        const int nkb = up ? nkb1 : nkb2;
-        for (int kb = 0; kb < nkb; ++kb) {
-          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * kStageBytesF;
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+      if (t < 0) break;
+      const bool up = t < N1;
+      int e, m0, n0;
+      if (up) map1.locate(t, kBM, nt1, kBN / 2, e, m0, n0);
+      else map2.locate(t - N1, kBM, nt2, kBN, e, m0, n0);
+      const bool gather = up && p.gather;
+      int g[4] = {0, 0, 0, 0};
+      if (gather) gather_rows4(p, m0, p.offsets[e + 1], lane, g);
+      const CUtensorMap* ta = up ? &tmX : &tmAct;
+      const CUtensorMap* tb = up ? &tmW1 : &tmW2;
+      // B rows: gate_up -> gate [n0, +128) over up F + [n0, +128); down -> [n0, +256)
+      const int brow0 = up ? e * 2 * p.F + n0 : e * p.d + n0;
+      const int brow1 = up ? brow0 + p.F : brow0 + kBN / 2;
+      const int nkb = up ? nkb1 : nkb2;
+      for (int kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * kStageBytesF;
+        if (lane == 0) {
           ptx::mbar_arrive_expect_tx(&full_bar[stage], kStageBytesF);
-          ptx::tma_load_2d(ta, &full_bar[stage], sa, kb * kBKf, m0, ptx::kEvictNormal);
+          if (!gather) ptx::tma_load_2d(ta, &full_bar[stage], sa, kb * kBKf, m0, ptx::kEvictNormal);
           ptx::tma_load_2d(tb, &full_bar[stage], sa + kABytesF, kb * kBKf, brow0, ptx::kEvictNormal);
           ptx::tma_load_2d(tb, &full_bar[stage], sa + kABytesF + (kBN / 2) * 128, kb * kBKf, brow1,
                            ptx::kEvictNormal);
-          if (++stage == kStagesF) { stage = 0; phase ^= 1; }
         }
+        if (gather)
+          ptx::tma_gather4(&tmX, &full_bar[stage], sa + lane * 512, kb * kBKf, g[0], g[1], g[2], g[3],
+                           ptx::kEvictNormal);
+        if (++stage == kStagesF) { stage = 0; phase ^= 1; }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
@@ -303,23 +331,29 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
   const int N1 = map1.total, N2 = map2.total;
 
   if (warp == 0) {
-    // ------------------------------------------------------------------ TMA producer (both CTAs)
+    // ------------------------------------------------------------------ TMA producer (both CTAs,
+    // warp-wide: lane 0 claims / receives tiles; in gather mode all lanes issue tile::gather4)
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmX);
       ptx::tma_prefetch_desc(&tmW1);
       ptx::tma_prefetch_desc(&tmAct);
       ptx::tma_prefetch_desc(&tmW2);
-      int stage = 0, slot = 0, last_e = -1;
-      uint32_t phase = 0, rphase = 0;
-      while (true) {
-        int t;
-        int e = 0, m0 = 0, n0 = 0;
+    }
+    int stage = 0, slot = 0, last_e = -1;
+    uint32_t phase = 0, rphase = 0;
+    while (true) {
+      int t = -1;
+      if (lane == 0) {
         if (leader) {
-          t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
-          if (t >= N1) {
-            map2.locate(t - N1, kBMp, nt2, kBN, e, m0, n0);
-            if (!expert_ready(p.done, e, map1.m_tiles[e - map1.e_first] * nt1 * 8, p.ws)) continue;
-            fence_proxy_async_global();
+          while (true) {
+            t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
+            if (t >= N1) {
+              int e2, m2, n2;
+              map2.locate(t - N1, kBMp, nt2, kBN, e2, m2, n2);
+              if (!expert_ready(p.done, e2, map1.m_tiles[e2 - map1.e_first] * nt1 * 8, p.ws)) continue;
+              fence_proxy_async_global();
+            }
+            break;
           }
           ptx::mbar_wait_cluster(&ring_empty[slot], rphase ^ 1);
           ring_tile[slot] = t;
@@ -331,33 +365,44 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
           t = ring_tile[slot];
           ptx::mbar_arrive_remote(&ring_empty[slot], 0);
           if (t >= N1) {
-            map2.locate(t - N1, kBMp, nt2, kBN, e, m0, n0);
-            (void)ld_acquire(p.done + e);  // the leader saw it complete; acquire it here too
+            int e2, m2, n2;
+            map2.locate(t - N1, kBMp, nt2, kBN, e2, m2, n2);
+            (void)ld_acquire(p.done + e2);  // the leader saw it complete; acquire it here too
             fence_proxy_async_global();
           }
         }
-        if (++slot == kRingF) { slot = 0; rphase ^= 1; }
-        if (t < 0) break;
-        const bool up = t < N1;
-        if (up) map1.locate(t, kBMp, nt1, kBN / 2, e, m0, n0);
-        const CUtensorMap* ta = up ? &tmX : &tmAct;
-        const CUtensorMap* tb = up ? &tmW1 : &tmW2;
-        const int arow = m0 + (int)rank * 128;
-        // this CTA's 128 B rows: gate_up -> CTA0 gate [n0, +128), CTA1 up F + [n0, +128);
-        // down -> rows n0 + rank*128 of expert e
-        const int brow = up ? e * 2 * p.F + (rank ? p.F : 0) + n0 : e * p.d + n0 + (int)rank * 128;
-        const int nkb = up ? nkb1 : nkb2;
-        for (int kb = 0; kb < nkb; ++kb) {
-          ptx::mbar_wait_cluster(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * kStageBytesP;
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+      if (t < 0) break;
+      const bool up = t < N1;
+      int e, m0, n0;
+      if (up) map1.locate(t, kBMp, nt1, kBN / 2, e, m0, n0);
+      else map2.locate(t - N1, kBMp, nt2, kBN, e, m0, n0);
+      const bool gather = up && p.gather;
+      int g[4] = {0, 0, 0, 0};
+      if (gather) gather_rows4(p, m0 + (int)rank * 128, p.offsets[e + 1], lane, g);
+      const CUtensorMap* ta = up ? &tmX : &tmAct;
+      const CUtensorMap* tb = up ? &tmW1 : &tmW2;
+      const int arow = m0 + (int)rank * 128;
+      // this CTA's 128 B rows: gate_up -> CTA0 gate [n0, +128), CTA1 up F + [n0, +128);
+      // down -> rows n0 + rank*128 of expert e
+      const int brow = up ? e * 2 * p.F + (rank ? p.F : 0) + n0 : e * p.d + n0 + (int)rank * 128;
+      const int nkb = up ? nkb1 : nkb2;
+      for (int kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait_cluster(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * kStageBytesP;
+        if (lane == 0) {
           if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytesP);
-          ptx::tma_load_2d_cg2(ta, &full_bar[stage], sa, kb * kBKf, arow, ptx::kEvictNormal);
+          if (!gather) ptx::tma_load_2d_cg2(ta, &full_bar[stage], sa, kb * kBKf, arow, ptx::kEvictNormal);
           ptx::tma_load_2d_cg2(tb, &full_bar[stage], sa + kHalfP, kb * kBKf, brow, ptx::kEvictNormal);
-          if (++stage == kStagesP) { stage = 0; phase ^= 1; }
         }
+        if (gather)
+          ptx::tma_gather4_cg2(&tmX, &full_bar[stage], sa + lane * 512, kb * kBKf, g[0], g[1], g[2], g[3],
+                               ptx::kEvictNormal);
+        if (++stage == kStagesP) { stage = 0; phase ^= 1; }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer (leader only)
     if (leader && lane == 0) {
@@ -483,12 +528,13 @@ bool use_fused_tc() {
 int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                      const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                     void* const* y_peers, bool pair, cudaStream_t s) {
+                     void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s) {
   int st;
   if ((st = ffn_ws_reset(ws, s))) return st;
   CUtensorMap maps[4];
-  // A boxes: 128 token rows (each CTA of a pair loads its own 128); B boxes: 128 weight rows
-  if ((st = tc_make_map(&maps[0], xp, xp_rows, d, kBM)) ||
+  // A boxes: 128 token rows (each CTA of a pair loads its own 128), or single rows of X for the
+  // tile::gather4 loads (x != nullptr); B boxes: 128 weight rows
+  if ((st = x != nullptr ? tc_make_map(&maps[0], x, T, d, 1) : tc_make_map(&maps[0], xp, xp_rows, d, kBM)) ||
       (st = tc_make_map(&maps[1], w1, (uint64_t)E * 2 * F, d, kBN / 2)) ||
       (st = tc_make_map(&maps[2], act_ws, xp_rows, F, kBM)) ||
       (st = tc_make_map(&maps[3], w2, (uint64_t)E * d, F, kBN / 2)))
@@ -506,6 +552,8 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
   p.act = (__nv_bfloat16*)act_ws;
   p.y = (__nv_bfloat16*)y;
   p.peers = y_peers;
+  p.k = k;
+  p.gather = x != nullptr;
   static bool attr_set = false;
   if (!attr_set) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemF));

@@ -624,7 +624,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   const bool pair = use_cta_pair(xp_rows, e_end - e_begin);
   if (down_splits(xp_rows, e_end - e_begin, d, F) == 1 && use_fused_tc())
     return expert_ffn_fused(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
-                            xp_rows, y_peers, pair, s);
+                            xp_rows, y_peers, pair, nullptr, 0, 0, s);
   // gate_up: act[r, :F] = SiLU(x W1^T) * (x W3^T), expert order rows
   if ((st = make_map(&ta, xp, xp_rows, d, BM)) || (st = make_map(&tb, w1, (uint64_t)E * 2 * F, d, BN / 2))) return st;
   p.N = F; p.K = d; p.b_rows = 2 * F;
@@ -657,6 +657,14 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   p2.nsplit = 1;
   if ((st = pair ? launch_tc2<EPI_DOWN>(ta2, tb2, p2, s) : launch_tc<BN, EPI_DOWN>(ta2, tb2, p2, s))) return st;
   return ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s);
+}
+
+int expert_ffn_path(int d, int F, int E, int xp_rows) {
+  if (d % 64 != 0 || F % 64 != 0) return QMOE_PATH_UNSUPPORTED;
+  if (use_swap_ab(xp_rows, E, d, F)) return QMOE_PATH_SWAP_AB;
+  const bool pair = use_cta_pair(xp_rows, E);
+  if (down_splits(xp_rows, E, d, F) == 1 && use_fused_tc()) return pair ? QMOE_PATH_FUSED_PAIR : QMOE_PATH_FUSED_1CTA;
+  return pair ? QMOE_PATH_TWO_LAUNCH_PAIR : QMOE_PATH_TWO_LAUNCH_1CTA;
 }
 
 // Large batches use the CTA-pair kernel (M = 256 rows per tile) unless its row padding would

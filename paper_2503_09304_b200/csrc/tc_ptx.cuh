@@ -187,6 +187,28 @@ __device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* map, uint64_t
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "l"(cache_hint)
       : "memory");
 }
+// Row gather (sm_100 tile::gather4): 4 rows r0..r3 x box-width columns starting at column c0,
+// written as 4 consecutive 128 B smem rows with the map's swizzle (the map's box height is 1).
+__device__ __forceinline__ void tma_gather4(const CUtensorMap* map, uint64_t* bar, void* smem_dst, int c0, int r0,
+                                            int r1, int r2, int r3, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "l"(cache_hint)
+      : "memory");
+}
+// 2-SM variant: completion counted on the leader CTA's barrier (as tma_load_2d_cg2).
+__device__ __forceinline__ void tma_gather4_cg2(const CUtensorMap* map, uint64_t* bar, void* smem_dst, int c0, int r0,
+                                                int r1, int r2, int r3, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(r0), "r"(r1), "r"(r2),
+      "r"(r3), "l"(cache_hint)
+      : "memory");
+}
+
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_cg2(uint32_t* dst_smem) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),

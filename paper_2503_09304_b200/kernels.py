@@ -327,3 +327,45 @@ def expert_ffn_peer(xp: torch.Tensor, offsets: torch.Tensor, ret: torch.Tensor, 
     ws = workspace(nbytes, "ffn", xp.device)
     check(lib.qmoe_expert_ffn_peer(_ptr(xp), _ptr(offsets), _ptr(ret), E, d, F, _ptr(gate_up), _ptr(down), rows,
                                    _ptr(act_ws), _ptr(y_peers), _ptr(ws), nbytes, _stream()), "qmoe_expert_ffn_peer")
+
+
+# ------------------------------------------------------------------ fused row gather
+
+PATH_SWAP_AB, PATH_FUSED_1CTA, PATH_FUSED_PAIR = _lib.QMOE_PATH_SWAP_AB, _lib.QMOE_PATH_FUSED_1CTA, _lib.QMOE_PATH_FUSED_PAIR
+
+
+def expert_ffn_path(d: int, F: int, E: int, rows: int) -> int:
+    """Which bf16 SwiGLU kernel qmoe_expert_ffn runs for `rows` routed rows over E experts."""
+    return int(_lib.load().qmoe_expert_ffn_path(d, F, E, rows))
+
+
+def gathers_rows(d: int, F: int, E: int, rows: int) -> bool:
+    """True when the expert kernel loads token rows from X itself (no permute gather needed)."""
+    return expert_ffn_path(d, F, E, rows) in (PATH_FUSED_1CTA, PATH_FUSED_PAIR)
+
+
+def expert_ffn_gather(x: torch.Tensor, k: int, offsets: torch.Tensor, perm: torch.Tensor, gate_up: torch.Tensor,
+                      down: torch.Tensor, y: torch.Tensor, e_begin: int = 0, e_end: Optional[int] = None,
+                      act_ws: Optional[torch.Tensor] = None, preempt_flag: Optional[torch.Tensor] = None,
+                      cursor_out: Optional[torch.Tensor] = None) -> None:
+    """Grouped bf16 SwiGLU experts with the row gather fused into the GEMM (TMA tile::gather4):
+    the i-th row of expert e is x[perm[offsets[e] + i] // k]; results land in y[perm[r]]."""
+    _need(x, "x", torch.bfloat16)
+    for name, t in (("gate_up", gate_up), ("down", down), ("y", y)):
+        _need(t, name, torch.bfloat16)
+    _need(offsets, "offsets", torch.int32)
+    _need(perm, "perm", torch.int32)
+    T, d = x.shape
+    E, twoF, _ = gate_up.shape
+    F = twoF // 2
+    rows = T * k
+    if act_ws is None:
+        act_ws = torch.empty((max(rows, 1), F), dtype=x.dtype, device=x.device)
+    if e_end is None:
+        e_end = E
+    lib = _lib.load()
+    nbytes = lib.qmoe_expert_ffn_workspace_bytes(EXPERT_SWIGLU, _lib.QMOE_BF16, d, rows)
+    ws = workspace(nbytes, "ffn", x.device)
+    check(lib.qmoe_expert_ffn_gather(_ptr(x), T, k, _ptr(offsets), _ptr(perm), E, d, F, _ptr(gate_up), _ptr(down),
+                                     e_begin, e_end, _ptr(act_ws), _ptr(y), _ptr(preempt_flag), _ptr(cursor_out),
+                                     _ptr(ws), nbytes, _stream()), "qmoe_expert_ffn_gather")

@@ -50,9 +50,21 @@ for (T, d, F, E, k) in json.loads(sys.argv[2]):
     done = perm[: oc[c]].long()
     part_ok = c == first and torch.equal(y2[done], y[done])
     K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y2, e_begin=c)
+    # the fused row gather (TMA tile::gather4 from X): identical to the Xp path, also when preempted
+    gather = K.gathers_rows(d, F, E, T * k)
+    gather_ok = True
+    if gather:
+        y3 = torch.zeros_like(y)
+        K.expert_ffn_gather(x, k, offsets, perm, gu, dn, y3)
+        y4 = torch.zeros_like(y)
+        flag.fill_(3)
+        K.expert_ffn_gather(x, k, offsets, perm, gu, dn, y4, preempt_flag=flag, cursor_out=cur)
+        c4 = int(cur)
+        K.expert_ffn_gather(x, k, offsets, perm, gu, dn, y4, e_begin=c4)
+        gather_ok = torch.equal(y3, y) and torch.equal(y4, y) and c4 == first
     import hashlib
     res.append({"shape": [T, d, F, E, k], "rel": rel, "stop": c, "want_stop": first, "partial_ok": part_ok,
-                "resume_identical": torch.equal(y2, y),
+                "resume_identical": torch.equal(y2, y), "gather": gather, "gather_ok": gather_ok,
                 "sha": hashlib.sha1(y.view(torch.int16).cpu().numpy().tobytes()).hexdigest()})
 print(json.dumps(res))
 """
@@ -70,6 +82,7 @@ def _run(env, shapes):
         assert r["rel"] < 1e-2, r
         assert r["stop"] == r["want_stop"] and r["partial_ok"], r
         assert r["resume_identical"], r
+        assert r["gather_ok"], r
     return res
 
 
@@ -78,6 +91,12 @@ def _run(env, shapes):
                          ids=["swap-ab", "tc-1cta-single-launch", "tc-pair"])
 def test_forced_expert_path(cuda, env):
     _run(env, SHAPES if env.get("QMOE_SWAP_AB") == "1" else [s for s in SHAPES if s[0] * s[4] > 512])
+
+
+@pytest.mark.parametrize("pair", ["0", "1"], ids=["1cta", "cta-pair"])
+def test_fused_row_gather_is_used(cuda, pair):
+    res = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": pair}, [s for s in SHAPES if s[0] * s[4] > 512])
+    assert all(r["gather"] for r in res)
 
 
 @pytest.mark.parametrize("pair", ["0", "1"], ids=["1cta", "cta-pair"])

@@ -36,11 +36,18 @@ for T in [int(t) for t in sys.argv[1:]] or [32, 256, 1024, 4096, 8192, 16384]:
     y = torch.empty((T * k, d), dtype=torch.bfloat16, device="cuda")
     act = torch.empty((T * k, F), dtype=torch.bfloat16, device="cuda")
     t_r = timeit(lambda: K.router(x, wr, k, mode))
-    t_p = timeit(lambda: K.permute(ids, E, x=x))
-    t_f = timeit(lambda: K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act))
+    gather = K.gathers_rows(d, F, E, T * k) and os.environ.get("PROBE_GATHER") is not None
+    if gather:  # the fused tile::gather4 A operand (measured ~2x slower than the Xp path on B200)
+        t_p = timeit(lambda: K.permute(ids, E))
+        t_f = timeit(lambda: K.expert_ffn_gather(x, k, offsets, perm, gu, dn, y, act_ws=act))
+    else:
+        t_p = timeit(lambda: K.permute(ids, E, x=x))
+        t_f = timeit(lambda: K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act))
     t_c = timeit(lambda: K.combine(y, w, x))
     flops = 6.0 * T * k * d * F
     hit = int((offsets[1:] > offsets[:-1]).sum())
     wbytes = hit * 3 * d * F * 2
     print(f"T={T:6d} router {t_r*1e3:8.1f}us permute {t_p*1e3:8.1f}us ffn {t_f*1e3:9.1f}us "
-          f"({flops/t_f/1e9:7.1f} TFLOP/s, weights {wbytes/t_f/1e6:7.1f} GB/s) combine {t_c*1e3:7.1f}us", flush=True)
+          f"({flops/t_f/1e9:7.1f} TFLOP/s, weights {wbytes/t_f/1e6:7.1f} GB/s) combine {t_c*1e3:7.1f}us "
+          f"path {K.expert_ffn_path(d, F, E, T * k)}{' gather' if gather else ''} "
+          f"total {(t_r + t_p + t_f + t_c) * 1e3:8.1f}us", flush=True)
