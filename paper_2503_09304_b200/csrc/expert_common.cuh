@@ -153,14 +153,15 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Single-launch gate_up + down kernels (expert_swap.cu, expert_fused.cu).  Claim the next unit:
-// gate_up units [0, N1) under the expert-boundary stop protocol of ffn_claim, then down units
-// [N1, N1 + N2).  Returns the global unit index or -1.
-__device__ __forceinline__ int two_phase_claim(const TileMap& m1, int N2, FfnWorkspace* ws, const volatile int32_t* flag,
-                                          int& last_e) {
+// Single-launch gate_up + down kernels (expert_swap.cu, expert_fused.cu).  Resolve a unit index
+// t taken from the claim counter: gate_up units [0, N1) under the expert-boundary stop protocol of
+// ffn_claim, then down units [N1, N1 + N2).  Returns the unit to run or -1.  Producers take the
+// NEXT index (atomicAdd on ws->next) as soon as they start a unit and resolve it one unit later,
+// so the claim's L2 round trip overlaps the current unit's loads instead of stalling the ring.
+__device__ __forceinline__ int resolve_claim(const TileMap& m1, int N2, FfnWorkspace* ws, const volatile int32_t* flag,
+                                             int& last_e, int t) {
   const int N1 = m1.total;
   while (true) {
-    const int t = atomicAdd(&ws->next, 1);
     if (t >= N1) return t - N1 < N2 ? t : -1;
     int local;
     const int e = m1.expert_of(t, local);
@@ -177,7 +178,13 @@ __device__ __forceinline__ int two_phase_claim(const TileMap& m1, int N2, FfnWor
     if (e < stop) return t;
     // every later gate_up unit belongs to an expert >= e >= stop: skip straight to the down units
     atomicMax(&ws->next, N1);
+    t = atomicAdd(&ws->next, 1);
   }
+}
+
+__device__ __forceinline__ int two_phase_claim(const TileMap& m1, int N2, FfnWorkspace* ws,
+                                               const volatile int32_t* flag, int& last_e) {
+  return resolve_claim(m1, N2, ws, flag, last_e, atomicAdd(&ws->next, 1));
 }
 
 // Down unit of expert e: true once all gate_up units of e stored their act rows, false if e can

@@ -120,15 +120,19 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     }
     int stage = 0, slot = 0, last_e = -1;
     uint32_t phase = 0, rphase = 0;
+    int pending = lane == 0 ? atomicAdd(&p.ws->next, 1) : 0;  // claim one unit ahead
     while (true) {
       int t = -1;
       if (lane == 0) {
         while (true) {
-          t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
+          t = resolve_claim(map1, N2, p.ws, p.flag, last_e, pending);
           if (t >= N1) {
             int e2, m2, n2;
             map2.locate(t - N1, kBM, nt2, kBN, e2, m2, n2);
-            if (!expert_ready(p.done, e2, map1.m_tiles[e2 - map1.e_first] * nt1 * 4, p.ws)) continue;
+            if (!expert_ready(p.done, e2, map1.m_tiles[e2 - map1.e_first] * nt1 * 4, p.ws)) {
+              pending = atomicAdd(&p.ws->next, 1);
+              continue;
+            }
             fence_proxy_async_global();  // act rows written by generic stores, read below by TMA
           }
           break;
@@ -136,6 +140,7 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         ptx::mbar_wait(&ring_empty[slot], rphase ^ 1);
         ring_tile[slot] = t;
         ptx::mbar_arrive(&ring_full[slot]);
+        if (t >= 0) pending = atomicAdd(&p.ws->next, 1);  // in flight while this unit's loads issue
       }
       t = __shfl_sync(0xffffffffu, t, 0);
       if (++slot == kRingF) { slot = 0; rphase ^= 1; }
@@ -341,16 +346,20 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
     }
     int stage = 0, slot = 0, last_e = -1;
     uint32_t phase = 0, rphase = 0;
+    int pending = (lane == 0 && leader) ? atomicAdd(&p.ws->next, 1) : 0;  // claim one unit ahead
     while (true) {
       int t = -1;
       if (lane == 0) {
         if (leader) {
           while (true) {
-            t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
+            t = resolve_claim(map1, N2, p.ws, p.flag, last_e, pending);
             if (t >= N1) {
               int e2, m2, n2;
               map2.locate(t - N1, kBMp, nt2, kBN, e2, m2, n2);
-              if (!expert_ready(p.done, e2, map1.m_tiles[e2 - map1.e_first] * nt1 * 8, p.ws)) continue;
+              if (!expert_ready(p.done, e2, map1.m_tiles[e2 - map1.e_first] * nt1 * 8, p.ws)) {
+                pending = atomicAdd(&p.ws->next, 1);
+                continue;
+              }
               fence_proxy_async_global();
             }
             break;
@@ -360,6 +369,7 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
           ptx::st_remote_u32(&ring_tile[slot], 1, (uint32_t)t);
           ptx::mbar_arrive(&ring_full[slot]);
           ptx::mbar_arrive_remote(&ring_full[slot], 1);
+          if (t >= 0) pending = atomicAdd(&p.ws->next, 1);  // in flight while this unit's loads issue
         } else {
           ptx::mbar_wait_cluster(&ring_full[slot], rphase);
           t = ring_tile[slot];

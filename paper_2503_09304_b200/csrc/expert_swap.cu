@@ -127,13 +127,17 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
       ptx::tma_prefetch_desc(&tmW2);
       int stage = 0, slot = 0, last_e = -1;
       uint32_t phase = 0, rphase = 0;
+      int pending = atomicAdd(&p.ws->next, 1);  // claim one unit ahead (see resolve_claim)
       while (true) {
-        int t = two_phase_claim(map1, N2, p.ws, p.flag, last_e);
+        int t = resolve_claim(map1, N2, p.ws, p.flag, last_e, pending);
         int e = 0, m0 = 0, n0 = 0, split = 0;
         if (t >= N1) {
           map2.locate(t - N1, NT, nt2 * p.nsplit, kWRows, e, m0, n0, p.nsplit, &split);
           const int i = e - map1.e_first;
-          if (!expert_ready(p.done, e, map1.m_tiles[i] * nt1 * 4, p.ws)) continue;
+          if (!expert_ready(p.done, e, map1.m_tiles[i] * nt1 * 4, p.ws)) {
+            pending = atomicAdd(&p.ws->next, 1);
+            continue;
+          }
           fence_proxy_async_global();  // act rows written by generic stores, read below by TMA
         } else if (t >= 0) {
           map1.locate(t, NT, nt1, kWRows, e, m0, n0);
@@ -143,6 +147,7 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
         ptx::mbar_arrive(&ring_full[slot]);
         if (++slot == kRing) { slot = 0; rphase ^= 1; }
         if (t < 0) break;
+        pending = atomicAdd(&p.ws->next, 1);  // in flight while this unit's loads issue
         if (t < N1) {
           const int g_row = e * 2 * p.F + n0, u_row = g_row + p.F;
           for (int kb = 0; kb < nkb1; ++kb) {
