@@ -3,6 +3,8 @@
 // Replaces MoEModel.route / route_many (reference model.py:115-134) and select_top_k /
 // softmax_over (model.py:71-80).  HBM-bound on X: each token row is read once; W_router (E x d)
 // stays L1/L2-resident and is reused across the TPC tokens a CTA owns (register blocking).
+#include <stdlib.h>
+
 #include <algorithm>
 #include <type_traits>
 
@@ -276,39 +278,42 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-template <int NP>  // n-tile pairs: experts padded to 16 * NP
+template <int NP, int MT>  // NP n-tile pairs (experts padded to 16 * NP); MT 16-token tiles per CTA
 __global__ void __launch_bounds__(256)
 router_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr, int ntok, int d, int E,
                   int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
                   float* __restrict__ logits_out) {
+  constexpr int kTok = 16 * MT;
   extern __shared__ __align__(16) __nv_bfloat16 sbuf[];  // kMmaStages x (X chunk, W chunk); reused below
   const int warp = warp_id(), lane = lane_id();
-  const int tok0 = blockIdx.x * kMmaTok;
+  const int tok0 = blockIdx.x * kTok;
   const int nk = d / kMmaK;
   constexpr int wrows = 16 * NP;  // W rows staged
-  const int stage_elems = (kMmaTok + wrows) * kLd;
+  constexpr int stage_elems = (kTok + wrows) * kLd;
   auto load = [&](int kc) {
     if (kc < nk) {
       __nv_bfloat16* sx = sbuf + (kc % kMmaStages) * stage_elems;
-      __nv_bfloat16* sw = sx + kMmaTok * kLd;
+      __nv_bfloat16* sw = sx + kTok * kLd;
       const int k0 = kc * kMmaK;
-      // (16 + wrows) rows x 16 pieces of 16 B over 256 threads
-      for (int piece = threadIdx.x; piece < (kMmaTok + wrows) * 16; piece += 256) {
+      // (kTok + wrows) rows x 16 pieces of 16 B over 256 threads
+      for (int piece = threadIdx.x; piece < (kTok + wrows) * 16; piece += 256) {
         const int r = piece >> 4, c = (piece & 15) * 8;
-        if (r < kMmaTok) {
+        if (r < kTok) {
           const int t = tok0 + r;
           cp_async16(sx + r * kLd + c, x + (size_t)min(t, ntok - 1) * d + k0 + c, t < ntok);
         } else {
-          const int e = r - kMmaTok;
+          const int e = r - kTok;
           cp_async16(sw + e * kLd + c, wr + (size_t)min(e, E - 1) * d + k0 + c, e < E);
         }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group per chunk
   };
-  float acc[2 * NP][4];
+  float acc[MT][2 * NP][4];
 #pragma unroll
-  for (int j = 0; j < 2 * NP; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int j = 0; j < 2 * NP; ++j) acc[mt][j][0] = acc[mt][j][1] = acc[mt][j][2] = acc[mt][j][3] = 0.f;
 #pragma unroll
   for (int i = 0; i < kMmaStages - 1; ++i) load(i);
   for (int kc = 0; kc < nk; ++kc) {
@@ -316,47 +321,55 @@ router_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __re
     asm volatile("cp.async.wait_group %0;" ::"n"(kMmaStages - 1) : "memory");  // chunk kc landed
     __syncthreads();
     const __nv_bfloat16* sx = sbuf + (kc % kMmaStages) * stage_elems;
-    const __nv_bfloat16* sw = sx + kMmaTok * kLd;
+    const __nv_bfloat16* sw = sx + kTok * kLd;
     const int ks = warp;  // this warp's k16 step of the chunk
-    uint32_t a0, a1, a2, a3;
-    ldsm_x4(sx + (lane & 15) * kLd + ks * 16 + (lane >> 4) * 8, a0, a1, a2, a3);
+    uint32_t a[MT][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+      ldsm_x4(sx + (16 * mt + (lane & 15)) * kLd + ks * 16 + (lane >> 4) * 8, a[mt][0], a[mt][1], a[mt][2], a[mt][3]);
 #pragma unroll
     for (int np = 0; np < NP; ++np) {
-      uint32_t b0, b1, b2, b3;
+      uint32_t b0, b1, b2, b3;  // one B fragment load feeds every token tile
       ldsm_x4(sw + (16 * np + (lane >> 4) * 8 + (lane & 7)) * kLd + ks * 16 + ((lane >> 3) & 1) * 8, b0, b1, b2, b3);
-      mma_bf16_16816(acc[2 * np], a0, a1, a2, a3, b0, b1);
-      mma_bf16_16816(acc[2 * np + 1], a0, a1, a2, a3, b2, b3);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        mma_bf16_16816(acc[mt][2 * np], a[mt][0], a[mt][1], a[mt][2], a[mt][3], b0, b1);
+        mma_bf16_16816(acc[mt][2 * np + 1], a[mt][0], a[mt][1], a[mt][2], a[mt][3], b2, b3);
+      }
     }
     __syncthreads();  // stage kc % kMmaStages is refilled by the next iteration's load
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  // partial tiles [warp][16 tokens][64 experts], summed in warp order
+  // partial tiles [warp][kTok tokens][64 experts], summed in warp order
   float* s_part = reinterpret_cast<float*>(sbuf);
-  float* s_logit = s_part + 8 * kMmaTok * kMaxE;
-  float* s_score = s_logit + kMmaTok * kMaxE;
+  float* s_logit = s_part + 8 * kTok * kMaxE;
+  float* s_score = s_logit + kTok * kMaxE;
   {
-    float* my = s_part + warp * kMmaTok * kMaxE;
-    const int r0 = lane >> 2;
+    float* my = s_part + warp * kTok * kMaxE;
 #pragma unroll
-    for (int j = 0; j < 2 * NP; ++j) {
-      const int e = 8 * j + 2 * (lane & 3);
-      my[r0 * kMaxE + e] = acc[j][0];
-      my[r0 * kMaxE + e + 1] = acc[j][1];
-      my[(r0 + 8) * kMaxE + e] = acc[j][2];
-      my[(r0 + 8) * kMaxE + e + 1] = acc[j][3];
+    for (int mt = 0; mt < MT; ++mt) {
+      const int r0 = 16 * mt + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < 2 * NP; ++j) {
+        const int e = 8 * j + 2 * (lane & 3);
+        my[r0 * kMaxE + e] = acc[mt][j][0];
+        my[r0 * kMaxE + e + 1] = acc[mt][j][1];
+        my[(r0 + 8) * kMaxE + e] = acc[mt][j][2];
+        my[(r0 + 8) * kMaxE + e + 1] = acc[mt][j][3];
+      }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kMmaTok * kMaxE; i += 256) {
+  for (int i = threadIdx.x; i < kTok * kMaxE; i += 256) {
     float v = s_part[i];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) v += s_part[w * kMmaTok * kMaxE + i];
+    for (int w = 1; w < 8; ++w) v += s_part[w * kTok * kMaxE + i];
     s_logit[i] = v;
   }
   __syncthreads();
 #pragma unroll 1
-  for (int ti = warp; ti < kMmaTok; ti += 8) {
+  for (int ti = warp; ti < kTok; ti += 8) {
     const int tok = tok0 + ti;
     if (tok >= ntok) break;
     select_token<float>(s_logit + ti * kMaxE, s_score + ti * kMaxE, tok, E, k, mode, lane, ids_out, w_out,
@@ -364,25 +377,39 @@ router_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __re
   }
 }
 
-template <int NP>
+template <int NP, int MT>
 int launch_router_mma_np(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
                          void* logits, cudaStream_t s) {
+  constexpr int kTok = 16 * MT;
   static bool attr_set = false;
-  const int smem = std::max(kMmaStages * (kMmaTok + 16 * NP) * kLd * 2, (8 + 2) * kMmaTok * kMaxE * 4);
+  const int smem = std::max(kMmaStages * (kTok + 16 * NP) * kLd * 2, (8 + 2) * kTok * kMaxE * 4);
   if (!attr_set) {
-    QMOE_CUDA_TRY(cudaFuncSetAttribute(router_mma_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(router_mma_kernel<NP, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
-  router_mma_kernel<NP><<<(T_ + kMmaTok - 1) / kMmaTok, 256, smem, s>>>(
+  router_mma_kernel<NP, MT><<<(T_ + kTok - 1) / kTok, 256, smem, s>>>(
       (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w, (float*)logits);
   return check_launch("qmoe_router(mma)");
 }
 
 int launch_router_mma(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
                       void* logits, cudaStream_t s) {
-  if (E <= 16) return launch_router_mma_np<1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
-  if (E <= 32) return launch_router_mma_np<2>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
-  return launch_router_mma_np<4>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  // 32 tokens per CTA from 4k tokens (halves the W_router re-reads and doubles the MMA work per
+  // staged chunk: Qwen 8k tokens 49 -> 39 us); 16 below that, to keep every SM busy.
+  // QMOE_ROUTER_MT=1/2 forces the tile
+  static const int mt_env = [] {
+    const char* v = getenv("QMOE_ROUTER_MT");
+    return v == nullptr ? 0 : atoi(v);
+  }();
+  const bool two = mt_env ? mt_env == 2 : T_ >= 4096;
+  if (E <= 16)
+    return two ? launch_router_mma_np<1, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s)
+               : launch_router_mma_np<1, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  if (E <= 32)
+    return two ? launch_router_mma_np<2, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s)
+               : launch_router_mma_np<2, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+  return two ? launch_router_mma_np<4, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s)
+             : launch_router_mma_np<4, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
 }
 
 // Few tokens (decode): one token per CTA, all 8 warps on it.  Many tokens: warps own tokens (2
