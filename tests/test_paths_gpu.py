@@ -107,3 +107,60 @@ def test_single_launch_equals_two_launches(cuda, pair):
     one = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": pair}, shapes)
     two = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": pair, "QMOE_FUSED": "0"}, shapes)
     assert [r["sha"] for r in one] == [r["sha"] for r in two]
+
+
+RACE = r"""
+import json, sys
+import torch
+sys.path.insert(0, sys.argv[1])
+from paper_2503_09304_b200 import kernels as K
+out = []
+for (T, d, F, E, k, delay) in json.loads(sys.argv[2]):
+    g = torch.Generator().manual_seed(T + delay)
+    x = torch.randn((T, d), generator=g).bfloat16().cuda()
+    wr = (torch.randn((E, d), generator=g) / d ** 0.5).bfloat16().cuda()
+    gu = (torch.randn((E, 2 * F, d), generator=g) / d ** 0.5).bfloat16().cuda()
+    dn = (torch.randn((E, d, F), generator=g) / F ** 0.5).bfloat16().cuda()
+    ids, w = K.router(x, wr, k)
+    perm, offsets, xp = K.permute(ids, E, x=x)
+    full = torch.zeros((T * k, d), dtype=torch.bfloat16, device="cuda")
+    K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, full)
+    oc = offsets.cpu().tolist()
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    cur = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    y = torch.zeros_like(full)
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):  # raise "stop at the first boundary >= 2" while the GEMM runs
+        torch.cuda._sleep(delay)
+        flag.fill_(2)
+    K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, preempt_flag=flag, cursor_out=cur)
+    torch.cuda.synchronize()
+    c = int(cur)
+    done = perm[: oc[c]].long()
+    ok_prefix = torch.equal(y[done], full[done])
+    flag.zero_()
+    K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, e_begin=c, cursor_out=cur)
+    out.append({"shape": [T, d, F, E, k], "delay": delay, "stop": c, "path": K.expert_ffn_path(d, F, E, T * k),
+                "prefix_ok": ok_prefix, "resume_ok": torch.equal(y, full) and int(cur) == E})
+print(json.dumps(out))
+"""
+
+
+def test_preempt_flag_raised_mid_launch(cuda):
+    """The device flag raised by another stream WHILE the grouped GEMM runs (the serving engine's
+    wall-clock path) on every bf16 kernel path: the launch stops at an expert boundary >= 2 (or runs
+    to the end if the flag came too late), every expert below the stop is complete and equal to an
+    uninterrupted launch, and resuming from the cursor completes the layer bit-identically."""
+    cases = [(32, 2048, 4096, 8, 2, d) for d in (0, 20000, 200000)]           # swap-AB
+    cases += [(1200, 2048, 4096, 8, 2, d) for d in (0, 20000, 60000)]        # fused 128-row tiles
+    cases += [(3000, 1024, 1408, 60, 4, d) for d in (0, 10000, 30000)]       # fused 256-row pair
+    out = subprocess.run([sys.executable, "-c", RACE, str(ROOT), json.dumps(cases)], capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert {r["path"] for r in res} >= {1, 2, 3}, res
+    assert any(r["stop"] < 8 for r in res), res  # at least some launches really stopped mid-way
+    for r in res:
+        assert r["stop"] >= 2, r
+        assert r["prefix_ok"] and r["resume_ok"], r
