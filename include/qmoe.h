@@ -142,12 +142,13 @@ QMOE_API int qmoe_expert_ffn_path(int d, int F, int E, int xp_rows);
  * Grouped bf16 SwiGLU experts reading the token rows straight from X (no gathered Xp): the i-th
  * row of expert e is X[perm[offsets[e] + i] / k], loaded by the GEMM's producer warp with TMA
  * tile::gather4 (4 arbitrary rows per instruction) -- the permute's row gather fused into the
- * A-operand load.  Only for the single-launch tcgen05 paths (QMOE_PATH_FUSED_1CTA / _PAIR for
- * xp_rows = T*k); other paths return QMOE_ERR_UNSUPPORTED (callers gather with qmoe_permute).
- * Measured on B200 it is ~2x SLOWER than qmoe_permute's gather + qmoe_expert_ffn (32 gather4
- * instructions per 64-wide K step per CTA saturate the TMA issue path, where the Xp tile is one
- * instruction), so the host paths do not use it; it serves callers that cannot afford the
- * T*k*d Xp buffer.
+ * A-operand (token-row) load.  For the single-launch paths (QMOE_PATH_SWAP_AB / _FUSED_1CTA /
+ * _FUSED_PAIR for xp_rows = T*k); other paths return QMOE_ERR_UNSUPPORTED (callers gather with
+ * qmoe_permute).  Measured on B200 it does not pay: on the 128/256-row tiles it is ~2x slower
+ * than qmoe_permute's gather + qmoe_expert_ffn (32 gather4 instructions per 64-wide K step per CTA
+ * saturate the TMA issue path, where an Xp tile is one instruction); on the swap-AB decode path it
+ * is neutral at 1-32 tokens and slower beyond.  The host paths therefore keep the Xp gather; this
+ * entry serves callers that cannot afford the T*k*d Xp buffer.
  * Same outputs, preemption flag, cursor and workspace as qmoe_expert_ffn (xp_rows = T*k).
  */
 QMOE_API int qmoe_expert_ffn_gather(const void* x, int T, int k, const int32_t* offsets, const int32_t* perm, int E,

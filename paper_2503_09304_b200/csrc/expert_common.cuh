@@ -216,7 +216,7 @@ bool use_swap_ab(int xp_rows, int n_experts, int d, int F);
 int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                    void* const* y_peers, cudaStream_t s);
+                    void* const* y_peers, const void* x, int T, int k, cudaStream_t s);
 
 // Mid-size and large batches (expert_fused.cu): 128 x 256 (1 CTA) or 256 x 256 (CTA pair) tiles,
 // gate_up and down in one persistent launch.

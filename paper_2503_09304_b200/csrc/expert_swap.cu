@@ -56,6 +56,8 @@ struct SwapParams {
   float* part;
   int nsplit, kb_per_split, part_rows;
   void* const* peers;  // expert parallel over peer memory: per-rank slot buffers (see out_row)
+  int k;               // top-k: gate_up B rows are x[perm[r] / k] when gather != 0
+  int gather;          // 1: token rows gathered from X by the producer warp (TMA tile::gather4)
 };
 
 template <int NT>
@@ -119,53 +121,80 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
   const int N1 = map1.total, N2 = map2.total;
 
   if (warp == 0) {
-    // ------------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------------ TMA producer (warp-wide:
+    // lane 0 claims and issues the tile loads; in gather mode lanes [0, NT/4) each issue one
+    // tile::gather4 of 4 token rows of X per K block instead of one Xp tile load)
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmX);
       ptx::tma_prefetch_desc(&tmW1);
       ptx::tma_prefetch_desc(&tmAct);
       ptx::tma_prefetch_desc(&tmW2);
-      int stage = 0, slot = 0, last_e = -1;
-      uint32_t phase = 0, rphase = 0;
-      int pending = atomicAdd(&p.ws->next, 1);  // claim one unit ahead (see resolve_claim)
-      while (true) {
-        int t = resolve_claim(map1, N2, p.ws, p.flag, last_e, pending);
-        int e = 0, m0 = 0, n0 = 0, split = 0;
-        if (t >= N1) {
-          map2.locate(t - N1, NT, nt2 * p.nsplit, kWRows, e, m0, n0, p.nsplit, &split);
-          const int i = e - map1.e_first;
-          if (!expert_ready(p.done, e, map1.m_tiles[i] * nt1 * 4, p.ws)) {
-            pending = atomicAdd(&p.ws->next, 1);
-            continue;
+    }
+    int stage = 0, slot = 0, last_e = -1;
+    uint32_t phase = 0, rphase = 0;
+    int pending = lane == 0 ? atomicAdd(&p.ws->next, 1) : 0;  // claim one unit ahead (see resolve_claim)
+    while (true) {
+      int t = -1;
+      if (lane == 0) {
+        while (true) {
+          t = resolve_claim(map1, N2, p.ws, p.flag, last_e, pending);
+          if (t >= N1) {
+            int e2, m2, n2, s2;
+            map2.locate(t - N1, NT, nt2 * p.nsplit, kWRows, e2, m2, n2, p.nsplit, &s2);
+            if (!expert_ready(p.done, e2, map1.m_tiles[e2 - map1.e_first] * nt1 * 4, p.ws)) {
+              pending = atomicAdd(&p.ws->next, 1);
+              continue;
+            }
+            fence_proxy_async_global();  // act rows written by generic stores, read below by TMA
           }
-          fence_proxy_async_global();  // act rows written by generic stores, read below by TMA
-        } else if (t >= 0) {
-          map1.locate(t, NT, nt1, kWRows, e, m0, n0);
+          break;
         }
         ptx::mbar_wait(&ring_empty[slot], rphase ^ 1);
         ring_tile[slot] = t;
         ptx::mbar_arrive(&ring_full[slot]);
-        if (++slot == kRing) { slot = 0; rphase ^= 1; }
-        if (t < 0) break;
-        pending = atomicAdd(&p.ws->next, 1);  // in flight while this unit's loads issue
-        if (t < N1) {
-          const int g_row = e * 2 * p.F + n0, u_row = g_row + p.F;
-          for (int kb = 0; kb < nkb1; ++kb) {
-            ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-            uint8_t* sa = smem + stage * C::kStageBytes;
+        if (t >= 0) pending = atomicAdd(&p.ws->next, 1);  // in flight while this unit's loads issue
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (++slot == kRing) { slot = 0; rphase ^= 1; }
+      if (t < 0) break;
+      int e = 0, m0 = 0, n0 = 0, split = 0;
+      if (t < N1) {
+        map1.locate(t, NT, nt1, kWRows, e, m0, n0);
+        const bool gather = p.gather != 0;
+        int g[4] = {0, 0, 0, 0};
+        const bool g_lane = gather && lane < NT / 4;
+        if (g_lane) {
+          const int row_end = p.offsets[e + 1];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = m0 + 4 * lane + j;
+            g[j] = r < row_end ? p.perm[r] / p.k : 0;  // rows past the queue read token 0 (never stored)
+          }
+        }
+        const int g_row = e * 2 * p.F + n0, u_row = g_row + p.F;
+        for (int kb = 0; kb < nkb1; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          if (lane == 0) {
             ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * C::kABytes + C::kBBytes);
             ptx::tma_load_2d(&tmW1, &full_bar[stage], sa, kb * kBK, g_row, ptx::kEvictNormal);
             ptx::tma_load_2d(&tmW1, &full_bar[stage], sa + C::kABytes, kb * kBK, u_row, ptx::kEvictNormal);
-            ptx::tma_load_2d(&tmX, &full_bar[stage], sa + 2 * C::kABytes, kb * kBK, m0, ptx::kEvictLast);
-            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+            if (!gather) ptx::tma_load_2d(&tmX, &full_bar[stage], sa + 2 * C::kABytes, kb * kBK, m0, ptx::kEvictLast);
           }
-        } else {
-          const int kb0 = split * p.kb_per_split, kb1 = min(nkb2, kb0 + p.kb_per_split);
-          const int w_row = e * p.d + n0;
-          for (int kb = kb0; kb < kb1; kb += C::kKB2) {
-            const bool two = C::kKB2 == 2 && kb + 1 < kb1;
-            ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-            uint8_t* sa = smem + stage * C::kStageBytes;
+          if (g_lane)
+            ptx::tma_gather4(&tmX, &full_bar[stage], sa + 2 * C::kABytes + lane * 512, kb * kBK, g[0], g[1], g[2], g[3],
+                             ptx::kEvictLast);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      } else {
+        map2.locate(t - N1, NT, nt2 * p.nsplit, kWRows, e, m0, n0, p.nsplit, &split);
+        const int kb0 = split * p.kb_per_split, kb1 = min(nkb2, kb0 + p.kb_per_split);
+        const int w_row = e * p.d + n0;
+        for (int kb = kb0; kb < kb1; kb += C::kKB2) {
+          const bool two = C::kKB2 == 2 && kb + 1 < kb1;
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          if (lane == 0) {
             ptx::mbar_arrive_expect_tx(&full_bar[stage], (two ? 2 : 1) * (C::kABytes + C::kBBytes));
             ptx::tma_load_2d(&tmW2, &full_bar[stage], sa, kb * kBK, w_row, ptx::kEvictNormal);
             ptx::tma_load_2d(&tmAct, &full_bar[stage], sa + 2 * C::kABytes, kb * kBK, m0, ptx::kEvictLast);
@@ -174,12 +203,11 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
               ptx::tma_load_2d(&tmAct, &full_bar[stage], sa + 2 * C::kABytes + C::kBBytes, (kb + 1) * kBK, m0,
                                ptx::kEvictLast);
             }
-            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
@@ -384,14 +412,15 @@ bool use_swap_ab(int xp_rows, int n_experts, int d, int F) {
 int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                    void* const* y_peers, cudaStream_t s) {
+                    void* const* y_peers, const void* x, int T, int k, cudaStream_t s) {
   int st;
   if ((st = ffn_ws_reset(ws, s))) return st;
   // Token tile: 32 rows when experts see ~1-24 rows on average (decode), 64 up to ~64, else 128.
   const double mean_rows = (double)xp_rows / (E > 0 ? E : 1);
   const int NT = mean_rows <= 24.0 ? 32 : (mean_rows <= 64.0 ? 64 : 128);
   CUtensorMap maps[4];
-  if ((st = tc_make_map(&maps[0], xp, xp_rows, d, NT)) || (st = tc_make_map(&maps[1], w1, (uint64_t)E * 2 * F, d, kWRows)) ||
+  // token rows: NT-row boxes of Xp, or single rows of X for the tile::gather4 loads (x != nullptr)
+  if ((st = x != nullptr ? tc_make_map(&maps[0], x, T, d, 1) : tc_make_map(&maps[0], xp, xp_rows, d, NT)) || (st = tc_make_map(&maps[1], w1, (uint64_t)E * 2 * F, d, kWRows)) ||
       (st = tc_make_map(&maps[2], act_ws, xp_rows, F, NT)) || (st = tc_make_map(&maps[3], w2, (uint64_t)E * d, F, kWRows)))
     return st;
   SwapParams p{};
@@ -407,6 +436,8 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
   p.act = (__nv_bfloat16*)act_ws;
   p.y = (__nv_bfloat16*)y;
   p.peers = y_peers;
+  p.k = k;
+  p.gather = x != nullptr;
   const int nkb2 = (F + kBK - 1) / kBK;
   const int want = xp_rows <= kSwapRowsMax ? swap_splits(F) : 1;  // partials sized for <= 512 rows
   p.kb_per_split = (nkb2 + want - 1) / want;

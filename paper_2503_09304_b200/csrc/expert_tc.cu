@@ -601,7 +601,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
                "qmoe_expert_ffn(bf16): buffers must be 16-byte aligned");
   if (variant == QMOE_EXPERT_SWIGLU && use_swap_ab(xp_rows, E, d, F))
     return expert_ffn_swap(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
-                           xp_rows, y_peers, s);
+                           xp_rows, y_peers, nullptr, 0, 0, s);
   constexpr int BN = 256;
   if ((st = ffn_ws_reset(ws, s))) return st;
   TcParams p{};

@@ -340,8 +340,9 @@ def expert_ffn_path(d: int, F: int, E: int, rows: int) -> int:
 
 
 def gathers_rows(d: int, F: int, E: int, rows: int) -> bool:
-    """True when the expert kernel loads token rows from X itself (no permute gather needed)."""
-    return expert_ffn_path(d, F, E, rows) in (PATH_FUSED_1CTA, PATH_FUSED_PAIR)
+    """True when expert_ffn_gather can run this shape (the kernel loads token rows from X itself
+    with TMA tile::gather4, so the permute needs no Xp gather)."""
+    return expert_ffn_path(d, F, E, rows) in (PATH_SWAP_AB, PATH_FUSED_1CTA, PATH_FUSED_PAIR)
 
 
 def expert_ffn_gather(x: torch.Tensor, k: int, offsets: torch.Tensor, perm: torch.Tensor, gate_up: torch.Tensor,

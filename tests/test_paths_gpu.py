@@ -99,6 +99,12 @@ def test_fused_row_gather_is_used(cuda, pair):
     assert all(r["gather"] for r in res)
 
 
+def test_fused_row_gather_swap_ab(cuda):
+    """The swap-AB kernel's token tiles gathered from X (lanes [0, NT/4) each issue one gather4)."""
+    res = _run({"QMOE_SWAP_AB": "1"}, SHAPES)
+    assert all(r["gather"] for r in res)
+
+
 @pytest.mark.parametrize("pair", ["0", "1"], ids=["1cta", "cta-pair"])
 def test_single_launch_equals_two_launches(cuda, pair):
     """The single-launch kernels (expert_fused.cu, 1-CTA and CTA pair) compute every tile exactly

@@ -37,7 +37,7 @@ for T in [int(t) for t in sys.argv[1:]] or [32, 256, 1024, 4096, 8192, 16384]:
     act = torch.empty((T * k, F), dtype=torch.bfloat16, device="cuda")
     t_r = timeit(lambda: K.router(x, wr, k, mode))
     gather = K.gathers_rows(d, F, E, T * k) and os.environ.get("PROBE_GATHER") is not None
-    if gather:  # the fused tile::gather4 A operand (measured ~2x slower than the Xp path on B200)
+    if gather:  # the kernel gathers X rows itself (TMA tile::gather4), the permute skips Xp
         t_p = timeit(lambda: K.permute(ids, E))
         t_f = timeit(lambda: K.expert_ffn_gather(x, k, offsets, perm, gu, dn, y, act_ws=act))
     else:
