@@ -331,6 +331,7 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
   if (warp == 2) ptx::tmem_alloc_cg2<2 * kBN>(&tmem_base_smem);
   ptx::tc_fence_before();
   ptx::cluster_sync();
+  __syncthreads();  // CTA-scope order for the allocator's smem write too (racecheck models this one)
   ptx::tc_fence_after();
   const uint32_t tmem_base = tmem_base_smem;
   const int N1 = map1.total, N2 = map2.total;

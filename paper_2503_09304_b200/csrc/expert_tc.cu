@@ -357,6 +357,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 2) ptx::tmem_alloc_cg2<2 * BN>(&tmem_base_smem);
   ptx::tc_fence_before();
   ptx::cluster_sync();
+  __syncthreads();  // CTA-scope order for the allocator's smem write too (racecheck models this one)
   ptx::tc_fence_after();
   const uint32_t tmem_base = tmem_base_smem;
 
