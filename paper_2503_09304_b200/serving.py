@@ -19,9 +19,26 @@ from .sim import Simulation
 from .workload import WorkloadSpec, trace_for_rate
 
 
-def serve_once(model, trace, scheduler: str, max_batch_size: int = 32, slo_ms: float = 3000.0) -> dict:
+def kv_pages_for(model, capacity_bytes: float, max_batch_size: int) -> dict:
+    """Page-pool kwargs sized for the admission ledger's capacity up front (one allocation, no
+    grow-and-copy next to the model): capacity / (page tokens x layers x entry bytes) pages plus one
+    partially filled page per possible resident sequence."""
+    kw = dict(getattr(model, "kv_page_kwargs", {}))
+    page = kw.get("page_size", 16)
+    per_page = page * model.config.num_layers * model.kv_entry_bytes()
+    kw["initial_pages"] = int(-(-capacity_bytes // per_page)) + 8 * max_batch_size
+    return kw
+
+
+def serve_once(model, trace, scheduler: str, max_batch_size: int = 32, slo_ms: float = 3000.0,
+               kv_capacity_bytes: Optional[float] = None) -> dict:
     torch.cuda.synchronize()
-    sim = Simulation(trace, model=model, scheduler=scheduler, max_batch_size=max_batch_size, clock=WallClock())
+    extra = {}
+    if kv_capacity_bytes is not None:
+        extra = {"cache_capacity_bytes": kv_capacity_bytes,
+                 "kv_page_kwargs": kv_pages_for(model, kv_capacity_bytes, max_batch_size)}
+    sim = Simulation(trace, model=model, scheduler=scheduler, max_batch_size=max_batch_size, clock=WallClock(),
+                     **extra)
     t0 = time.perf_counter()
     res = sim.run()
     wall = time.perf_counter() - t0
@@ -54,9 +71,11 @@ def warm_up(model, max_batch_size: int = 32) -> None:
 
 
 def compare(model, rate: float, duration_s: float, seed: int = 0, max_batch_size: int = 32,
-            slo_ms: float = 3000.0, schedulers=("baseline", "qllm"), workload: Optional[WorkloadSpec] = None) -> dict:
+            slo_ms: float = 3000.0, schedulers=("baseline", "qllm"), workload: Optional[WorkloadSpec] = None,
+            kv_capacity_bytes: Optional[float] = None) -> dict:
     trace = trace_for_rate(replace(workload or WorkloadSpec(), duration_s=duration_s), rate, seed=seed)
-    out = {"rate": rate, "duration_s": duration_s, "jobs": len(trace), "slo_ms": slo_ms}
+    out = {"rate": rate, "duration_s": duration_s, "jobs": len(trace), "slo_ms": slo_ms,
+           "kv_capacity_gib": (kv_capacity_bytes or 8 * 1024**3) / 1024**3}
     for s in schedulers:
-        out["fcfs" if s == "baseline" else s] = serve_once(model, trace, s, max_batch_size, slo_ms)
+        out["fcfs" if s == "baseline" else s] = serve_once(model, trace, s, max_batch_size, slo_ms, kv_capacity_bytes)
     return out

@@ -16,6 +16,8 @@ def main():
     ap.add_argument("--mbs", type=int, default=32)
     ap.add_argument("--slo-ms", type=float, default=3000.0)
     ap.add_argument("--layers", type=int, default=0, help="debug only: fewer layers")
+    ap.add_argument("--kv-gib", type=float, default=0.0,
+                    help="KV admission capacity in GiB (default: the reference's 8 GiB ledger)")
     args = ap.parse_args()
     cfg = MIXTRAL_8X7B if args.model == "mixtral" else QWEN15_MOE_A27B
     if args.layers:
@@ -28,7 +30,8 @@ def main():
     warm_up(model, args.mbs)
     for rate in [float(r) for r in args.rates.split(",")]:
         out = compare(model, rate, args.duration, max_batch_size=args.mbs, slo_ms=args.slo_ms,
-                      schedulers=args.schedulers.split(","))
+                      schedulers=args.schedulers.split(","),
+                      kv_capacity_bytes=args.kv_gib * 1024**3 if args.kv_gib else None)
         out["model"] = cfg.name
         print(json.dumps(out), flush=True)
 
