@@ -94,7 +94,6 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
   const int nt2 = (p.d + kWRows - 1) / kWRows;  // d column blocks (down)
   const int nkb1 = (p.d + kBK - 1) / kBK;
   const int nkb2 = (p.F + kBK - 1) / kBK;
-  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kWRows, NT);
 
   if (warp == 0) build_tile_map(map1, p.offsets, p.e_begin, p.e_end, nullptr, NT, nt1);
   if (warp == 3) build_tile_map(map2, p.offsets, p.e_begin, p.e_end, nullptr, NT, nt2 * p.nsplit);
@@ -219,6 +218,13 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
         ptx::mbar_arrive(&ring_empty[slot]);
         if (++slot == kRing) { slot = 0; rphase ^= 1; }
         if (t < 0) break;
+        // MMA N = the tile's valid token rows rounded up to 16 (an expert's last token tile is
+        // usually partial): the tensor work tracks the real rows instead of NT
+        int e, m0, n0, split = 0;
+        if (t < N1) map1.locate(t, NT, nt1, kWRows, e, m0, n0);
+        else map2.locate(t - N1, NT, nt2 * p.nsplit, kWRows, e, m0, n0, p.nsplit, &split);
+        const int rows = min(NT, p.offsets[e + 1] - m0);
+        const uint32_t kIdesc = ptx::idesc_bf16_f32(kWRows, max(16, (rows + 15) & ~15));
         ptx::mbar_wait(&tempty_bar[acc], aphase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 2 * NT;
@@ -239,8 +245,6 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
         } else {
-          int e, m0, n0, split;
-          map2.locate(t - N1, NT, nt2 * p.nsplit, kWRows, e, m0, n0, p.nsplit, &split);
           const int kb0 = split * p.kb_per_split, kb1 = min(nkb2, kb0 + p.kb_per_split);
           for (int kb = kb0; kb < kb1; kb += C::kKB2) {
             const int nh = C::kKB2 == 2 && kb + 1 < kb1 ? 2 : 1;
