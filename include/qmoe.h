@@ -124,7 +124,9 @@ QMOE_API int qmoe_permute(const int32_t* ids, const int32_t* cursor, int T, int 
  * xp_rows = allocated rows of Xp / act_ws (>= offsets[E]; bounds the TMA tensor maps).
  * workspace: qmoe_expert_ffn_workspace_bytes(variant, dtype, d, xp_rows) bytes of device memory
  * (tile claim counters; for small bf16 SwiGLU batches also the fp32 split-K partials of the down
- * projection, which is then K-split so few-expert launches still fill every SM).
+ * projection, which is then K-split so few-expert launches still fill every SM).  ZERO it once
+ * when it is allocated (cudaMemset): every launch leaves its counter header zeroed again, so no
+ * launch needs a memset in front of it.  Launches sharing a workspace must be stream-ordered.
  */
 QMOE_API size_t qmoe_expert_ffn_workspace_bytes(int variant, int dtype, int d, int xp_rows);
 QMOE_API int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int32_t* offsets,

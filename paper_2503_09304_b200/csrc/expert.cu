@@ -10,14 +10,11 @@ __global__ void ffn_finalize_kernel(FfnWorkspace* ws, const int32_t* limit, int 
   if (limit != nullptr && *limit < c) c = *limit;
   ws->stop = c;
   if (cursor_out != nullptr) *cursor_out = c;
+  ws->next = 0;  // leave the slot zeroed for the next launch (workspace invariant, expert_common.cuh)
+  ws->stop_inv = 0;
 }
 
 }  // namespace
-
-int ffn_ws_reset(FfnWorkspace* ws, cudaStream_t s) {
-  QMOE_CUDA_TRY(cudaMemsetAsync(ws, 0, kFfnHeaderBytes, s));
-  return QMOE_OK;
-}
 
 int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out, cudaStream_t s) {
   ffn_finalize_kernel<<<1, 1, 0, s>>>(ws, limit, e_end, cursor_out);
@@ -53,8 +50,6 @@ static int expert_ffn_entry(int variant, int dtype, const void* xp, const int32_
   FfnWorkspace* ws = reinterpret_cast<FfnWorkspace*>(workspace);
   cudaStream_t s = as_stream(stream);
   if (xp_rows == 0 || e_begin == e_end) {
-    int st = ffn_ws_reset(ws, s);
-    if (st) return st;
     return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
   }
   QMOE_REQUIRE(y_peers == nullptr || (dtype == QMOE_BF16 && variant == QMOE_EXPERT_SWIGLU),
@@ -109,8 +104,6 @@ extern "C" int qmoe_expert_ffn_gather(const void* x, int T, int k, const int32_t
   FfnWorkspace* ws = reinterpret_cast<FfnWorkspace*>(workspace);
   cudaStream_t s = as_stream(stream);
   if (rows == 0 || e_begin == e_end) {
-    int st = ffn_ws_reset(ws, s);
-    if (st) return st;
     return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
   }
   QMOE_REQUIRE(x && offsets && perm && gate_up && down && act_ws && y, "qmoe_expert_ffn_gather: null pointer");

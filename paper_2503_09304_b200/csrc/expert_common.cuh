@@ -24,7 +24,8 @@ struct alignas(128) FfnWorkspace {
   int next;      // next tile index to claim
   int stop_inv;  // INT_MAX - stop expert (0 == no stop yet)
   int stop;      // finalized stop (written by ffn_finalize_kernel, read by chained launches)
-  int pad[29];
+  int exits;     // CTAs that left a single-launch kernel (the last one finalizes, ffn_exit)
+  int pad[28];
 };
 
 constexpr int kFfnWorkspaceSlots = 2;
@@ -33,6 +34,28 @@ constexpr int kFfnWorkspaceSlots = 2;
 constexpr int kFfnMaxExperts = 64;
 constexpr size_t kFfnHeaderBytes = sizeof(FfnWorkspace) * kFfnWorkspaceSlots + kFfnMaxExperts * sizeof(int);
 __host__ __device__ inline int* ffn_done(FfnWorkspace* ws) { return reinterpret_cast<int*>(ws + kFfnWorkspaceSlots); }
+
+// Workspace invariant: between launches every claim counter, vote and completion counter of the
+// header is zero (the caller zeroes the header once at allocation; each launch leaves it so), so
+// no launch needs a memset in front of it.  `stop` survives until the next launch's finalize.
+//
+// Single-launch kernels finalize in-kernel: one thread per CTA calls this after the CTA's last
+// claim and store; the LAST CTA out publishes the stop expert (what ffn_finalize_kernel does for
+// the multi-launch paths), writes cursor_out, and re-zeroes the header for the next launch.
+__device__ __forceinline__ void ffn_exit(FfnWorkspace* ws, int* done, int e_end, int32_t* cursor_out) {
+  __threadfence();
+  const unsigned n = gridDim.x * gridDim.y * gridDim.z;
+  if (atomicAdd(&ws->exits, 1) != (int)n - 1) return;
+  __threadfence();
+  int c = INT_MAX - atomicOr(&ws->stop_inv, 0);
+  if (c > e_end) c = e_end;
+  ws->stop = c;
+  if (cursor_out != nullptr) *cursor_out = c;
+  ws->next = 0;
+  ws->stop_inv = 0;
+  ws->exits = 0;
+  for (int e = 0; e < kFfnMaxExperts; ++e) done[e] = 0;
+}
 
 struct TileMap {
   int e_first;              // absolute id of experts[0]
@@ -197,7 +220,6 @@ __device__ __forceinline__ bool expert_ready(const int* done, int e, int need, c
   }
 }
 
-int ffn_ws_reset(FfnWorkspace* ws, cudaStream_t s);
 // Extra workspace the bf16 SwiGLU path needs for split-K partials of the down projection.
 size_t splitk_bytes(int xp_rows, int d);
 // cursor = min(stop of ws, *limit (optional), e_end); written to ws->stop and cursor_out (optional).

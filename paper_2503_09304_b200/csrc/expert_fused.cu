@@ -49,6 +49,7 @@ struct FusedParams {
   void* const* peers;
   int k;       // top-k: gate_up A rows are x[perm[r] / k] when gather != 0
   int gather;  // 1: gate_up A tiles are gathered from X by the producer warp (TMA tile::gather4)
+  int32_t* cursor;  // optional cursor_out (written by the last CTA out, ffn_exit)
 };
 
 // Token rows of one 128-row A tile for the gather: lane l owns rows [4l, 4l+4) of the tile; rows
@@ -272,6 +273,7 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<2 * kBN>(tmem_base);
@@ -518,6 +520,7 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
+  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_cg2<2 * kBN>(tmem_base);
@@ -541,7 +544,6 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
                      void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s) {
   int st;
-  if ((st = ffn_ws_reset(ws, s))) return st;
   CUtensorMap maps[4];
   // A boxes: 128 token rows (each CTA of a pair loads its own 128), or single rows of X for the
   // tile::gather4 loads (x != nullptr); B boxes: 128 weight rows
@@ -565,6 +567,7 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
   p.peers = y_peers;
   p.k = k;
   p.gather = x != nullptr;
+  p.cursor = cursor_out;
   static bool attr_set = false;
   if (!attr_set) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemF));
@@ -575,8 +578,7 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
     ffn_fused_pair_kernel<<<(tc_num_sms() / 2) * 2, kThreadsF, kSmemP, s>>>(maps[0], maps[1], maps[2], maps[3], p);
   else
     ffn_fused_kernel<<<tc_num_sms(), kThreadsF, kSmemF, s>>>(maps[0], maps[1], maps[2], maps[3], p);
-  if ((st = check_launch("qmoe_expert_ffn(tcgen05 single launch)"))) return st;
-  return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
+  return check_launch("qmoe_expert_ffn(tcgen05 single launch)");
 }
 
 }  // namespace qmoe

@@ -121,8 +121,7 @@ int run_simt(int variant, const void* xp, const int32_t* offsets, const int32_t*
              const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
              const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, cudaStream_t s) {
   const int grid = 148 * 4;
-  int st = ffn_ws_reset(ws, s);
-  if (st) return st;
+  int st;
   if (variant == QMOE_EXPERT_TANH_AFFINE) {
     ffn_simt_kernel<T, EPI_TANH><<<grid, kThreads, 0, s>>>((const T*)xp, offsets, perm, E, d, d, (const T*)w1,
                                                           (const T*)w2, e_begin, e_end, nullptr, (T*)y, flag,

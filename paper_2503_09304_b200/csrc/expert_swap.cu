@@ -58,6 +58,7 @@ struct SwapParams {
   void* const* peers;  // expert parallel over peer memory: per-rank slot buffers (see out_row)
   int k;               // top-k: gate_up B rows are x[perm[r] / k] when gather != 0
   int gather;          // 1: token rows gathered from X by the producer warp (TMA tile::gather4)
+  int32_t* cursor;     // optional cursor_out (written by the last CTA out, ffn_exit)
 };
 
 template <int NT>
@@ -339,6 +340,7 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
@@ -418,7 +420,6 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
                     void* const* y_peers, const void* x, int T, int k, cudaStream_t s) {
   int st;
-  if ((st = ffn_ws_reset(ws, s))) return st;
   // Token tile: 32 rows when experts see ~1-24 rows on average (decode), 64 up to ~64, else 128.
   const double mean_rows = (double)xp_rows / (E > 0 ? E : 1);
   const int NT = mean_rows <= 24.0 ? 32 : (mean_rows <= 64.0 ? 64 : 128);
@@ -442,6 +443,7 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
   p.peers = y_peers;
   p.k = k;
   p.gather = x != nullptr;
+  p.cursor = cursor_out;
   const int nkb2 = (F + kBK - 1) / kBK;
   const int want = xp_rows <= kSwapRowsMax ? swap_splits(F) : 1;  // partials sized for <= 512 rows
   p.kb_per_split = (nkb2 + want - 1) / want;
@@ -451,7 +453,6 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
   if ((st = NT == 32 ? launch_swap<32>(maps, p, s)
                      : (NT == 64 ? launch_swap<64>(maps, p, s) : launch_swap<128>(maps, p, s))))
     return st;
-  if ((st = ffn_finalize(ws, nullptr, e_end, cursor_out, s))) return st;
   if (p.nsplit > 1) {
     const long long work = (long long)xp_rows * (d / 8);
     const int grid = (int)std::min<long long>((work + 255) / 256, 148 * 8);

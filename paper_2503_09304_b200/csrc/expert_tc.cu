@@ -604,7 +604,6 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
     return expert_ffn_swap(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
                            xp_rows, y_peers, nullptr, 0, 0, s);
   constexpr int BN = 256;
-  if ((st = ffn_ws_reset(ws, s))) return st;
   TcParams p{};
   p.e_begin = e_begin;
   p.e_end = e_end;

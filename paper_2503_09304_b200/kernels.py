@@ -58,11 +58,12 @@ def acc_dtype(dtype: torch.dtype) -> torch.dtype:
 
 
 def workspace(nbytes: int, tag: str, device: torch.device) -> torch.Tensor:
-    """Stream-ordered scratch, grown on demand and reused (one buffer per device/stream/tag)."""
+    """Stream-ordered scratch, grown on demand and reused (one buffer per device/stream/tag).
+    Zeroed when allocated: the expert-FFN workspace header must start zeroed (qmoe.h)."""
     key = (device.index or 0, _stream(), tag)
     buf = _workspaces.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
         _workspaces[key] = buf
     return buf
 
