@@ -197,15 +197,16 @@ def make_layer(rank: int, world: int, device, transport: str = "p2p", max_tokens
 
 def count_launches(T: int, world: int, transport: str = "p2p") -> int:
     """Our kernels per MoE-layer step: router 1; permute count+scatter(+gather) 2-3; expert FFN:
-    the single-launch kernels (swap-AB / fused tcgen05) + finalize = 2 (+1 split-K reduce for the
-    K-split swap-AB path), the two-launch kernels = 4; combine 1.  EP over NCCL adds the regroup
+    the single-launch kernels (swap-AB, swap-AB pair, fused tcgen05; they finalize in-kernel) = 1
+    (+1 split-K reduce for the K-split swap-AB path), the two-launch kernels = 4; combine 1.  EP over NCCL adds the regroup
     gather and the return scatter; EP over peer memory replaces the permute's gather with the
     dispatch kernel and adds two flag barriers."""
     from paper_2503_09304_b200 import kernels as K
 
     rows = T * TOPK  # a rank's expert launch sees ~T*k rows under uniform routing (EP: from all ranks)
     path = K.expert_ffn_path(D, F, E // world, rows)
-    ffn = {K.PATH_SWAP_AB: 2 + (1 if rows <= 512 else 0), K.PATH_FUSED_1CTA: 2, K.PATH_FUSED_PAIR: 2}.get(path, 4)
+    ffn = {K.PATH_SWAP_AB: 1 + (1 if rows <= 512 else 0), K.PATH_SWAP_PAIR: 1, K.PATH_FUSED_1CTA: 1,
+           K.PATH_FUSED_PAIR: 1}.get(path, 4)
     if world > 1 and transport == "p2p":
         return 1 + K.permute_launches(T, TOPK, gather=False) + 1 + 2 + ffn + 1
     return 1 + K.permute_launches(T, TOPK) + ffn + 1 + (2 if world > 1 else 0)

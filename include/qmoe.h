@@ -77,6 +77,7 @@ extern "C" {
 #define QMOE_PATH_FUSED_PAIR 3        /* 256x256 CTA-pair tiles, gate_up+down in one launch        */
 #define QMOE_PATH_TWO_LAUNCH_1CTA 4   /* 128x256 tiles, one launch per projection (split-K small)  */
 #define QMOE_PATH_TWO_LAUNCH_PAIR 5   /* 256x256 CTA-pair tiles, one launch per projection         */
+#define QMOE_PATH_SWAP_PAIR 6         /* swap-AB CTA pair: 256 weight rows x <=256 tokens, 1 launch */
 
 QMOE_API int qmoe_version(void);
 QMOE_API const char* qmoe_status_string(int status);
@@ -144,8 +145,8 @@ QMOE_API int qmoe_expert_ffn_path(int d, int F, int E, int xp_rows);
  * Grouped bf16 SwiGLU experts reading the token rows straight from X (no gathered Xp): the i-th
  * row of expert e is X[perm[offsets[e] + i] / k], loaded by the GEMM's producer warp with TMA
  * tile::gather4 (4 arbitrary rows per instruction) -- the permute's row gather fused into the
- * A-operand (token-row) load.  For the single-launch paths (QMOE_PATH_SWAP_AB / _FUSED_1CTA /
- * _FUSED_PAIR for xp_rows = T*k); other paths return QMOE_ERR_UNSUPPORTED (callers gather with
+ * A-operand (token-row) load.  For the single-launch paths (QMOE_PATH_SWAP_AB / _SWAP_PAIR /
+ * _FUSED_1CTA / _FUSED_PAIR for xp_rows = T*k); other paths return QMOE_ERR_UNSUPPORTED (callers gather with
  * qmoe_permute).  Measured on B200 it does not pay: on the 128/256-row tiles it is ~2x slower
  * than qmoe_permute's gather + qmoe_expert_ffn (32 gather4 instructions per 64-wide K step per CTA
  * saturate the TMA issue path, where an Xp tile is one instruction); on the swap-AB decode path it

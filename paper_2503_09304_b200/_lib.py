@@ -40,6 +40,7 @@ QMOE_PATH_FUSED_1CTA = 2
 QMOE_PATH_FUSED_PAIR = 3
 QMOE_PATH_TWO_LAUNCH_1CTA = 4
 QMOE_PATH_TWO_LAUNCH_PAIR = 5
+QMOE_PATH_SWAP_PAIR = 6
 
 _c_int = ctypes.c_int
 _c_size = ctypes.c_size_t

@@ -110,7 +110,8 @@ extern "C" int qmoe_expert_ffn_gather(const void* x, int T, int k, const int32_t
   QMOE_REQUIRE(((uintptr_t)x | (uintptr_t)gate_up | (uintptr_t)y | (uintptr_t)act_ws) % 16 == 0,
                "qmoe_expert_ffn_gather: buffers must be 16-byte aligned");
   const int path = expert_ffn_path(d, F, E, rows);
-  if (path != QMOE_PATH_SWAP_AB && path != QMOE_PATH_FUSED_1CTA && path != QMOE_PATH_FUSED_PAIR) {
+  if (path != QMOE_PATH_SWAP_AB && path != QMOE_PATH_SWAP_PAIR && path != QMOE_PATH_FUSED_1CTA &&
+      path != QMOE_PATH_FUSED_PAIR) {
     set_error("qmoe_expert_ffn_gather: path %d has no fused row gather (use qmoe_permute's gather)", path);
     return QMOE_ERR_UNSUPPORTED;
   }
@@ -119,6 +120,9 @@ extern "C" int qmoe_expert_ffn_gather(const void* x, int T, int k, const int32_t
   if (path == QMOE_PATH_SWAP_AB)
     return expert_ffn_swap(nullptr, offsets, perm, E, d, F, gate_up, down, e_begin, e_end, act_ws, y, preempt_flag,
                            cursor_out, ws, rows, nullptr, x, T, k, s);
+  if (path == QMOE_PATH_SWAP_PAIR)
+    return expert_ffn_swap_pair(nullptr, offsets, perm, E, d, F, gate_up, down, e_begin, e_end, act_ws, y,
+                                preempt_flag, cursor_out, ws, rows, nullptr, x, T, k, s);
   return expert_ffn_fused(nullptr, offsets, perm, E, d, F, gate_up, down, e_begin, e_end, act_ws, y, preempt_flag,
                           cursor_out, ws, rows, nullptr, path == QMOE_PATH_FUSED_PAIR, x, T, k, s);
 }

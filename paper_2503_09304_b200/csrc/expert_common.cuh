@@ -247,6 +247,13 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
                      const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
                      void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s);
+// Mid-size batches of fine-grained experts (expert_fused.cu): swap-AB CTA-pair tiles (256 weight
+// rows x <= 256 tokens, N sized to the valid rows), gate_up and down in one persistent launch.
+bool use_swap_pair(int xp_rows, int n_experts, int d, int F);
+int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
+                         const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
+                         const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
+                         void* const* y_peers, const void* x, int T, int k, cudaStream_t s);
 // Which bf16 SwiGLU kernel qmoe_expert_ffn runs for this shape (QMOE_PATH_* in qmoe.h).
 int expert_ffn_path(int d, int F, int E, int xp_rows);
 

@@ -527,6 +527,293 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
   }
 }
 
+// ================================================================================================
+// Swap-AB CTA pair (cta_group::2): WEIGHT rows on the MMA's M side (256 per unit, 128 per CTA),
+// token rows on N, N = the unit's valid token rows rounded up to 16 (<= 256; each CTA supplies
+// N/2 token rows).  For fine-grained experts (Qwen: ~270 rows per expert at 4k tokens) the
+// token-row padding of a 256-row M tile (the pair kernel above) or a 128-row one (the 1-CTA
+// kernel) wastes 30-50% of the tensor work; here it is < 16 rows per token tile, at the pair's
+// operand traffic (each SM stages 128 weight rows + N/2 token rows per K block).
+//   gate_up unit = (expert, 128 F columns f0, <= 256 tokens): CTA c stages gate rows
+//                  f0 + 64c + [0, 64) over up rows F + f0 + 64c + [0, 64), so its TMEM lanes
+//                  [0, 64) hold gate and [64, 128) the matching up rows; the up warps hand their
+//                  rows to the gate warps through shared memory for SiLU(g) * u;
+//   down unit    = (expert, 256 d columns, <= 256 tokens), CTA c owns d columns + 128c.
+// Same claim / ring / completion-counter / preemption protocol as ffn_fused_pair_kernel.
+constexpr int kStagesSP = 6;
+constexpr int kTokSP = 256;                     // token rows per unit
+constexpr int kHalfSP = 128 * kBKf * 2;         // 16 KB: this CTA's weight rows, then its token rows
+constexpr int kStageBytesSP = 2 * kHalfSP;
+constexpr int kSmemSP = kStagesSP * kStageBytesSP + 1024;
+
+__device__ __forceinline__ int sp_ncols(int rows) { return rows < 16 ? 16 : (rows + 15) & ~15; }
+
+// Token-row boxes of 32 / 64 / 128 rows: a CTA stages the smallest box holding its N/2 rows, so a
+// short token tile (an expert's remainder rows) does not pay a full 128-row operand load.
+struct alignas(64) SpMaps {
+  CUtensorMap tok[2][3];  // [Xp (or X for tile::gather4), act][box 32, 64, 128]
+  CUtensorMap w1, w2;     // 64-row gate / up boxes, 128-row down boxes
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsF, 1)
+ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStagesSP], empty_bar[kStagesSP];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t ring_full[kRingF], ring_empty[kRingF];
+  __shared__ int ring_tile[kRingF];
+  __shared__ uint32_t tmem_base_smem;
+  __shared__ TileMap map1, map2;
+  __shared__ float sp_xg[2][32][17], sp_xu[2][32][17];       // gate <-> up halves (warp pairs 0/2, 1/3)
+  __shared__ __align__(16) __nv_bfloat16 sp_out[32][128 + 8];  // one 32-token chunk of output rows
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int nt1 = (p.F + 127) / 128, nt2 = (p.d + 255) / 256;
+  const int nkb1 = (p.d + kBKf - 1) / kBKf, nkb2 = (p.F + kBKf - 1) / kBKf;
+
+  if (warp == 0) build_tile_map(map1, p.offsets, p.e_begin, p.e_end, nullptr, kTokSP, nt1);
+  if (warp == 3) build_tile_map(map2, p.offsets, p.e_begin, p.e_end, nullptr, kTokSP, nt2);
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < kStagesSP; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull_bar[a], 1);
+      ptx::mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    for (int i = 0; i < kRingF; ++i) {
+      ptx::mbar_init(&ring_full[i], 1);
+      ptx::mbar_init(&ring_empty[i], 10);  // leader: MMA + 4 epi; peer: producer + 4 epi
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_cg2<2 * kTokSP>(&tmem_base_smem);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = tmem_base_smem;
+  const int N1 = map1.total, N2 = map2.total;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      for (int i = 0; i < 6; ++i) ptx::tma_prefetch_desc(&maps.tok[i / 3][i % 3]);
+      ptx::tma_prefetch_desc(&maps.w1);
+      ptx::tma_prefetch_desc(&maps.w2);
+    }
+    int stage = 0, slot = 0, last_e = -1;
+    uint32_t phase = 0, rphase = 0;
+    int pending = (lane == 0 && leader) ? atomicAdd(&p.ws->next, 1) : 0;  // claim one unit ahead
+    while (true) {
+      int t = -1;
+      if (lane == 0) {
+        if (leader) {
+          while (true) {
+            t = resolve_claim(map1, N2, p.ws, p.flag, last_e, pending);
+            if (t >= N1) {
+              int e2, m2, n2;
+              map2.locate(t - N1, kTokSP, nt2, 256, e2, m2, n2);
+              if (!expert_ready(p.done, e2, map1.m_tiles[e2 - map1.e_first] * nt1 * 8, p.ws)) {
+                pending = atomicAdd(&p.ws->next, 1);
+                continue;
+              }
+              fence_proxy_async_global();
+            }
+            break;
+          }
+          ptx::mbar_wait_cluster(&ring_empty[slot], rphase ^ 1);
+          ring_tile[slot] = t;
+          ptx::st_remote_u32(&ring_tile[slot], 1, (uint32_t)t);
+          ptx::mbar_arrive(&ring_full[slot]);
+          ptx::mbar_arrive_remote(&ring_full[slot], 1);
+          if (t >= 0) pending = atomicAdd(&p.ws->next, 1);
+        } else {
+          ptx::mbar_wait_cluster(&ring_full[slot], rphase);
+          t = ring_tile[slot];
+          ptx::mbar_arrive_remote(&ring_empty[slot], 0);
+          if (t >= N1) {
+            int e2, m2, n2;
+            map2.locate(t - N1, kTokSP, nt2, 256, e2, m2, n2);
+            (void)ld_acquire(p.done + e2);  // the leader saw it complete; acquire it here too
+            fence_proxy_async_global();
+          }
+        }
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+      if (t < 0) break;
+      const bool up = t < N1;
+      int e, m0, n0;
+      if (up) map1.locate(t, kTokSP, nt1, 128, e, m0, n0);
+      else map2.locate(t - N1, kTokSP, nt2, 256, e, m0, n0);
+      const int row_end = p.offsets[e + 1];
+      const int half = sp_ncols(min(kTokSP, row_end - m0)) >> 1;
+      const int tok = m0 + (int)rank * half;  // this CTA's N/2 token rows
+      const int bi = half <= 32 ? 0 : (half <= 64 ? 1 : 2);
+      const int box = 32 << bi;
+      const CUtensorMap* tm = &maps.tok[up ? 0 : 1][up && p.gather ? 0 : bi];
+      const bool gather = up && p.gather;
+      int g[4] = {0, 0, 0, 0};
+      if (gather) gather_rows4(p, tok, row_end, lane, g);
+      const int wrow = up ? e * 2 * p.F + n0 + (int)rank * 64 : e * p.d + n0 + (int)rank * 128;
+      const int nkb = up ? nkb1 : nkb2;
+      for (int kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait_cluster(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * kStageBytesSP;
+        if (lane == 0) {
+          if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * (kHalfSP + box * kBKf * 2));
+          if (up) {  // 64 gate rows over the 64 matching up rows
+            ptx::tma_load_2d_cg2(&maps.w1, &full_bar[stage], sa, kb * kBKf, wrow, ptx::kEvictNormal);
+            ptx::tma_load_2d_cg2(&maps.w1, &full_bar[stage], sa + kHalfSP / 2, kb * kBKf, wrow + p.F, ptx::kEvictNormal);
+          } else {
+            ptx::tma_load_2d_cg2(&maps.w2, &full_bar[stage], sa, kb * kBKf, wrow, ptx::kEvictNormal);
+          }
+          if (!gather) ptx::tma_load_2d_cg2(tm, &full_bar[stage], sa + kHalfSP, kb * kBKf, tok, ptx::kEvictNormal);
+        }
+        if (gather && lane < box / 4)
+          ptx::tma_gather4_cg2(tm, &full_bar[stage], sa + kHalfSP + lane * 512, kb * kBKf, g[0], g[1], g[2], g[3],
+                               ptx::kEvictNormal);
+        if (++stage == kStagesSP) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      int stage = 0, slot = 0, acc = 0;
+      uint32_t phase = 0, rphase = 0, aphase = 0;
+      while (true) {
+        ptx::mbar_wait_cluster(&ring_full[slot], rphase);
+        const int t = ring_tile[slot];
+        ptx::mbar_arrive(&ring_empty[slot]);
+        if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+        if (t < 0) break;
+        int e, m0, n0;
+        if (t < N1) map1.locate(t, kTokSP, nt1, 128, e, m0, n0);
+        else map2.locate(t - N1, kTokSP, nt2, 256, e, m0, n0);
+        const uint32_t idesc = ptx::idesc_bf16_f32(256, sp_ncols(min(kTokSP, p.offsets[e + 1] - m0)));
+        const int nkb = t < N1 ? nkb1 : nkb2;
+        ptx::mbar_wait_cluster(&tempty_bar[acc], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kTokSP;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem + stage * kStageBytesSP);
+          const uint32_t b_addr = a_addr + kHalfSP;
+#pragma unroll
+          for (int k = 0; k < kBKf / 16; ++k)
+            ptx::tc_mma_bf16_cg2(d_tmem, ptx::sw128_kmajor_desc(a_addr + k * 32),
+                                 ptx::sw128_kmajor_desc(b_addr + k * 32), idesc, (kb | k) != 0);
+          ptx::tc_commit_cg2(&empty_bar[stage], 0x3);
+          if (++stage == kStagesSP) { stage = 0; phase ^= 1; }
+        }
+        ptx::tc_commit_cg2(&tfull_bar[acc], 0x3);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kEpiF) {
+    // ------------------------------------------------------------------ epilogue (both CTAs)
+    // Thread (ew, lane) owns TMEM lane 32 ew + lane = one weight row, columns = the unit's tokens.
+    const int ew = warp - kEpiF;
+    int slot = 0, acc = 0;
+    uint32_t rphase = 0, aphase = 0;
+    while (true) {
+      ptx::mbar_wait_cluster(&ring_full[slot], rphase);
+      const int t = ring_tile[slot];
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&ring_empty[slot]);
+        else ptx::mbar_arrive_remote(&ring_empty[slot], 0);
+      }
+      if (++slot == kRingF) { slot = 0; rphase ^= 1; }
+      if (t < 0) break;
+      const bool up = t < N1;
+      int e, m0, n0;
+      if (up) map1.locate(t, kTokSP, nt1, 128, e, m0, n0);
+      else map2.locate(t - N1, kTokSP, nt2, 256, e, m0, n0);
+      const int rows = min(kTokSP, p.offsets[e + 1] - m0);  // uniform over the CTA
+      ptx::mbar_wait_cluster(&tfull_bar[acc], aphase);
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * kTokSP;
+      const int et = threadIdx.x - kEpiF * 32;  // 0..127 over the epilogue warps
+#pragma unroll 1
+      for (int c = 0; c < rows; c += 32) {
+        uint32_t v[32];
+        ptx::tmem_ld32(t_row + c, v);
+        ptx::tmem_ld_wait();
+        if (up) {
+          // warp pair q = ew & 1 holds gate (ew = q) and up (ew = q + 2) of the same 32 features:
+          // the gate warp finishes tokens [0, 16) of the chunk, the up warp tokens [16, 32)
+          const int q = ew & 1;
+          const bool gate = ew < 2;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (gate) sp_xg[q][lane][j] = __uint_as_float(v[16 + j]);
+            else sp_xu[q][lane][j] = __uint_as_float(v[j]);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float gv = gate ? __uint_as_float(v[j]) : sp_xg[q][lane][j];
+            const float uv = gate ? sp_xu[q][lane][j] : __uint_as_float(v[16 + j]);
+            sp_out[(gate ? 0 : 16) + j][32 * q + lane] = __float2bfloat16_rn(gv / (1.f + __expf(-gv)) * uv);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          // 32 token rows x 64 features (128 B) of act, 16-byte stores
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int idx = et + 128 * i, r = idx >> 3, vq = idx & 7;
+            const int f = n0 + (int)rank * 64 + 8 * vq;
+            if (c + r < rows && f < p.F)
+              *reinterpret_cast<uint4*>(p.act + (size_t)(m0 + c + r) * p.F + f) =
+                  *reinterpret_cast<const uint4*>(&sp_out[r][8 * vq]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sp_out[j][32 * ew + lane] = __float2bfloat16_rn(__uint_as_float(v[j]));
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          // 32 token rows x 128 output columns (256 B) scattered to the token slots
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int idx = et + 128 * i, r = idx >> 4, vq = idx & 15;
+            const int col = n0 + (int)rank * 128 + 8 * vq;
+            if (c + r < rows && col < p.d)
+              *reinterpret_cast<uint4*>(out_row(p.y, p.peers, p.perm[m0 + c + r], p.d) + col) =
+                  *reinterpret_cast<const uint4*>(&sp_out[r][8 * vq]);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // sp_out / exchange reused by the next chunk
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&tempty_bar[acc]);
+        else ptx::mbar_arrive_remote(&tempty_bar[acc], 0);
+      }
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+      if (up) {
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.done + e, 1);
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor);
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg2<2 * kTokSP>(tmem_base);
+  }
+}
+
 }  // namespace
 
 // The single-launch path for the 1-CTA tile shape (mid-size batches and fine-grained experts);
@@ -579,6 +866,67 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
   else
     ffn_fused_kernel<<<tc_num_sms(), kThreadsF, kSmemF, s>>>(maps[0], maps[1], maps[2], maps[3], p);
   return check_launch("qmoe_expert_ffn(tcgen05 single launch)");
+}
+
+// Batches past the swap-AB range (checked first) of coarse experts: the swap-AB CTA-pair kernel,
+// whose token tiles pad to 16 rows instead of 256.  Same-box eager A/B on B200 (tools/ffn_ab.py,
+// FFN alone, L2 flushed): Mixtral 768/1k/2k tokens 0.54/0.72/1.18 ms vs 0.58/0.80/1.25 on the
+// 256-row pair tiles, tied (+-2%) at 4k-16k.  Fine-grained experts (Qwen, 60 experts) lose 3-10%
+// at 1.5k-16k tokens except at 2k (+6%), and a single expert (Qwen's shared expert) loses 17-25%
+// (ncu: tensor pipe 58% vs 72% active with neither operand loads nor the epilogue on the critical
+// path -- open), so the path is used for 4..16 experts.  QMOE_SWAP_PAIR=0/1 forces it off/on (when
+// the shape allows it: d % 256 == 0, F % 128 == 0).
+bool use_swap_pair(int xp_rows, int n_experts, int d, int F) {
+  static int forced = [] {
+    const char* v = getenv("QMOE_SWAP_PAIR");
+    return v == nullptr ? -1 : atoi(v);
+  }();
+  if (d % 256 != 0 || F % 128 != 0 || n_experts < 1 || n_experts > kFfnMaxExperts) return false;
+  if (forced >= 0) return forced == 1;
+  (void)xp_rows;
+  return n_experts >= 4 && n_experts <= 16;
+}
+
+int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
+                         const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
+                         const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
+                         void* const* y_peers, const void* x, int T, int k, cudaStream_t s) {
+  int st;
+  SpMaps maps;
+  // tokens: 32/64/128-row boxes of Xp / act (each CTA loads its N/2 rows from the box start), or
+  // single rows of X for tile::gather4; weights: 64-row gate / up boxes, 128-row down boxes
+  for (int b = 0; b < 3; ++b) {
+    if ((st = x != nullptr ? tc_make_map(&maps.tok[0][b], x, T, d, 1)
+                           : tc_make_map(&maps.tok[0][b], xp, xp_rows, d, 32 << b)) ||
+        (st = tc_make_map(&maps.tok[1][b], act_ws, xp_rows, F, 32 << b)))
+      return st;
+  }
+  if ((st = tc_make_map(&maps.w1, w1, (uint64_t)E * 2 * F, d, 64)) ||
+      (st = tc_make_map(&maps.w2, w2, (uint64_t)E * d, F, 128)))
+    return st;
+  FusedParams p{};
+  p.d = d;
+  p.F = F;
+  p.e_begin = e_begin;
+  p.e_end = e_end;
+  p.offsets = offsets;
+  p.perm = perm;
+  p.flag = flag;
+  p.ws = ws;
+  p.done = ffn_done(ws);
+  p.act = (__nv_bfloat16*)act_ws;
+  p.y = (__nv_bfloat16*)y;
+  p.peers = y_peers;
+  p.k = k;
+  p.gather = x != nullptr;
+  p.cursor = cursor_out;
+  static bool attr_set = false;
+  if (!attr_set) {
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_swap_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSP));
+    attr_set = true;
+  }
+  ffn_swap_pair_kernel<<<(tc_num_sms() / 2) * 2, kThreadsF, kSmemSP, s>>>(maps, p);
+  return check_launch("qmoe_expert_ffn(tcgen05 swap-AB pair)");
 }
 
 }  // namespace qmoe

@@ -603,6 +603,9 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   if (variant == QMOE_EXPERT_SWIGLU && use_swap_ab(xp_rows, E, d, F))
     return expert_ffn_swap(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
                            xp_rows, y_peers, nullptr, 0, 0, s);
+  if (variant == QMOE_EXPERT_SWIGLU && use_swap_pair(xp_rows, E, d, F))
+    return expert_ffn_swap_pair(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
+                                xp_rows, y_peers, nullptr, 0, 0, s);
   constexpr int BN = 256;
   TcParams p{};
   p.e_begin = e_begin;
@@ -662,6 +665,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
 int expert_ffn_path(int d, int F, int E, int xp_rows) {
   if (d % 64 != 0 || F % 64 != 0) return QMOE_PATH_UNSUPPORTED;
   if (use_swap_ab(xp_rows, E, d, F)) return QMOE_PATH_SWAP_AB;
+  if (use_swap_pair(xp_rows, E, d, F)) return QMOE_PATH_SWAP_PAIR;
   const bool pair = use_cta_pair(xp_rows, E);
   if (down_splits(xp_rows, E, d, F) == 1 && use_fused_tc()) return pair ? QMOE_PATH_FUSED_PAIR : QMOE_PATH_FUSED_1CTA;
   return pair ? QMOE_PATH_TWO_LAUNCH_PAIR : QMOE_PATH_TWO_LAUNCH_1CTA;

@@ -333,6 +333,7 @@ def expert_ffn_peer(xp: torch.Tensor, offsets: torch.Tensor, ret: torch.Tensor, 
 # ------------------------------------------------------------------ fused row gather
 
 PATH_SWAP_AB, PATH_FUSED_1CTA, PATH_FUSED_PAIR = _lib.QMOE_PATH_SWAP_AB, _lib.QMOE_PATH_FUSED_1CTA, _lib.QMOE_PATH_FUSED_PAIR
+PATH_SWAP_PAIR = _lib.QMOE_PATH_SWAP_PAIR
 
 
 def expert_ffn_path(d: int, F: int, E: int, rows: int) -> int:
@@ -343,7 +344,7 @@ def expert_ffn_path(d: int, F: int, E: int, rows: int) -> int:
 def gathers_rows(d: int, F: int, E: int, rows: int) -> bool:
     """True when expert_ffn_gather can run this shape (the kernel loads token rows from X itself
     with TMA tile::gather4, so the permute needs no Xp gather)."""
-    return expert_ffn_path(d, F, E, rows) in (PATH_SWAP_AB, PATH_FUSED_1CTA, PATH_FUSED_PAIR)
+    return expert_ffn_path(d, F, E, rows) in (PATH_SWAP_AB, PATH_SWAP_PAIR, PATH_FUSED_1CTA, PATH_FUSED_PAIR)
 
 
 def expert_ffn_gather(x: torch.Tensor, k: int, offsets: torch.Tensor, perm: torch.Tensor, gate_up: torch.Tensor,

@@ -1,4 +1,4 @@
-"""Every bf16 expert-FFN code path, forced through the QMOE_SWAP_AB / QMOE_CTA_PAIR switches (read
+"""Every bf16 expert-FFN code path, forced through the QMOE_SWAP_AB / QMOE_SWAP_PAIR / QMOE_CTA_PAIR switches (read
 once per process, so each configuration runs in its own interpreter), against the torch fp32
 restatement of HF MixtralExperts on the same bf16 inputs: swap-AB with 32/64/128-row token tiles,
 the 1-CTA 128-row tcgen05 kernel and the CTA-pair 256-row kernel, plus a preempted launch and its
@@ -86,22 +86,26 @@ def _run(env, shapes):
     return res
 
 
-@pytest.mark.parametrize("env", [{"QMOE_SWAP_AB": "1"}, {"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "0"},
-                                 {"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": "1"}],
-                         ids=["swap-ab", "tc-1cta-single-launch", "tc-pair"])
+@pytest.mark.parametrize("env", [{"QMOE_SWAP_AB": "1"}, {"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "1"},
+                                 {"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "0", "QMOE_CTA_PAIR": "0"},
+                                 {"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "0", "QMOE_CTA_PAIR": "1"}],
+                         ids=["swap-ab", "swap-pair", "tc-1cta-single-launch", "tc-pair"])
 def test_forced_expert_path(cuda, env):
-    _run(env, SHAPES if env.get("QMOE_SWAP_AB") == "1" else [s for s in SHAPES if s[0] * s[4] > 512])
+    _run(env, SHAPES if env.get("QMOE_SWAP_AB") == "1" or env.get("QMOE_SWAP_PAIR") == "1"
+         else [s for s in SHAPES if s[0] * s[4] > 512])
 
 
 @pytest.mark.parametrize("pair", ["0", "1"], ids=["1cta", "cta-pair"])
 def test_fused_row_gather_is_used(cuda, pair):
-    res = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": pair}, [s for s in SHAPES if s[0] * s[4] > 512])
+    res = _run({"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "0", "QMOE_CTA_PAIR": pair}, [s for s in SHAPES if s[0] * s[4] > 512])
     assert all(r["gather"] for r in res)
 
 
-def test_fused_row_gather_swap_ab(cuda):
-    """The swap-AB kernel's token tiles gathered from X (lanes [0, NT/4) each issue one gather4)."""
-    res = _run({"QMOE_SWAP_AB": "1"}, SHAPES)
+@pytest.mark.parametrize("env", [{"QMOE_SWAP_AB": "1"}, {"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "1"}],
+                         ids=["swap-ab", "swap-pair"])
+def test_fused_row_gather_swap_ab(cuda, env):
+    """The swap-AB kernels' token tiles gathered from X (tile::gather4)."""
+    res = _run(env, SHAPES)
     assert all(r["gather"] for r in res)
 
 
@@ -110,8 +114,8 @@ def test_single_launch_equals_two_launches(cuda, pair):
     """The single-launch kernels (expert_fused.cu, 1-CTA and CTA pair) compute every tile exactly
     like the two-launch paths (same tiles, same MMA order, same epilogue): bit-identical outputs."""
     shapes = [s for s in SHAPES if s[0] * s[4] > 512]
-    one = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": pair}, shapes)
-    two = _run({"QMOE_SWAP_AB": "0", "QMOE_CTA_PAIR": pair, "QMOE_FUSED": "0"}, shapes)
+    one = _run({"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "0", "QMOE_CTA_PAIR": pair}, shapes)
+    two = _run({"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "0", "QMOE_CTA_PAIR": pair, "QMOE_FUSED": "0"}, shapes)
     assert [r["sha"] for r in one] == [r["sha"] for r in two]
 
 
@@ -153,19 +157,20 @@ print(json.dumps(out))
 """
 
 
-def test_preempt_flag_raised_mid_launch(cuda):
+@pytest.mark.parametrize("env", [{}, {"QMOE_SWAP_PAIR": "0"}], ids=["default-paths", "token-row-tiles"])
+def test_preempt_flag_raised_mid_launch(cuda, env):
     """The device flag raised by another stream WHILE the grouped GEMM runs (the serving engine's
     wall-clock path) on every bf16 kernel path: the launch stops at an expert boundary >= 2 (or runs
     to the end if the flag came too late), every expert below the stop is complete and equal to an
     uninterrupted launch, and resuming from the cursor completes the layer bit-identically."""
     cases = [(32, 2048, 4096, 8, 2, d) for d in (0, 20000, 200000)]           # swap-AB
-    cases += [(1200, 2048, 4096, 8, 2, d) for d in (0, 20000, 60000)]        # fused 128-row tiles
-    cases += [(3000, 1024, 1408, 60, 4, d) for d in (0, 10000, 30000)]       # fused 256-row pair
+    cases += [(1200, 2048, 4096, 8, 2, d) for d in (0, 20000, 60000)]        # swap-AB pair / fused 128-row tiles
+    cases += [(3000, 1024, 1408, 60, 4, d) for d in (0, 10000, 30000)]       # swap-AB pair / fused 256-row pair
     out = subprocess.run([sys.executable, "-c", RACE, str(ROOT), json.dumps(cases)], capture_output=True, text=True,
-                         timeout=600)
+                         env={**os.environ, **env}, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     res = json.loads(out.stdout.strip().splitlines()[-1])
-    assert {r["path"] for r in res} >= {1, 2, 3}, res
+    assert {r["path"] for r in res} >= ({1, 6} if not env else {1, 2, 3}), res
     assert any(r["stop"] < 8 for r in res), res  # at least some launches really stopped mid-way
     for r in res:
         assert r["stop"] >= 2, r

@@ -4,7 +4,8 @@ sys.path.insert(0, ".")
 from paper_2503_09304_b200 import kernels as K
 
 import os
-SHAPES = {"mixtral": (4096, 14336, 8, 2, K.ROUTE_TOPK_SOFTMAX), "qwen": (2048, 1408, 60, 4, K.ROUTE_SOFTMAX_TOPK)}
+SHAPES = {"mixtral": (4096, 14336, 8, 2, K.ROUTE_TOPK_SOFTMAX), "qwen": (2048, 1408, 60, 4, K.ROUTE_SOFTMAX_TOPK),
+          "qwen_shared": (2048, 5632, 1, 1, K.ROUTE_SOFTMAX_TOPK)}
 d, F, E, k, mode = SHAPES[os.environ.get("SHAPE", "mixtral")]
 g = torch.Generator(device="cuda").manual_seed(0)
 wr = (torch.randn((E, d), device="cuda", generator=g) / 64).bfloat16()
