@@ -471,7 +471,11 @@ def run_ours(args, rank: int, world: int) -> None:
                        "D2H pipelined on three streams (no L2 flush in this leg)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "qmoe_expert_ffn launch group (tcgen05 gate_up+SiLU*up, tcgen05 down)",
+                     "kernel": "qmoe_expert_ffn (" + {K.PATH_SWAP_PAIR: "swap-AB CTA-pair tcgen05 kernel",
+                                                       K.PATH_FUSED_PAIR: "CTA-pair tcgen05 kernel",
+                                                       K.PATH_FUSED_1CTA: "1-CTA tcgen05 kernel"}.get(
+                         K.expert_ffn_path(D, F, E // world, T * TOPK), "tcgen05 launch group")
+                     + ", gate_up + SiLU*up + down in one launch)",
                      "peak_source": f"{peak_src} bf16 dense, sustained (kernel timed inside a continuous loop)",
                      "frac_of_burst": achieved / peak_burst, "ms_per_launch": ffn_mean},
         "decode_step": {"tokens": args.decode_tokens, "ms": dec_ms,
