@@ -1,5 +1,5 @@
 """Small kernel workload for compute-sanitizer (memcheck / racecheck / synccheck): router, permute,
-every bf16 expert path (swap-AB, fused 1-CTA, fused CTA pair), combine, on tiny shapes."""
+every bf16 expert path (swap-AB, swap-AB CTA pair, fused 1-CTA, fused CTA pair), combine, on tiny shapes."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
