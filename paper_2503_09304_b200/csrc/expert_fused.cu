@@ -564,8 +564,11 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
   __shared__ int ring_tile[kRingF];
   __shared__ uint32_t tmem_base_smem;
   __shared__ TileMap map1, map2;
-  __shared__ float sp_xg[2][32][17], sp_xu[2][32][17];       // gate <-> up halves (warp pairs 0/2, 1/3)
-  __shared__ __align__(16) __nv_bfloat16 sp_out[32][128 + 8];  // one 32-token chunk of output rows
+  // gate <-> up halves of a 32-token chunk ([0] gate, [1] up; warp pairs 0/2, 1/3), float4 rows of
+  // 20 floats (conflict-free 16-byte accesses); one chunk of output rows, 160 bf16 per row so the
+  // two rows of a paired 32-bit store land 16 banks apart
+  __shared__ __align__(16) float sp_x[2][2][32][20];
+  __shared__ __align__(16) __nv_bfloat16 sp_out[32][160];
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -752,17 +755,37 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
           // the gate warp finishes tokens [0, 16) of the chunk, the up warp tokens [16, 32)
           const int q = ew & 1;
           const bool gate = ew < 2;
+          float4* xs = reinterpret_cast<float4*>(&sp_x[gate ? 0 : 1][q][lane][0]);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (gate) sp_xg[q][lane][j] = __uint_as_float(v[16 + j]);
-            else sp_xu[q][lane][j] = __uint_as_float(v[j]);
+          for (int i = 0; i < 4; ++i) {
+            float e4[4];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) e4[c4] = __uint_as_float(gate ? v[16 + 4 * i + c4] : v[4 * i + c4]);
+            xs[i] = make_float4(e4[0], e4[1], e4[2], e4[3]);
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
+          const float4* xr = reinterpret_cast<const float4*>(&sp_x[gate ? 1 : 0][q][lane][0]);
+          float h[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float gv = gate ? __uint_as_float(v[j]) : sp_xg[q][lane][j];
-            const float uv = gate ? sp_xu[q][lane][j] : __uint_as_float(v[16 + j]);
-            sp_out[(gate ? 0 : 16) + j][32 * q + lane] = __float2bfloat16_rn(gv / (1.f + __expf(-gv)) * uv);
+          for (int i = 0; i < 4; ++i) {
+            const float4 t4 = xr[i];
+            const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const int j = 4 * i + c4;
+              const float gv = gate ? __uint_as_float(v[j]) : tv[c4];
+              const float uv = gate ? tv[c4] : __uint_as_float(v[16 + j]);
+              h[j] = gv / (1.f + __expf(-gv)) * uv;
+            }
+          }
+          // lane pairs (2m, 2m+1) swap one value per token pair so each lane stores one 32-bit word:
+          // the even lane features (2m, 2m+1) of token j, the odd lane the same of token j+1
+          const int t0 = gate ? 0 : 16, fl = 32 * q + (lane & ~1);
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            const float recv = __shfl_xor_sync(0xffffffffu, (lane & 1) ? h[j] : h[j + 1], 1);
+            if (lane & 1) *reinterpret_cast<uint32_t*>(&sp_out[t0 + j + 1][fl]) = pack2(recv, h[j + 1]);
+            else *reinterpret_cast<uint32_t*>(&sp_out[t0 + j][fl]) = pack2(h[j], recv);
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
           // 32 token rows x 64 features (128 B) of act, 16-byte stores
@@ -775,8 +798,14 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
                   *reinterpret_cast<const uint4*>(&sp_out[r][8 * vq]);
           }
         } else {
+          const int fl = 32 * ew + (lane & ~1);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) sp_out[j][32 * ew + lane] = __float2bfloat16_rn(__uint_as_float(v[j]));
+          for (int j = 0; j < 32; j += 2) {
+            const float a0 = __uint_as_float(v[j]), a1 = __uint_as_float(v[j + 1]);
+            const float recv = __shfl_xor_sync(0xffffffffu, (lane & 1) ? a0 : a1, 1);
+            if (lane & 1) *reinterpret_cast<uint32_t*>(&sp_out[j + 1][fl]) = pack2(recv, a1);
+            else *reinterpret_cast<uint32_t*>(&sp_out[j][fl]) = pack2(a0, recv);
+          }
           asm volatile("bar.sync 1, 128;" ::: "memory");
           // 32 token rows x 128 output columns (256 B) scattered to the token slots
 #pragma unroll
