@@ -53,6 +53,8 @@ __global__ void __launch_bounds__(kCombWarps * 32)
 combine_bf16_kernel(const __nv_bfloat16* __restrict__ y, const float* __restrict__ w,
                     const __nv_bfloat16* __restrict__ residual, int ntok, int k, int d, int parts,
                     __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int gw = blockIdx.x * kCombWarps + warp_id();
   const int tok = gw / parts, part = gw - tok * parts;
   if (tok >= ntok) return;
@@ -185,12 +187,13 @@ extern "C" int qmoe_combine(int dtype, const void* y, const void* w, const void*
       parts = parts < 1 ? 1 : (parts > max_parts ? max_parts : parts);
       const dim3 g2((T * parts + kCombWarps - 1) / kCombWarps);
       if (k == 2)
-        combine_bf16_kernel<2><<<g2, block, 0, s>>>(yb, (const float*)w, rb, T, k, d, parts, ob);
-      else if (k == 4)
-        combine_bf16_kernel<4><<<g2, block, 0, s>>>(yb, (const float*)w, rb, T, k, d, parts, ob);
-      else
-        combine_bf16_kernel<0><<<g2, block, 0, s>>>(yb, (const float*)w, rb, T, k, d, parts, ob);
-      break;
+        return launch_pdl("qmoe_combine", combine_bf16_kernel<2>, g2, block, 0, s, yb, (const float*)w, rb, T, k, d,
+                          parts, ob);
+      if (k == 4)
+        return launch_pdl("qmoe_combine", combine_bf16_kernel<4>, g2, block, 0, s, yb, (const float*)w, rb, T, k, d,
+                          parts, ob);
+      return launch_pdl("qmoe_combine", combine_bf16_kernel<0>, g2, block, 0, s, yb, (const float*)w, rb, T, k, d,
+                        parts, ob);
     }
     default:
       set_error("qmoe_combine: unknown dtype %d", dtype);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -50,6 +51,47 @@ inline size_t dtype_bytes(int dtype) {
 }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- programmatic dependent launch (PDL) -----------------------------------------------
+// The hot-path kernels (router, permute, expert FFN, split-K reduce, combine) are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization: a kernel may be scheduled while its
+// predecessor in the stream is still running, and blocks in pdl_wait() -- its first statement,
+// before any global memory access -- until the predecessor grid has completed and its writes are
+// visible.  pdl_trigger() right after lets this kernel's own successor be scheduled as soon as all
+// of this grid's CTAs are resident, so a layer's 5-7 dependent launches do not pay a full
+// launch latency each.  Launched without the attribute both are no-ops.  QMOE_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("QMOE_PDL");
+    return v == nullptr || atoi(v) != 0;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline int launch_pdl(const char* what, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                      Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return QMOE_ERR_CUDA;
+  }
+  return QMOE_OK;
+}
 
 // ---- element conversion ---------------------------------------------------------------
 template <typename T> __device__ __forceinline__ float to_f32(T v);

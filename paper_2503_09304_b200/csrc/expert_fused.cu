@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(kThreadsF, 1)
 ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                  const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW2,
                  FusedParams p) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStagesF], empty_bar[kStagesF];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
@@ -296,6 +298,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsF, 1)
 ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                       const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW2,
                       FusedParams p) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int kBMp = 256;
   constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kBMp, kBN);
   extern __shared__ uint8_t smem_raw[];
@@ -557,6 +561,8 @@ struct alignas(64) SpMaps {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsF, 1)
 ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStagesSP], empty_bar[kStagesSP];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
@@ -891,10 +897,10 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
     attr_set = true;
   }
   if (pair)
-    ffn_fused_pair_kernel<<<(tc_num_sms() / 2) * 2, kThreadsF, kSmemP, s>>>(maps[0], maps[1], maps[2], maps[3], p);
-  else
-    ffn_fused_kernel<<<tc_num_sms(), kThreadsF, kSmemF, s>>>(maps[0], maps[1], maps[2], maps[3], p);
-  return check_launch("qmoe_expert_ffn(tcgen05 single launch)");
+    return launch_pdl("qmoe_expert_ffn(tcgen05 single launch, pair)", ffn_fused_pair_kernel,
+                      dim3((tc_num_sms() / 2) * 2), dim3(kThreadsF), kSmemP, s, maps[0], maps[1], maps[2], maps[3], p);
+  return launch_pdl("qmoe_expert_ffn(tcgen05 single launch)", ffn_fused_kernel, dim3(tc_num_sms()), dim3(kThreadsF),
+                    kSmemF, s, maps[0], maps[1], maps[2], maps[3], p);
 }
 
 // Batches past the swap-AB range (checked first) of coarse experts: the swap-AB CTA-pair kernel,
@@ -954,8 +960,8 @@ int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* 
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_swap_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSP));
     attr_set = true;
   }
-  ffn_swap_pair_kernel<<<(tc_num_sms() / 2) * 2, kThreadsF, kSmemSP, s>>>(maps, p);
-  return check_launch("qmoe_expert_ffn(tcgen05 swap-AB pair)");
+  return launch_pdl("qmoe_expert_ffn(tcgen05 swap-AB pair)", ffn_swap_pair_kernel, dim3((tc_num_sms() / 2) * 2),
+                    dim3(kThreadsF), kSmemSP, s, maps, p);
 }
 
 }  // namespace qmoe

@@ -80,6 +80,8 @@ template <int NT>
 __global__ void __launch_bounds__(kThreadsS, 1)
 ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                 const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW2, SwapParams p) {
+  pdl_wait();
+  pdl_trigger();
   using C = SwapCfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[C::kStages], empty_bar[C::kStages];
@@ -355,6 +357,8 @@ __global__ void __launch_bounds__(256) swap_reduce_kernel(const float* __restric
                                                           const int32_t* __restrict__ offsets, int e_begin,
                                                           const int32_t* __restrict__ stop,
                                                           __nv_bfloat16* __restrict__ y, void* const* peers) {
+  pdl_wait();
+  pdl_trigger();
   const int r0 = offsets[e_begin], r1 = offsets[*stop];
   const int per_row = N / 8;
   const long long total = (long long)(r1 - r0) * per_row;
@@ -381,8 +385,8 @@ int launch_swap(const CUtensorMap* maps, const SwapParams& p, cudaStream_t s) {
                                        SwapCfg<NT>::kSmem));
     attr_set = true;
   }
-  ffn_swap_kernel<NT><<<tc_num_sms(), kThreadsS, SwapCfg<NT>::kSmem, s>>>(maps[0], maps[1], maps[2], maps[3], p);
-  return check_launch("qmoe_expert_ffn(tcgen05 swap-AB)");
+  return launch_pdl("qmoe_expert_ffn(tcgen05 swap-AB)", ffn_swap_kernel<NT>, dim3(tc_num_sms()), dim3(kThreadsS),
+                    SwapCfg<NT>::kSmem, s, maps[0], maps[1], maps[2], maps[3], p);
 }
 
 // K splits of a down unit so each streams about 1 MB of weights (Mixtral: 128 x 14336 bf16 =
@@ -456,9 +460,9 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
   if (p.nsplit > 1) {
     const long long work = (long long)xp_rows * (d / 8);
     const int grid = (int)std::min<long long>((work + 255) / 256, 148 * 8);
-    swap_reduce_kernel<<<grid, 256, 0, s>>>(p.part, p.nsplit, xp_rows, d, perm, offsets, e_begin, &ws[0].stop,
-                                            (__nv_bfloat16*)y, y_peers);
-    return check_launch("qmoe_expert_ffn(swap-AB split-K reduce)");
+    return launch_pdl("qmoe_expert_ffn(swap-AB split-K reduce)", swap_reduce_kernel, dim3(grid), dim3(256), 0, s,
+                      (const float*)p.part, p.nsplit, xp_rows, d, perm, offsets, e_begin, (const int32_t*)&ws[0].stop,
+                      (__nv_bfloat16*)y, y_peers);
   }
   return QMOE_OK;
 }

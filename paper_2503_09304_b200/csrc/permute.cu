@@ -32,6 +32,8 @@ __device__ __forceinline__ int slot_expert(const int32_t* ids, const int32_t* cu
 __global__ void __launch_bounds__(256) perm_count_kernel(const int32_t* __restrict__ ids,
                                                          const int32_t* __restrict__ cursor, int S,
                                                          int k, int E, int32_t* __restrict__ hist) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int h[kMaxE];
   for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = 0;
   __syncthreads();
@@ -67,6 +69,8 @@ __global__ void __launch_bounds__(256) perm_gather_kernel(const int32_t* __restr
                                                           const int32_t* __restrict__ offsets, int E, int k,
                                                           int max_rows, const uint8_t* __restrict__ x,
                                                           uint8_t* __restrict__ xp, size_t row_bytes) {
+  pdl_wait();
+  pdl_trigger();
   const int R = offsets[E];
   const int lane = lane_id();
   for (int r = blockIdx.x * 8 + warp_id(); r < R && r < max_rows; r += gridDim.x * 8)
@@ -78,6 +82,8 @@ perm_scatter_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__
                     int E, int nblk, int32_t* __restrict__ hist, int32_t* __restrict__ perm,
                     int32_t* __restrict__ offsets, const uint8_t* __restrict__ x, uint8_t* __restrict__ xp,
                     size_t row_bytes) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int base[kMaxE];
   __shared__ int warp_cnt[kWarpsPer][kMaxE];
   __shared__ int pass_tot[kMaxE];
@@ -214,21 +220,22 @@ extern "C" int qmoe_permute(const int32_t* ids, const int32_t* cursor, int T, in
   int32_t* hist = reinterpret_cast<int32_t*>(workspace);
   int st;
   if (nblk > 1) {  // multi-chunk: per-chunk histograms first
-    perm_count_kernel<<<nblk, 256, 0, s>>>(ids, cursor, (int)S, k, E, hist);
-    if ((st = check_launch("qmoe_permute(count)"))) return st;
+    if ((st = launch_pdl("qmoe_permute(count)", perm_count_kernel, dim3(nblk), dim3(256), 0, s, ids, cursor, (int)S, k,
+                         E, hist)))
+      return st;
   }
   // one CTA: count + rank + scatter + gather fused; many CTAs: gather runs wide afterwards
   const bool inline_gather = S <= 32;  // decode-sized: one launch; otherwise gather wide
-  perm_scatter_kernel<<<nblk, kThreads, 0, s>>>(ids, cursor, (int)S, k, E, nblk, hist, perm_out, offsets_out,
-                                                (const uint8_t*)x, inline_gather ? (uint8_t*)xp : nullptr,
-                                                row_bytes);
-  if ((st = check_launch("qmoe_permute(scatter)"))) return st;
+  if ((st = launch_pdl("qmoe_permute(scatter)", perm_scatter_kernel, dim3(nblk), dim3(kThreads), 0, s, ids, cursor,
+                       (int)S, k, E, nblk, hist, perm_out, offsets_out, (const uint8_t*)x,
+                       inline_gather ? (uint8_t*)xp : nullptr, row_bytes)))
+    return st;
   if (xp != nullptr && !inline_gather) {
     const int rows = (int)S;
     const int grid = rows / 8 < 148 * 16 ? (rows + 7) / 8 : 148 * 16;
-    perm_gather_kernel<<<grid, 256, 0, s>>>(perm_out, offsets_out, E, k, rows, (const uint8_t*)x, (uint8_t*)xp,
-                                            row_bytes);
-    if ((st = check_launch("qmoe_permute(gather)"))) return st;
+    if ((st = launch_pdl("qmoe_permute(gather)", perm_gather_kernel, dim3(grid), dim3(256), 0, s, perm_out,
+                         offsets_out, E, k, rows, (const uint8_t*)x, (uint8_t*)xp, row_bytes)))
+      return st;
   }
   return QMOE_OK;
 }

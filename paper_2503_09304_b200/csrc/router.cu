@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(kWarps * 32)
 router_kernel(const T* __restrict__ x, const T* __restrict__ wr, int ntok, int d, int E, int k,
               int mode, int32_t* __restrict__ ids_out, typename AccOf<T>::type* __restrict__ w_out,
               typename AccOf<T>::type* __restrict__ logits_out, int rounds) {
+  pdl_wait();
+  pdl_trigger();
   using A = typename AccOf<T>::type;
   constexpr int kGroups = TPC / TPW;
   constexpr int kWpg = kWarps / kGroups;  // warps per token group
@@ -236,12 +238,10 @@ int launch_router(const void* x, const void* wr, int T_, int d, int E, int k, in
   const bool vec = (d % Vec<T>::N == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(wr) % 16 == 0);
   if (vec)
-    router_kernel<T, TPC, TPW, true, NW><<<grid, NW * 32, 0, s>>>(
-        (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits, rounds);
-  else
-    router_kernel<T, TPC, TPW, false, NW><<<grid, NW * 32, 0, s>>>(
-        (const T*)x, (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits, rounds);
-  return check_launch("qmoe_router");
+    return launch_pdl("qmoe_router", router_kernel<T, TPC, TPW, true, NW>, grid, dim3(NW * 32), 0, s, (const T*)x,
+                      (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits, rounds);
+  return launch_pdl("qmoe_router", router_kernel<T, TPC, TPW, false, NW>, grid, dim3(NW * 32), 0, s, (const T*)x,
+                    (const T*)wr, T_, d, E, k, mode, ids, (A*)w, (A*)logits, rounds);
 }
 
 // ---- bf16, many tokens: the logits as a skinny GEMM on the tensor cores ------------------------
@@ -283,6 +283,8 @@ __global__ void __launch_bounds__(256)
 router_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr, int ntok, int d, int E,
                   int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
                   float* __restrict__ logits_out) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int kTok = 16 * MT;
   extern __shared__ __align__(16) __nv_bfloat16 sbuf[];  // kMmaStages x (X chunk, W chunk); reused below
   const int warp = warp_id(), lane = lane_id();
@@ -387,9 +389,9 @@ int launch_router_mma_np(const void* x, const void* wr, int T_, int d, int E, in
     QMOE_CUDA_TRY(cudaFuncSetAttribute(router_mma_kernel<NP, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
-  router_mma_kernel<NP, MT><<<(T_ + kTok - 1) / kTok, 256, smem, s>>>(
-      (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w, (float*)logits);
-  return check_launch("qmoe_router(mma)");
+  return launch_pdl("qmoe_router(mma)", router_mma_kernel<NP, MT>, dim3((T_ + kTok - 1) / kTok), dim3(256), smem, s,
+                    (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,
+                    (float*)logits);
 }
 
 int launch_router_mma(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
