@@ -571,10 +571,10 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
   __shared__ uint32_t tmem_base_smem;
   __shared__ TileMap map1, map2;
   // gate <-> up halves of a 32-token chunk ([0] gate, [1] up; warp pairs 0/2, 1/3), float4 rows of
-  // 20 floats (conflict-free 16-byte accesses); one chunk of output rows, 160 bf16 per row so the
-  // two rows of a paired 32-bit store land 16 banks apart
+  // 20 floats (conflict-free 16-byte accesses); per-warp staging tiles of 32 token rows x 32
+  // columns (64-byte rows: the two rows of a paired 32-bit store land 16 banks apart)
   __shared__ __align__(16) float sp_x[2][2][32][20];
-  __shared__ __align__(16) __nv_bfloat16 sp_out[32][160];
+  __shared__ __align__(16) __nv_bfloat16 sp_w[4][32][32];
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -750,7 +750,7 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
       ptx::mbar_wait_cluster(&tfull_bar[acc], aphase);
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * kTokSP;
-      const int et = threadIdx.x - kEpiF * 32;  // 0..127 over the epilogue warps
+      __nv_bfloat16 (*stg)[32] = sp_w[ew];  // this warp's staging tile (token rows x 32 columns)
 #pragma unroll 1
       for (int c = 0; c < rows; c += 32) {
         uint32_t v[32];
@@ -758,7 +758,8 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
         ptx::tmem_ld_wait();
         if (up) {
           // warp pair q = ew & 1 holds gate (ew = q) and up (ew = q + 2) of the same 32 features:
-          // the gate warp finishes tokens [0, 16) of the chunk, the up warp tokens [16, 32)
+          // the gate warp finishes tokens [0, 16) of the chunk, the up warp tokens [16, 32); the
+          // halves cross through shared memory under a barrier of the pair only
           const int q = ew & 1;
           const bool gate = ew < 2;
           float4* xs = reinterpret_cast<float4*>(&sp_x[gate ? 0 : 1][q][lane][0]);
@@ -769,7 +770,7 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
             for (int c4 = 0; c4 < 4; ++c4) e4[c4] = __uint_as_float(gate ? v[16 + 4 * i + c4] : v[4 * i + c4]);
             xs[i] = make_float4(e4[0], e4[1], e4[2], e4[3]);
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
           const float4* xr = reinterpret_cast<const float4*>(&sp_x[gate ? 1 : 0][q][lane][0]);
           float h[16];
 #pragma unroll
@@ -784,46 +785,46 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
               h[j] = gv / (1.f + __expf(-gv)) * uv;
             }
           }
-          // lane pairs (2m, 2m+1) swap one value per token pair so each lane stores one 32-bit word:
-          // the even lane features (2m, 2m+1) of token j, the odd lane the same of token j+1
-          const int t0 = gate ? 0 : 16, fl = 32 * q + (lane & ~1);
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // sp_x is rewritten by the next chunk
+          // transpose through the warp's staging tile: lane pairs (2m, 2m+1) swap one value per
+          // token pair so each lane stores one 32-bit word (rows j, j+1 land 16 banks apart)
 #pragma unroll
           for (int j = 0; j < 16; j += 2) {
             const float recv = __shfl_xor_sync(0xffffffffu, (lane & 1) ? h[j] : h[j + 1], 1);
-            if (lane & 1) *reinterpret_cast<uint32_t*>(&sp_out[t0 + j + 1][fl]) = pack2(recv, h[j + 1]);
-            else *reinterpret_cast<uint32_t*>(&sp_out[t0 + j][fl]) = pack2(h[j], recv);
+            *reinterpret_cast<uint32_t*>(&stg[j + (lane & 1)][lane & ~1]) =
+                (lane & 1) ? pack2(recv, h[j + 1]) : pack2(h[j], recv);
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          // 32 token rows x 64 features (128 B) of act, 16-byte stores
+          __syncwarp();
+          // 16 token rows x 32 features (64 B) of act, 16-byte stores
+          const int t0 = c + (gate ? 0 : 16);
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
-            const int idx = et + 128 * i, r = idx >> 3, vq = idx & 7;
-            const int f = n0 + (int)rank * 64 + 8 * vq;
-            if (c + r < rows && f < p.F)
-              *reinterpret_cast<uint4*>(p.act + (size_t)(m0 + c + r) * p.F + f) =
-                  *reinterpret_cast<const uint4*>(&sp_out[r][8 * vq]);
+            const int idx = lane + 32 * i, r = idx >> 2, vq = idx & 3;
+            if (t0 + r < rows)
+              *reinterpret_cast<uint4*>(p.act + (size_t)(m0 + t0 + r) * p.F + n0 + (int)rank * 64 + 32 * q + 8 * vq) =
+                  *reinterpret_cast<const uint4*>(&stg[r][8 * vq]);
           }
         } else {
-          const int fl = 32 * ew + (lane & ~1);
+          const int pr = c + lane < rows ? p.perm[m0 + c + lane] : 0;  // slot of token c + lane
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             const float a0 = __uint_as_float(v[j]), a1 = __uint_as_float(v[j + 1]);
             const float recv = __shfl_xor_sync(0xffffffffu, (lane & 1) ? a0 : a1, 1);
-            if (lane & 1) *reinterpret_cast<uint32_t*>(&sp_out[j + 1][fl]) = pack2(recv, a1);
-            else *reinterpret_cast<uint32_t*>(&sp_out[j][fl]) = pack2(a0, recv);
+            *reinterpret_cast<uint32_t*>(&stg[j + (lane & 1)][lane & ~1]) = (lane & 1) ? pack2(recv, a1) : pack2(a0, recv);
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          // 32 token rows x 128 output columns (256 B) scattered to the token slots
+          __syncwarp();
+          // 32 token rows x 32 output columns (64 B) scattered to the token slots, 16-byte stores
+          const int col = n0 + (int)rank * 128 + 32 * ew;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int idx = et + 128 * i, r = idx >> 4, vq = idx & 15;
-            const int col = n0 + (int)rank * 128 + 8 * vq;
-            if (c + r < rows && col < p.d)
-              *reinterpret_cast<uint4*>(out_row(p.y, p.peers, p.perm[m0 + c + r], p.d) + col) =
-                  *reinterpret_cast<const uint4*>(&sp_out[r][8 * vq]);
+            const int idx = lane + 32 * i, r = idx >> 2, vq = idx & 3;
+            const int slot = __shfl_sync(0xffffffffu, pr, r);
+            if (c + r < rows)
+              *reinterpret_cast<uint4*>(out_row(p.y, p.peers, slot, p.d) + col + 8 * vq) =
+                  *reinterpret_cast<const uint4*>(&stg[r][8 * vq]);
           }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // sp_out / exchange reused by the next chunk
+        __syncwarp();  // the staging tile is rewritten by the next chunk
       }
       ptx::tc_fence_before();
       __syncwarp();
