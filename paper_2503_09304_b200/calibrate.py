@@ -1,0 +1,159 @@
+"""Virtual cost-model calibration.
+
+`calibration_iteration_ms` and `calibrate` restate the reference's closed-loop rescaling
+(reference cli.py:198-255): run one canonical decode iteration (32 members, 32 layers, 180-token
+contexts, after a prefill that fills the caches) through the engine on a virtual clock, then scale
+every CostModel parameter by target / measured.  The virtual charges depend only on the routing and
+the token counts, so on the reference's own toy model (f64 kernels) this engine returns the
+reference's number exactly (tests/test_calibrate_gpu.py).
+
+`b200_cost_model` is what the reference cannot do: it runs the same canonical iteration of a real
+model (e.g. the Mixtral-shaped decoder) on a wall clock on the B200 and returns the CostModel
+scaled so that the virtual iteration of that model lasts exactly what the B200 measured, so
+virtual-clock studies (decision logs, SLO sweeps) are charged at B200 speed.
+"""
+from __future__ import annotations
+
+import functools
+import statistics
+from dataclasses import replace
+from typing import Optional
+
+import numpy as np
+import torch
+
+from .core import EOS_TOKEN, Phase, Priority, SchedulerDirective, batch_form, sequence_new
+from .engine import Completed, CostModel, InferenceEngine, VirtualClock, WallClock
+from .kvcache import UnifiedDynamicCache
+from .model import ModelConfig, MoEModel
+
+# reference cli.py:41-43
+CANONICAL_CONTEXT = 180
+CALIBRATION_BATCH = 32
+CALIBRATION_LAYERS = 32
+
+
+def _canonical_iteration_ms(model, clock, cost_model: CostModel, seed: int, vocab_size: int,
+                            repeats: int = 1) -> list[float]:
+    """Prefill CALIBRATION_BATCH sequences of CANONICAL_CONTEXT random tokens, then time decode
+    iterations of the whole batch (reference cli.py:209-236).  Returns one duration per repeat
+    (the reference takes one)."""
+    cache = UnifiedDynamicCache(model.config.num_layers, model.kv_row_shape(), model.kv_dtype, model.device,
+                                model.kv_entry_bytes(), **getattr(model, "kv_page_kwargs", {}))
+    engine = InferenceEngine(model, cache, clock, cost_model, CALIBRATION_BATCH)
+    rng = np.random.default_rng(seed + 1)
+    seqs = []
+    for i in range(CALIBRATION_BATCH):
+        prompt = [int(t) for t in rng.integers(1, vocab_size, size=CANONICAL_CONTEXT)]
+        seq = sequence_new(prompt, priority=Priority.BEST_EFFORT, max_new_tokens=max(4, 2 + repeats), arrival=0.0,
+                           seq_id=i)
+        seq.cache_handle = i
+        cache.register(i)
+        seqs.append(seq)
+
+    def cont(report):
+        return SchedulerDirective.CONTINUE
+
+    outcome = engine.execute(batch_form(seqs, Phase.PREFILL, CALIBRATION_BATCH, engine.next_batch_id()), seqs, cont)
+    assert isinstance(outcome, Completed)
+    for seq in seqs:
+        seq.generated.append(outcome.tokens[seq.id])
+        seq.advance_phase(Phase.DECODE)
+    out = []
+    for r in range(repeats):
+        # the reference's single timed iteration decodes every member; later repeats drop members
+        # that emitted EOS (a random-init model may)
+        live = seqs if r == 0 else [q for q in seqs if q.generated[-1] != EOS_TOKEN]
+        if not live:
+            break
+        decode = batch_form(live, Phase.DECODE, CALIBRATION_BATCH, engine.next_batch_id())
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+        start = clock.now
+        outcome = engine.execute(decode, live, cont)
+        assert isinstance(outcome, Completed)
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+        out.append(clock.now - start)
+        for seq in live:
+            seq.generated.append(outcome.tokens[seq.id])
+    return out
+
+
+@functools.lru_cache(maxsize=32)
+def calibration_iteration_ms(model_config: ModelConfig, cost_model: CostModel) -> float:
+    """Virtual ms of one canonical decode iteration of the reference's toy model (f64) with
+    `cost_model` (reference cli.py:198-236; memoized like the reference, both configs frozen)."""
+    config = replace(model_config, num_layers=CALIBRATION_LAYERS)
+    model = MoEModel(config)
+    return _canonical_iteration_ms(model, VirtualClock(), cost_model, config.seed, config.vocab_size)[0]
+
+
+def calibrate(model_config: ModelConfig, cost_model: CostModel, target_lo: float, target_hi: float) -> CostModel:
+    """Rescale `cost_model` so the canonical decode iteration lands in [target_lo, target_hi]
+    (reference cli.py:238-255): every parameter times midpoint / measured, then re-measured as a
+    closed-loop check.  ValueError on an infeasible window or a landing outside it."""
+    if target_hi <= 0 or target_lo < 0 or target_lo > target_hi:
+        raise ValueError(f"infeasible target range [{target_lo}, {target_hi}]")
+    measured = calibration_iteration_ms(model_config, cost_model)
+    if measured <= 0:
+        raise ValueError("cost model charges nothing; cannot calibrate")
+    mid = 0.5 * (target_lo + target_hi)
+    scaled = cost_model.scaled(mid / measured)
+    check = calibration_iteration_ms(model_config, scaled)
+    if not (target_lo <= check <= target_hi):
+        raise ValueError(f"calibration landed at {check:.3f} ms, outside [{target_lo}, {target_hi}]")
+    return scaled
+
+
+def b200_cost_model(model, cost_model: CostModel = CostModel(), repeats: int = 5,
+                    seed: Optional[int] = None) -> tuple[CostModel, dict]:
+    """CostModel whose virtual canonical decode iteration of `model` equals the B200's wall time.
+
+    The canonical iteration (CALIBRATION_BATCH members, CANONICAL_CONTEXT-token contexts, all of
+    `model`'s layers) runs `repeats` times on a WallClock (median taken; the first prefill warms
+    the kernels up) and once on a VirtualClock with `cost_model`; every parameter is scaled by
+    wall / virtual, the reference's one-factor rescaling (cli.py:250-251) with the B200 as the
+    target.  Returns (scaled model, {"wall_ms", "virtual_ms", "scale"})."""
+    cfg = model.config
+    seed = getattr(cfg, "seed", 0) if seed is None else seed
+    wall = _canonical_iteration_ms(model, WallClock(), cost_model, seed, cfg.vocab_size, repeats=repeats)
+    virt = _canonical_iteration_ms(model, VirtualClock(), cost_model, seed, cfg.vocab_size)[0]
+    if virt <= 0:
+        raise ValueError("cost model charges nothing; cannot calibrate")
+    wall_ms = statistics.median(wall)
+    scale = wall_ms / virt
+    return cost_model.scaled(scale), {"wall_ms": wall_ms, "wall_ms_all": wall, "virtual_ms": virt, "scale": scale}
+
+
+def main(argv=None) -> int:
+    """python -m paper_2503_09304_b200.calibrate [--model mixtral|qwen] [--repeats N] [--out F]:
+    the B200-calibrated CostModel of a random-init bf16 decoder (JSON)."""
+    import argparse
+    import json
+
+    from .mixtral import MIXTRAL_8X7B, QWEN15_MOE_A27B, DecoderMoEModel
+
+    ap = argparse.ArgumentParser(description=main.__doc__)
+    ap.add_argument("--model", choices=("mixtral", "qwen"), default="mixtral")
+    ap.add_argument("--repeats", type=int, default=5)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args(argv)
+    model = DecoderMoEModel(QWEN15_MOE_A27B if args.model == "qwen" else MIXTRAL_8X7B)
+    scaled, info = b200_cost_model(model, repeats=args.repeats)
+    rec = {"model": model.config.name, "canonical_iteration": {"members": CALIBRATION_BATCH,
+                                                                "context_tokens": CANONICAL_CONTEXT,
+                                                                "layers": model.config.num_layers},
+           "wall_ms": info["wall_ms"], "wall_ms_all": info["wall_ms_all"],
+           "virtual_ms_default_cost_model": info["virtual_ms"], "scale": info["scale"],
+           "cost_model": scaled.__dict__}
+    text = json.dumps(rec, indent=1)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write(text + "\n")
+    print(text)
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())
