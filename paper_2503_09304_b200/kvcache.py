@@ -103,6 +103,37 @@ class UnifiedDynamicCache:
         self._ledger += n * self.entry_bytes
         return self.slots(handle, start, n) if want_slots else []
 
+    def counts_at(self, handles, layer: int) -> list[int]:
+        """count(h, layer) for many handles (KeyError for an unknown one)."""
+        counts = self._counts
+        return [counts[h][layer] for h in handles]
+
+    def reserve_batch(self, handles, layer: int, ns, want_slots: bool = True) -> list[int]:
+        """reserve() for every member of a batch at one layer, one call per layer: same counts,
+        pages, ledger and slots (concatenated in member order).  When the batch would not fit,
+        or a handle is unknown, it falls back to member-by-member reserve() so the error is
+        raised at the same member with the same partial accounting."""
+        total = sum(ns)
+        pages_d, counts_d = self._pages, self._counts
+        if self._ledger + total * self.entry_bytes > self.capacity_bytes or any(h not in pages_d for h in handles):
+            out: list[int] = []
+            for h, n in zip(handles, ns):
+                out += self.reserve(h, layer, n, want_slots)
+            return out
+        ps = self.page_size
+        out = []
+        for h, n in zip(handles, ns):
+            cnt = counts_d[h]
+            start = cnt[layer]
+            pages = pages_d[h]
+            if len(pages) * ps < start + n:
+                self._ensure_pages(h, start + n)
+            cnt[layer] = start + n
+            if want_slots:
+                out += [pages[p // ps] * ps + p % ps for p in range(start, start + n)]
+        self._ledger += total * self.entry_bytes
+        return out
+
     def append_many(self, handle: int, layer: int, rows: torch.Tensor) -> None:
         slots = self.reserve(handle, layer, rows.shape[0])
         K.kv_append(self._pools[layer], torch.tensor(slots, dtype=torch.int32, device=self.device),

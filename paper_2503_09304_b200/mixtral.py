@@ -106,6 +106,7 @@ class DecoderMoEModel:
         self._cos, self._sin = emb.cos(), emb.sin()
         self._stop = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._meta, self._meta_key = None, None
+        self._expect = None  # (handles, members, expected cached entries) of the current pass
         self._shared_T, self._shared_off, self._shared_ident = -1, None, None
 
     # ------------------------------------------------------------------ cache geometry
@@ -138,15 +139,24 @@ class DecoderMoEModel:
         qkv = x @ L.w_qkv.T
         # Per-iteration metadata (positions, slot mapping, block table, lengths) is identical in
         # every layer of a decode/prefill pass, so it is built once and reused across layers.
-        key = tuple((m.seq.cache_handle, cache.count(m.seq.cache_handle, layer), m.n) for m in members)
+        handles = [m.seq.cache_handle for m in members]
+        ns = [m.n for m in members]
+        haves = cache.counts_at(handles, layer)
+        key = tuple(zip(handles, haves, ns))
         meta = self._meta if self._meta_key == key else None
         decode = members[0].seq.phase is Phase.DECODE
-        slots = []
-        for m, (handle, have, n) in zip(members, key):
-            seq = m.seq
-            if (seq.phase is Phase.DECODE) != decode or have != (seq.tokens_fed() if decode else 0):
-                raise StateCorruptionError(f"sequence {seq.id} layer {layer}: {have} cached entries")
-            slots += cache.reserve(handle, layer, n, want_slots=meta is None)
+        # every member must hold exactly its fed tokens at this layer: the expectation is built
+        # once per pass (all layers expect the same counts) and compared as one list per layer
+        exp = self._expect
+        if exp is None or exp[0] != handles or exp[1] is not members:
+            for m in members:
+                if (m.seq.phase is Phase.DECODE) != decode:
+                    raise StateCorruptionError(f"sequence {m.seq.id}: mixed phases in one batch")
+            exp = self._expect = (handles, members, [m.seq.tokens_fed() for m in members] if decode else [0] * len(members))
+        if haves != exp[2]:
+            bad = next(i for i, (a, b) in enumerate(zip(haves, exp[2])) if a != b)
+            raise StateCorruptionError(f"sequence {members[bad].seq.id} layer {layer}: {haves[bad]} cached entries")
+        slots = cache.reserve_batch(handles, layer, ns, want_slots=meta is None)
         if meta is None:
             pos = [p for (_, have, n) in key for p in range(have, have + n)]
             meta = {"pos": torch.tensor(pos, dtype=torch.long, device=self.device),

@@ -23,7 +23,11 @@ for dp in (False, True):
     for s in seqs:
         s.generated.append(out.tokens[s.id]); s.advance_phase(Phase.DECODE)
     ts, gs = [], []
+    import os, cProfile, pstats, io
+    prof = cProfile.Profile() if os.environ.get("PROF") and dp else None
     for it in range(12):
+        if prof is not None and it == 2:
+            prof.enable()
         torch.cuda.synchronize(); t = time.perf_counter()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -32,5 +36,10 @@ for dp in (False, True):
         ts.append((time.perf_counter() - t) * 1e3); gs.append(a.elapsed_time(b))
         for s in seqs:
             s.generated.append(out.tokens[s.id])
+    if prof is not None:
+        prof.disable()
+        buf = io.StringIO()
+        pstats.Stats(prof, stream=buf).sort_stats("tottime").print_stats(30)
+        print(buf.getvalue()[:7000])
     print(f"{cfg.name} device_preempt={dp}: decode iteration ms {sorted(ts)[len(ts)//2]:.2f} "
           f"(GPU span {sorted(gs)[len(gs)//2]:.2f})", flush=True)
