@@ -138,3 +138,43 @@ def test_paged_cache_ledger_pages_and_capacity():
     c.register(7)
     c.reserve(7, 0, 4)
     assert c._n_pages == before
+
+
+def test_paged_cache_reserve_batch_equals_member_reserves():
+    """reserve_batch (one call per layer, the decoder's attention stage) leaves the same counts,
+    pages, ledger and slots as member-by-member reserve; over capacity it raises at the same
+    member with the same partial accounting."""
+    def make():
+        c = UnifiedDynamicCache(3, (1,), torch.float32, torch.device("cpu"), entry_bytes=64, capacity_bytes=64 * 300,
+                                page_size=4, initial_pages=2)
+        for h in range(5):
+            c.register(h)
+        return c
+
+    a, b = make(), make()
+    rng = np.random.default_rng(3)
+    for _ in range(6):
+        handles = [int(h) for h in rng.permutation(5)[:4]]
+        ns = [int(n) for n in rng.integers(0, 7, size=4)]
+        for layer in range(3):
+            sa = []
+            for h, n in zip(handles, ns):
+                sa += a.reserve(h, layer, n)
+            sb = b.reserve_batch(handles, layer, ns)
+            assert sa == sb
+            assert a.counts_at(handles, layer) == b.counts_at(handles, layer)
+    assert a._pages == b._pages and a._counts == b._counts and a.usage_bytes() == b.usage_bytes()
+    assert b.reserve_batch([0, 1], 0, [1, 1], want_slots=False) == []
+    a.reserve(0, 0, 1), a.reserve(1, 0, 1)
+    # over capacity: the first members still reserve, the failing one raises, like reserve()
+    left = (a.capacity_bytes - a.usage_bytes()) // 64
+    for c in (a, b):
+        with pytest.raises(CacheCapacityError):
+            if c is a:
+                a.reserve(2, 1, left - 1)
+                a.reserve(3, 1, 5)
+            else:
+                b.reserve_batch([2, 3], 1, [left - 1, 5])
+    assert a._counts == b._counts and a.usage_bytes() == b.usage_bytes()
+    with pytest.raises(StateCorruptionError):
+        b.reserve_batch([0, 99], 0, [1, 1])
