@@ -1,8 +1,9 @@
 """Every bf16 expert-FFN code path, forced through the QMOE_SWAP_AB / QMOE_SWAP_PAIR / QMOE_CTA_PAIR switches (read
 once per process, so each configuration runs in its own interpreter), against the torch fp32
 restatement of HF MixtralExperts on the same bf16 inputs: swap-AB with 32/64/128-row token tiles,
-the 1-CTA 128-row tcgen05 kernel and the CTA-pair 256-row kernel, plus a preempted launch and its
-resume on each path (bit-identical to the uninterrupted launch)."""
+the swap-AB CTA pair (256 weight rows x token tiles of <= 256 rows), the 1-CTA 128-row tcgen05
+kernel and the CTA-pair 256-row kernel, plus a preempted launch and its resume on each path
+(bit-identical to the uninterrupted launch)."""
 
 import json
 import os
