@@ -176,3 +176,17 @@ def test_preempt_flag_raised_mid_launch(cuda, env):
     for r in res:
         assert r["stop"] >= 2, r
         assert r["prefix_ok"] and r["resume_ok"], r
+
+
+def test_all_single_launch_kernels_agree_bit_for_bit(cuda):
+    """The tcgen05 kernels differ in tile orientation (weights or tokens on the MMA's M side), CTA
+    pairing and tile shape, but accumulate every output over K in the same 64-wide blocks and round
+    act and Y identically, so the swap-AB, swap-AB CTA-pair, 1-CTA and CTA-pair kernels return the
+    same bits; the kernel-path heuristics therefore never change numerics (only the K-split decode
+    and two-launch split-K paths, with their fp32 partials, round differently)."""
+    shapes = [s for s in SHAPES if s[0] * s[4] > 512] + [(3000, 1024, 1408, 8, 2)]
+    runs = [_run(env, shapes) for env in ({"QMOE_SWAP_AB": "1"}, {"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "1"},
+                                          {"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "0", "QMOE_CTA_PAIR": "0"},
+                                          {"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "0", "QMOE_CTA_PAIR": "1"})]
+    for k in range(len(shapes)):
+        assert len({r[k]["sha"] for r in runs}) == 1, [r[k] for r in runs]
