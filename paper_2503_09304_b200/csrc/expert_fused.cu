@@ -908,9 +908,9 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
 // whose token tiles pad to 16 rows instead of 256.  Same-box eager A/B on B200 (tools/ffn_ab.py,
 // FFN alone, L2 flushed): Mixtral 768/1k/2k tokens 0.54/0.72/1.18 ms vs 0.58/0.80/1.25 on the
 // 256-row pair tiles, tied (+-2%) at 4k-16k.  Fine-grained experts (Qwen, 60 experts) lose 3-10%
-// at 1.5k-16k tokens except at 2k (+6%), and a single expert (Qwen's shared expert) loses 17-25%
-// (ncu: tensor pipe 58% vs 72% active with neither operand loads nor the epilogue on the critical
-// path -- open), so the path is used for 4..16 experts.  QMOE_SWAP_PAIR=0/1 forces it off/on (when
+// at 1.5k-16k tokens except at 2k (+6%), and a single expert (Qwen's shared expert) loses 5-9%
+// (the transposing epilogue, DESIGN 2.3b), so the path is used for 4..16 experts, and for more
+// experts only where the token-row tiles would pad by > 30%.  QMOE_SWAP_PAIR=0/1 forces it off/on (when
 // the shape allows it: d % 256 == 0, F % 128 == 0).
 bool use_swap_pair(int xp_rows, int n_experts, int d, int F) {
   static int forced = [] {
@@ -919,8 +919,14 @@ bool use_swap_pair(int xp_rows, int n_experts, int d, int F) {
   }();
   if (d % 256 != 0 || F % 128 != 0 || n_experts < 1 || n_experts > kFfnMaxExperts) return false;
   if (forced >= 0) return forced == 1;
-  (void)xp_rows;
-  return n_experts >= 4 && n_experts <= 16;
+  if (n_experts >= 4 && n_experts <= 16) return true;
+  if (n_experts <= 16) return false;
+  // fine-grained experts: only where the 128-row token tiles would waste > 30% of the tensor
+  // work on padding (mean rows per expert just above a multiple of 128: Qwen 2k tokens, ~137
+  // rows, 0.22 vs 0.23 ms); elsewhere the token-row tiles are 3-10% faster (epilogue, §2.3b)
+  const double rows = (double)xp_rows / n_experts;
+  const double padded = 128.0 * (double)(long long)((rows + 127.0) / 128.0);
+  return rows > 128.0 && rows / padded < 0.7;
 }
 
 int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
