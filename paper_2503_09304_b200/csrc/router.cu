@@ -278,7 +278,11 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-template <int NP, int MT>  // NP n-tile pairs (experts padded to 16 * NP); MT 16-token tiles per CTA
+// NP n-tile pairs (experts padded to 16 * NP); MT 16-token tiles per CTA; KC K-chunk width (128 or
+// 256: a 256-wide chunk halves the chunk iterations -- each with two barriers -- and warp w then
+// takes k16 steps w and w + 8 of it, the same per-warp step sequence as two 128-wide chunks, so
+// the logits are bit-identical)
+template <int NP, int MT, int KC = kMmaK>
 __global__ void __launch_bounds__(256)
 router_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr, int ntok, int d, int E,
                   int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
@@ -289,23 +293,25 @@ router_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __re
   extern __shared__ __align__(16) __nv_bfloat16 sbuf[];  // kMmaStages x (X chunk, W chunk); reused below
   const int warp = warp_id(), lane = lane_id();
   const int tok0 = blockIdx.x * kTok;
-  const int nk = d / kMmaK;
+  constexpr int kLdC = KC + 8;     // bf16 per padded smem row
+  constexpr int kPieces = KC / 8;  // 16-byte pieces per row
+  const int nk = d / KC;
   constexpr int wrows = 16 * NP;  // W rows staged
-  constexpr int stage_elems = (kTok + wrows) * kLd;
+  constexpr int stage_elems = (kTok + wrows) * kLdC;
   auto load = [&](int kc) {
     if (kc < nk) {
       __nv_bfloat16* sx = sbuf + (kc % kMmaStages) * stage_elems;
-      __nv_bfloat16* sw = sx + kTok * kLd;
-      const int k0 = kc * kMmaK;
-      // (kTok + wrows) rows x 16 pieces of 16 B over 256 threads
-      for (int piece = threadIdx.x; piece < (kTok + wrows) * 16; piece += 256) {
-        const int r = piece >> 4, c = (piece & 15) * 8;
+      __nv_bfloat16* sw = sx + kTok * kLdC;
+      const int k0 = kc * KC;
+      // (kTok + wrows) rows x kPieces pieces of 16 B over 256 threads
+      for (int piece = threadIdx.x; piece < (kTok + wrows) * kPieces; piece += 256) {
+        const int r = piece / kPieces, c = (piece % kPieces) * 8;
         if (r < kTok) {
           const int t = tok0 + r;
-          cp_async16(sx + r * kLd + c, x + (size_t)min(t, ntok - 1) * d + k0 + c, t < ntok);
+          cp_async16(sx + r * kLdC + c, x + (size_t)min(t, ntok - 1) * d + k0 + c, t < ntok);
         } else {
           const int e = r - kTok;
-          cp_async16(sw + e * kLd + c, wr + (size_t)min(e, E - 1) * d + k0 + c, e < E);
+          cp_async16(sw + e * kLdC + c, wr + (size_t)min(e, E - 1) * d + k0 + c, e < E);
         }
       }
     }
@@ -323,20 +329,25 @@ router_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __re
     asm volatile("cp.async.wait_group %0;" ::"n"(kMmaStages - 1) : "memory");  // chunk kc landed
     __syncthreads();
     const __nv_bfloat16* sx = sbuf + (kc % kMmaStages) * stage_elems;
-    const __nv_bfloat16* sw = sx + kTok * kLd;
-    const int ks = warp;  // this warp's k16 step of the chunk
-    uint32_t a[MT][4];
+    const __nv_bfloat16* sw = sx + kTok * kLdC;
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-      ldsm_x4(sx + (16 * mt + (lane & 15)) * kLd + ks * 16 + (lane >> 4) * 8, a[mt][0], a[mt][1], a[mt][2], a[mt][3]);
+    for (int sub = 0; sub < KC / 128; ++sub) {
+      const int ks = warp + 8 * sub;  // this warp's k16 step(s) of the chunk
+      uint32_t a[MT][4];
 #pragma unroll
-    for (int np = 0; np < NP; ++np) {
-      uint32_t b0, b1, b2, b3;  // one B fragment load feeds every token tile
-      ldsm_x4(sw + (16 * np + (lane >> 4) * 8 + (lane & 7)) * kLd + ks * 16 + ((lane >> 3) & 1) * 8, b0, b1, b2, b3);
+      for (int mt = 0; mt < MT; ++mt)
+        ldsm_x4(sx + (16 * mt + (lane & 15)) * kLdC + ks * 16 + (lane >> 4) * 8, a[mt][0], a[mt][1], a[mt][2],
+                a[mt][3]);
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        mma_bf16_16816(acc[mt][2 * np], a[mt][0], a[mt][1], a[mt][2], a[mt][3], b0, b1);
-        mma_bf16_16816(acc[mt][2 * np + 1], a[mt][0], a[mt][1], a[mt][2], a[mt][3], b2, b3);
+      for (int np = 0; np < NP; ++np) {
+        uint32_t b0, b1, b2, b3;  // one B fragment load feeds every token tile
+        ldsm_x4(sw + (16 * np + (lane >> 4) * 8 + (lane & 7)) * kLdC + ks * 16 + ((lane >> 3) & 1) * 8, b0, b1, b2,
+                b3);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          mma_bf16_16816(acc[mt][2 * np], a[mt][0], a[mt][1], a[mt][2], a[mt][3], b0, b1);
+          mma_bf16_16816(acc[mt][2 * np + 1], a[mt][0], a[mt][1], a[mt][2], a[mt][3], b2, b3);
+        }
       }
     }
     __syncthreads();  // stage kc % kMmaStages is refilled by the next iteration's load
@@ -379,17 +390,18 @@ router_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __re
   }
 }
 
-template <int NP, int MT>
+template <int NP, int MT, int KC = kMmaK>
 int launch_router_mma_np(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
                          void* logits, cudaStream_t s) {
   constexpr int kTok = 16 * MT;
   static bool attr_set = false;
-  const int smem = std::max(kMmaStages * (kTok + 16 * NP) * kLd * 2, (8 + 2) * kTok * kMaxE * 4);
+  const int smem = std::max(kMmaStages * (kTok + 16 * NP) * (KC + 8) * 2, (8 + 2) * kTok * kMaxE * 4);
   if (!attr_set) {
-    QMOE_CUDA_TRY(cudaFuncSetAttribute(router_mma_kernel<NP, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(router_mma_kernel<NP, MT, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem));
     attr_set = true;
   }
-  return launch_pdl("qmoe_router(mma)", router_mma_kernel<NP, MT>, dim3((T_ + kTok - 1) / kTok), dim3(256), smem, s,
+  return launch_pdl("qmoe_router(mma)", router_mma_kernel<NP, MT, KC>, dim3((T_ + kTok - 1) / kTok), dim3(256), smem, s,
                     (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,
                     (float*)logits);
 }
@@ -405,8 +417,10 @@ int launch_router_mma(const void* x, const void* wr, int T_, int d, int E, int k
   }();
   const bool two = mt_env ? mt_env == 2 : T_ >= 4096;
   if (E <= 16)
-    return two ? launch_router_mma_np<1, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s)
-               : launch_router_mma_np<1, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+    return d % 256 == 0 ? (two ? launch_router_mma_np<1, 2, 256>(x, wr, T_, d, E, k, mode, ids, w, logits, s)
+                               : launch_router_mma_np<1, 1, 256>(x, wr, T_, d, E, k, mode, ids, w, logits, s))
+                        : (two ? launch_router_mma_np<1, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s)
+                               : launch_router_mma_np<1, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s));
   if (E <= 32)
     return two ? launch_router_mma_np<2, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s)
                : launch_router_mma_np<2, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
