@@ -920,7 +920,10 @@ bool use_swap_pair(int xp_rows, int n_experts, int d, int F) {
   if (d % 256 != 0 || F % 128 != 0 || n_experts < 1 || n_experts > kFfnMaxExperts) return false;
   if (forced >= 0) return forced == 1;
   if (n_experts >= 4 && n_experts <= 16) return true;
-  if (n_experts <= 16) return false;
+  // one to three experts (Qwen's shared expert) up to 256 rows: the alternative is the two-launch
+  // split-K path (0.057 / 0.061 / 0.070 ms vs 0.084 / 0.071 / 0.073 at 96 / 128 / 256 tokens;
+  // behind from 384)
+  if (n_experts < 4) return xp_rows <= 256;
   // fine-grained experts: only where the 128-row token tiles would waste > 30% of the tensor
   // work on padding (mean rows per expert just above a multiple of 128: Qwen 2k tokens, ~137
   // rows, 0.22 vs 0.23 ms); elsewhere the token-row tiles are 3-10% faster (epilogue, §2.3b)
