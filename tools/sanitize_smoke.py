@@ -6,7 +6,8 @@ import torch
 from paper_2503_09304_b200 import kernels as K
 
 torch.manual_seed(0)
-for (T, d, F, E, k) in [(16, 256, 512, 8, 2), (400, 256, 512, 4, 2), (600, 256, 256, 2, 2), (1600, 256, 256, 2, 2)]:
+for (T, d, F, E, k) in [(16, 256, 512, 8, 2), (400, 256, 512, 4, 2), (600, 256, 256, 2, 2), (1600, 256, 256, 2, 2),
+                        (200, 256, 512, 1, 1), (1100, 256, 256, 32, 4)]:
     x = torch.randn((T, d), device="cuda").bfloat16()
     wr = (torch.randn((E, d), device="cuda") / d ** 0.5).bfloat16()
     gu = (torch.randn((E, 2 * F, d), device="cuda") / d ** 0.5).bfloat16()
