@@ -408,14 +408,15 @@ int launch_router_mma_np(const void* x, const void* wr, int T_, int d, int E, in
 
 int launch_router_mma(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
                       void* logits, cudaStream_t s) {
-  // 32 tokens per CTA from 4k tokens (halves the W_router re-reads and doubles the MMA work per
-  // staged chunk: Qwen 8k tokens 49 -> 39 us); 16 below that, to keep every SM busy.
+  // 32 tokens per CTA from ~6k tokens (halves the W_router re-reads and doubles the MMA work per
+  // staged chunk: Qwen 8k tokens 49 -> 39 us); 16 below that, to keep every SM busy (4k tokens:
+  // 22.5 vs 26.6 us Mixtral, 28.7 vs 30.7 Qwen).  Same per-token k16 order either way.
   // QMOE_ROUTER_MT=1/2 forces the tile
   static const int mt_env = [] {
     const char* v = getenv("QMOE_ROUTER_MT");
     return v == nullptr ? 0 : atoi(v);
   }();
-  const bool two = mt_env ? mt_env == 2 : T_ >= 4096;
+  const bool two = mt_env ? mt_env == 2 : T_ >= 6144;
   if (E <= 16)
     return d % 256 == 0 ? (two ? launch_router_mma_np<1, 2, 256>(x, wr, T_, d, E, k, mode, ids, w, logits, s)
                                : launch_router_mma_np<1, 1, 256>(x, wr, T_, d, E, k, mode, ids, w, logits, s))
