@@ -7,8 +7,11 @@ used exclusively as the checker by tests/, __graft_entry__.smoke() and bench.py'
 Parity pinning: the toy-model functions below are pinned against the reference's own golden
 fixtures (reference tests/test_model.py:21-23) and against outputs of the reference itself,
 generated in this container by tests/golden/gen_golden.py and committed under tests/golden/.
-The SwiGLU / Qwen functions have NO reference counterpart ("parity unpinned" for them): they
-restate HF transformers 5.5.0 MixtralExperts / Qwen2MoeSparseMoeBlock semantics.
+The SwiGLU / Qwen functions have NO counterpart in the reference: they restate the named
+third-party source, HF transformers 5.5.0 (MixtralTopKRouter / MixtralExperts /
+MixtralSparseMoeBlock, modeling_mixtral.py; Qwen2MoeTopKRouter / Qwen2MoeMLP /
+Qwen2MoeSparseMoeBlock, modeling_qwen2_moe.py), and are pinned against those installed modules
+run in fp64 on CPU (tests/test_hf_parity.py).
 
 Every function cites the reference file:line it restates (paths relative to pkg/src/moesim/).
 """
@@ -153,6 +156,32 @@ def expert_swiglu(gate_up: np.ndarray, down: np.ndarray, X: np.ndarray) -> np.nd
     F = gate_up.shape[0] // 2
     h = X @ gate_up.T
     return (silu(h[:, :F]) * h[:, F:]) @ down.T
+
+
+def sigmoid(x: np.ndarray) -> np.ndarray:
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def sparse_moe_block(w_router: np.ndarray, gate_up: np.ndarray, down: np.ndarray, H: np.ndarray, k: int,
+                     qwen: bool = False, shared_gate_up: np.ndarray | None = None,
+                     shared_down: np.ndarray | None = None, shared_gate: np.ndarray | None = None):
+    """HF MixtralSparseMoeBlock.forward (qwen=False: softmax over the k picked logits == HF's
+    softmax -> top-k -> renormalise) or Qwen2MoeSparseMoeBlock.forward with norm_topk_prob=False
+    (qwen=True: weights are the full softmax at the picked ids), plus the sigmoid-gated shared
+    expert when its weights are given: out = sum_j w_j expert_{id_j}(h) + sigmoid(g.h) shared(h).
+    Routed terms are summed in ascending expert id (reference engine.py:358-360).
+    Returns (ids, w, out)."""
+    ids, w = (route_many_qwen if qwen else route_many)(w_router, H, k)
+    T = H.shape[0]
+    Y = np.zeros((T, k, H.shape[1]))
+    for e, q in enumerate(expert_queues(ids, None, gate_up.shape[0])):
+        if q:
+            rows = np.array(q)
+            Y.reshape(T * k, -1)[rows] = expert_swiglu(gate_up[e], down[e], H[rows // k])
+    out = combine(None, w, Y)
+    if shared_gate_up is not None:
+        out = out + sigmoid(H @ shared_gate.reshape(-1))[:, None] * expert_swiglu(shared_gate_up, shared_down, H)
+    return ids, w, out
 
 
 # ---------------------------------------------------------------------------------------------

@@ -52,6 +52,15 @@ inline size_t dtype_bytes(int dtype) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Bit of the current device in a per-call-site mask: function attributes such as
+// cudaFuncAttributeMaxDynamicSharedMemorySize are per device, so a process driving several GPUs
+// must set them once on each.
+inline uint64_t current_device_bit() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return 1ull << (dev & 63);
+}
+
 // ---- programmatic dependent launch (PDL) -----------------------------------------------
 // The hot-path kernels (router, permute, expert FFN, split-K reduce, combine) are launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization: a kernel may be scheduled while its

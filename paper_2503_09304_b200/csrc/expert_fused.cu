@@ -891,11 +891,11 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
   p.k = k;
   p.gather = x != nullptr;
   p.cursor = cursor_out;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;  // devices already configured
+  if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemF));
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_fused_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemP));
-    attr_set = true;
+    attr_set |= current_device_bit();
   }
   if (pair)
     return launch_pdl("qmoe_expert_ffn(tcgen05 single launch, pair)", ffn_fused_pair_kernel,
@@ -965,10 +965,10 @@ int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* 
   p.k = k;
   p.gather = x != nullptr;
   p.cursor = cursor_out;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;  // devices already configured
+  if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_swap_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSP));
-    attr_set = true;
+    attr_set |= current_device_bit();
   }
   return launch_pdl("qmoe_expert_ffn(tcgen05 swap-AB pair)", ffn_swap_pair_kernel, dim3((tc_num_sms() / 2) * 2),
                     dim3(kThreadsF), kSmemSP, s, maps, p);

@@ -379,11 +379,11 @@ __global__ void __launch_bounds__(256) swap_reduce_kernel(const float* __restric
 
 template <int NT>
 int launch_swap(const CUtensorMap* maps, const SwapParams& p, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;  // devices already configured
+  if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_swap_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        SwapCfg<NT>::kSmem));
-    attr_set = true;
+    attr_set |= current_device_bit();
   }
   return launch_pdl("qmoe_expert_ffn(tcgen05 swap-AB)", ffn_swap_kernel<NT>, dim3(tc_num_sms()), dim3(kThreadsS),
                     SwapCfg<NT>::kSmem, s, maps[0], maps[1], maps[2], maps[3], p);

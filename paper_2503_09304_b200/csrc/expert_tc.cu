@@ -558,7 +558,15 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
 }  // namespace
 
 int tc_init_driver() { return init_driver(); }
-int tc_num_sms() { return g_num_sms; }
+int tc_num_sms() {
+  // per device (g_num_sms is the count of the device current at driver init)
+  static int per_dev[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& n = per_dev[dev & 63];
+  if (n == 0) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : g_num_sms;
+}
 int tc_make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   return make_map(m, base, rows, cols, box_rows);
 }
@@ -567,24 +575,24 @@ namespace {
 
 template <int BN, int EPI>
 int launch_tc(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;  // devices already configured
+  if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem_bytes<BN>()));
-    attr_set = true;
+    attr_set |= current_device_bit();
   }
-  ffn_tc_kernel<BN, EPI><<<g_num_sms, kThreads, smem_bytes<BN>(), s>>>(a, b, p);
+  ffn_tc_kernel<BN, EPI><<<tc_num_sms(), kThreads, smem_bytes<BN>(), s>>>(a, b, p);
   return check_launch("qmoe_expert_ffn(tcgen05)");
 }
 
 template <int EPI>
 int launch_tc2(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;  // devices already configured
+  if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_tc2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes2()));
-    attr_set = true;
+    attr_set |= current_device_bit();
   }
-  ffn_tc2_kernel<EPI><<<(g_num_sms / 2) * 2, kThreads, smem_bytes2(), s>>>(a, b, p);
+  ffn_tc2_kernel<EPI><<<(tc_num_sms() / 2) * 2, kThreads, smem_bytes2(), s>>>(a, b, p);
   return check_launch("qmoe_expert_ffn(tcgen05 cta pair)");
 }
 

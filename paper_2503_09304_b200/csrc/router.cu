@@ -394,12 +394,12 @@ template <int NP, int MT, int KC = kMmaK>
 int launch_router_mma_np(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
                          void* logits, cudaStream_t s) {
   constexpr int kTok = 16 * MT;
-  static bool attr_set = false;
+  static uint64_t attr_set = 0;  // devices already configured
   const int smem = std::max(kMmaStages * (kTok + 16 * NP) * (KC + 8) * 2, (8 + 2) * kTok * kMaxE * 4);
-  if (!attr_set) {
+  if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(router_mma_kernel<NP, MT, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem));
-    attr_set = true;
+    attr_set |= current_device_bit();
   }
   return launch_pdl("qmoe_router(mma)", router_mma_kernel<NP, MT, KC>, dim3((T_ + kTok - 1) / kTok), dim3(256), smem, s,
                     (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,

@@ -132,6 +132,7 @@ class ExpertParallelMoE(torch.nn.Module):
         T = x.shape[0]
         ids, w = ops.router(x, self.w_router, k, self.route_mode)
         perm, offsets, xp = ops.permute(ids, E, x=x)
+        self.last_routing = (ids, w, perm, offsets)
         off = offsets.tolist()
         counts = [off[e + 1] - off[e] for e in range(E)]
         allc = self.exchange_counts(counts)
@@ -225,6 +226,7 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
         x_peers, ret_peers, y_peers, flag_peers = self._peer_tables
         ids, w = ops.router(x, self.w_router, k, self.route_mode)
         perm, offsets, _ = ops.permute(ids, E)
+        self.last_routing = (ids, w, perm, offsets)
         off = offsets.tolist()
         allc = self.exchange_counts([off[e + 1] - off[e] for e in range(E)])
         dest_rank, dest_base = self.dispatch_tables(allc)

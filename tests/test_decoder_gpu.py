@@ -113,7 +113,8 @@ def test_small_mixtral_decoder_prefill_and_decode_match_torch(cuda):
         for i, s in enumerate(seqs):
             ref = torch_reference_hidden(m, s.prompt + s.generated)
             rel = ((captured["h"][i] - ref).norm() / ref.norm()).item()
-            assert rel < 3e-2, (step, i, rel)
+            print(f"decoder step {step} seq {i}: rel {rel:.3e}")
+            assert rel < 1e-2, (step, i, rel)
         for s in seqs:
             s.generated.append(out.tokens[s.id])
             if s.phase is Phase.PREFILL:
@@ -143,4 +144,5 @@ def test_qwen_shape_block_runs_with_shared_expert(cuda):
         a = (torch.nn.functional.silu(gs[: cfg.shared_ffn_dim]) * gs[cfg.shared_ffn_dim:]).bfloat16().float()
         ref[t] += torch.sigmoid(L.sh_gate[0].float() @ x[t].float()) * (L.sh_down[0].float() @ a)
     rel = ((out.float() - ref).norm() / ref.norm()).item()
-    assert rel < 2e-2, rel
+    print(f"qwen block rel {rel:.3e}")
+    assert rel < 1e-2, rel
