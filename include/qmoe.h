@@ -137,6 +137,23 @@ QMOE_API int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int32
                     size_t workspace_bytes, void* stream);
 
 /*
+ * qmoe_expert_ffn plus expert-boundary progress signals (wall-clock serving: the host answers
+ * expert e's report when the GPU has drained expert e, reference engine.py:204-219).
+ * progress (optional): int32[E] in pinned host memory (device-accessible, e.g. cudaHostAlloc under
+ * UVA).  When the last down-projection output of expert e in [e_begin, e_end) is stored, the kernel
+ * writes progress_seq into progress[e] (system-scope release).  Experts at or past a preemption
+ * stop are never signalled.  Paths whose kernels cannot signal per expert (f32/f64 SIMT, the tanh
+ * expert, the two-launch bf16 paths) write every progress[e] of the launch when the stream reaches
+ * its end.  Use a fresh progress_seq per launch (the words are never reset).
+ * Same arguments as qmoe_expert_ffn otherwise.
+ */
+QMOE_API int qmoe_expert_ffn_ex(int variant, int dtype, const void* xp, const int32_t* offsets, const int32_t* perm,
+                                int E, int d, int F, const void* w1, const void* w2, int e_begin, int e_end,
+                                int xp_rows, void* act_ws, void* y, const volatile int32_t* preempt_flag,
+                                int32_t* cursor_out, int32_t* progress, int32_t progress_seq, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/*
  * Kernel path qmoe_expert_ffn takes for a bf16 SwiGLU launch over all E experts of xp_rows routed
  * rows (QMOE_PATH_*).  Host-only, no device work.
  */

@@ -57,6 +57,8 @@ SIGNATURES = {
     "qmoe_expert_ffn_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int, _c_int]),
     "qmoe_expert_ffn": (_c_int, [_c_int, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _c_int,
                                  _c_int, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
+    "qmoe_expert_ffn_ex": (_c_int, [_c_int, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _c_int,
+                                    _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _vp, _c_size, _vp]),
     "qmoe_combine": (_c_int, [_c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp]),
     "qmoe_gather_rows": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),
     "qmoe_scatter_rows": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),

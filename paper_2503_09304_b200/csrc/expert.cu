@@ -14,7 +14,18 @@ __global__ void ffn_finalize_kernel(FfnWorkspace* ws, const int32_t* limit, int 
   ws->stop_inv = 0;
 }
 
+__global__ void ffn_progress_all_kernel(int32_t* progress, int seq, int e_begin, int e_end) {
+  const int e = e_begin + (int)threadIdx.x;
+  if (e < e_end) asm volatile("st.release.sys.b32 [%0], %1;" ::"l"(progress + e), "r"(seq) : "memory");
+}
+
 }  // namespace
+
+int ffn_progress_all(int32_t* progress, int seq, int e_begin, int e_end, cudaStream_t s) {
+  if (progress == nullptr || e_end <= e_begin) return QMOE_OK;
+  ffn_progress_all_kernel<<<1, kFfnMaxExperts, 0, s>>>(progress, seq, e_begin, e_end);
+  return check_launch("qmoe_expert_ffn(progress)");
+}
 
 int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out, cudaStream_t s) {
   ffn_finalize_kernel<<<1, 1, 0, s>>>(ws, limit, e_end, cursor_out);
@@ -33,7 +44,8 @@ static int expert_ffn_entry(int variant, int dtype, const void* xp, const int32_
                                const int32_t* perm, int E, int d, int F, const void* w1, const void* w2,
                                int e_begin, int e_end, int xp_rows, void* act_ws, void* y,
                                const volatile int32_t* preempt_flag, int32_t* cursor_out, void* workspace,
-                               size_t workspace_bytes, void* const* y_peers, void* stream) {
+                               size_t workspace_bytes, void* const* y_peers, void* stream,
+                               int32_t* progress = nullptr, int progress_seq = 0) {
   using namespace qmoe;
   QMOE_REQUIRE(variant == QMOE_EXPERT_TANH_AFFINE || variant == QMOE_EXPERT_SWIGLU,
                "qmoe_expert_ffn: unknown variant %d", variant);
@@ -50,18 +62,29 @@ static int expert_ffn_entry(int variant, int dtype, const void* xp, const int32_
   FfnWorkspace* ws = reinterpret_cast<FfnWorkspace*>(workspace);
   cudaStream_t s = as_stream(stream);
   if (xp_rows == 0 || e_begin == e_end) {
-    return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
+    const int st = ffn_finalize(ws, nullptr, e_end, cursor_out, s);
+    return st ? st : ffn_progress_all(progress, progress_seq, e_begin, e_end, s);
   }
   QMOE_REQUIRE(y_peers == nullptr || (dtype == QMOE_BF16 && variant == QMOE_EXPERT_SWIGLU),
                "qmoe_expert_ffn_peer: peer-memory outputs need the bf16 SwiGLU path");
   switch (dtype) {
     case QMOE_F64:
-    case QMOE_F32:
-      return expert_ffn_simt(variant, dtype, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y,
-                             preempt_flag, cursor_out, ws, s);
-    case QMOE_BF16:
-      return expert_ffn_tc(variant, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, preempt_flag,
-                           cursor_out, ws, xp_rows, y_peers, s);
+    case QMOE_F32: {
+      const int st = expert_ffn_simt(variant, dtype, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y,
+                                     preempt_flag, cursor_out, ws, s);
+      return st ? st : ffn_progress_all(progress, progress_seq, e_begin, e_end, s);
+    }
+    case QMOE_BF16: {
+      // the single-launch kernels signal each expert as its last down unit is stored; the others
+      // mark the launch's experts done when the stream reaches the end of the launch
+      const int path = variant == QMOE_EXPERT_SWIGLU ? expert_ffn_path(d, F, E, xp_rows) : QMOE_PATH_UNSUPPORTED;
+      const bool signals = path == QMOE_PATH_SWAP_AB || path == QMOE_PATH_SWAP_PAIR || path == QMOE_PATH_FUSED_1CTA ||
+                           path == QMOE_PATH_FUSED_PAIR;
+      const int st = expert_ffn_tc(variant, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y,
+                                   preempt_flag, cursor_out, ws, xp_rows, y_peers, s, signals ? progress : nullptr,
+                                   progress_seq);
+      return st || signals ? st : ffn_progress_all(progress, progress_seq, e_begin, e_end, s);
+    }
     default:
       set_error("qmoe_expert_ffn: unknown dtype %d", dtype);
       return QMOE_ERR_INVALID;
@@ -75,6 +98,16 @@ extern "C" int qmoe_expert_ffn(int variant, int dtype, const void* xp, const int
                                size_t workspace_bytes, void* stream) {
   return expert_ffn_entry(variant, dtype, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, xp_rows, act_ws, y,
                           preempt_flag, cursor_out, workspace, workspace_bytes, nullptr, stream);
+}
+
+extern "C" int qmoe_expert_ffn_ex(int variant, int dtype, const void* xp, const int32_t* offsets, const int32_t* perm,
+                                  int E, int d, int F, const void* w1, const void* w2, int e_begin, int e_end,
+                                  int xp_rows, void* act_ws, void* y, const volatile int32_t* preempt_flag,
+                                  int32_t* cursor_out, int32_t* progress, int32_t progress_seq, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  return expert_ffn_entry(variant, dtype, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, xp_rows, act_ws, y,
+                          preempt_flag, cursor_out, workspace, workspace_bytes, nullptr, stream, progress,
+                          progress_seq);
 }
 
 extern "C" int qmoe_expert_ffn_peer(const void* xp, const int32_t* offsets, const int32_t* ret, int E, int d, int F,

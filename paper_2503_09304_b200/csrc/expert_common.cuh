@@ -29,10 +29,11 @@ struct alignas(128) FfnWorkspace {
 };
 
 constexpr int kFfnWorkspaceSlots = 2;
-// Workspace header: kFfnWorkspaceSlots claim slots, then one completion counter per expert (the
-// fused small-batch kernel's gate_up -> down dependency), then the split-K partials.
+// Workspace header: kFfnWorkspaceSlots claim slots, then one gate_up completion counter per expert
+// (the single-launch kernels' gate_up -> down dependency), one down completion counter per expert
+// (expert-boundary progress signals, signal_expert_done), then the split-K partials.
 constexpr int kFfnMaxExperts = 64;
-constexpr size_t kFfnHeaderBytes = sizeof(FfnWorkspace) * kFfnWorkspaceSlots + kFfnMaxExperts * sizeof(int);
+constexpr size_t kFfnHeaderBytes = sizeof(FfnWorkspace) * kFfnWorkspaceSlots + 2 * kFfnMaxExperts * sizeof(int);
 __host__ __device__ inline int* ffn_done(FfnWorkspace* ws) { return reinterpret_cast<int*>(ws + kFfnWorkspaceSlots); }
 
 // Workspace invariant: between launches every claim counter, vote and completion counter of the
@@ -54,7 +55,18 @@ __device__ __forceinline__ void ffn_exit(FfnWorkspace* ws, int* done, int e_end,
   ws->next = 0;
   ws->stop_inv = 0;
   ws->exits = 0;
-  for (int e = 0; e < kFfnMaxExperts; ++e) done[e] = 0;
+  for (int e = 0; e < 2 * kFfnMaxExperts; ++e) done[e] = 0;
+}
+
+// Expert-boundary progress (qmoe_expert_ffn_ex, wall-clock reporting): every epilogue warp that
+// finished storing a down unit of expert e counts itself (lane 0, after __syncwarp); the warp that
+// completes e's count (`need` = down units of e x epilogue warps per unit) publishes `seq` into
+// progress[e] -- pinned host memory the serving host polls, so it answers expert e's report when
+// the GPU has actually drained expert e (reference engine.py:204-219: the report follows the drain).
+__device__ __forceinline__ void signal_expert_done(int* done, int e, int need, int32_t* progress, int seq) {
+  __threadfence();
+  if (atomicAdd(done + kFfnMaxExperts + e, 1) == need - 1)
+    asm volatile("st.release.sys.b32 [%0], %1;" ::"l"(progress + e), "r"(seq) : "memory");
 }
 
 struct TileMap {
@@ -238,7 +250,8 @@ bool use_swap_ab(int xp_rows, int n_experts, int d, int F);
 int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                    void* const* y_peers, const void* x, int T, int k, cudaStream_t s);
+                    void* const* y_peers, const void* x, int T, int k, cudaStream_t s,
+                    int32_t* progress = nullptr, int seq = 0);
 
 // Mid-size and large batches (expert_fused.cu): 128 x 256 (1 CTA) or 256 x 256 (CTA pair) tiles,
 // gate_up and down in one persistent launch.
@@ -246,20 +259,25 @@ bool use_fused_tc();
 int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                      const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                     void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s);
+                     void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s,
+                     int32_t* progress = nullptr, int seq = 0);
 // Mid-size batches of fine-grained experts (expert_fused.cu): swap-AB CTA-pair tiles (256 weight
 // rows x <= 256 tokens, N sized to the valid rows), gate_up and down in one persistent launch.
 bool use_swap_pair(int xp_rows, int n_experts, int d, int F);
 int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                          const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                          const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                         void* const* y_peers, const void* x, int T, int k, cudaStream_t s);
+                         void* const* y_peers, const void* x, int T, int k, cudaStream_t s,
+                         int32_t* progress = nullptr, int seq = 0);
 // Which bf16 SwiGLU kernel qmoe_expert_ffn runs for this shape (QMOE_PATH_* in qmoe.h).
 int expert_ffn_path(int d, int F, int E, int xp_rows);
 
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                   const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int total_rows_hint,
-                  void* const* y_peers, cudaStream_t s);
+                  void* const* y_peers, cudaStream_t s, int32_t* progress = nullptr, int seq = 0);
+// Marks experts [e_begin, e_end) done in progress[] once the stream reaches it (paths whose
+// kernels do not signal per expert: SIMT, tanh, two-launch).
+int ffn_progress_all(int32_t* progress, int seq, int e_begin, int e_end, cudaStream_t s);
 
 }  // namespace qmoe

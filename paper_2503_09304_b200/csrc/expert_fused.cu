@@ -50,6 +50,8 @@ struct FusedParams {
   int k;       // top-k: gate_up A rows are x[perm[r] / k] when gather != 0
   int gather;  // 1: gate_up A tiles are gathered from X by the producer warp (TMA tile::gather4)
   int32_t* cursor;  // optional cursor_out (written by the last CTA out, ffn_exit)
+  int32_t* progress;  // optional host-mapped per-expert progress words (signal_expert_done)
+  int seq;
 };
 
 // Token rows of one 128-row A tile for the gather: lane l owns rows [4l, 4l+4) of the tile; rows
@@ -271,6 +273,9 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(p.done + e, 1);
+      } else if (p.progress != nullptr) {
+        __syncwarp();
+        if (lane == 0) signal_expert_done(p.done, e, map2.m_tiles[e - map2.e_first] * nt2 * 4, p.progress, p.seq);
       }
     }
   }
@@ -519,6 +524,9 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(p.done + e, 1);
+      } else if (p.progress != nullptr) {
+        __syncwarp();  // both CTAs' 4 epilogue warps store part of every pair tile
+        if (lane == 0) signal_expert_done(p.done, e, map2.m_tiles[e - map2.e_first] * nt2 * 8, p.progress, p.seq);
       }
     }
   }
@@ -838,6 +846,9 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(p.done + e, 1);
+      } else if (p.progress != nullptr) {
+        __syncwarp();  // both CTAs' 4 epilogue warps store part of every pair tile
+        if (lane == 0) signal_expert_done(p.done, e, map2.m_tiles[e - map2.e_first] * nt2 * 8, p.progress, p.seq);
       }
     }
   }
@@ -865,7 +876,8 @@ bool use_fused_tc() {
 int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                      const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                     void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s) {
+                     void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s,
+                     int32_t* progress, int seq) {
   int st;
   CUtensorMap maps[4];
   // A boxes: 128 token rows (each CTA of a pair loads its own 128), or single rows of X for the
@@ -891,6 +903,8 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
   p.k = k;
   p.gather = x != nullptr;
   p.cursor = cursor_out;
+  p.progress = progress;
+  p.seq = seq;
   static uint64_t attr_set = 0;  // devices already configured
   if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemF));
@@ -935,7 +949,8 @@ bool use_swap_pair(int xp_rows, int n_experts, int d, int F) {
 int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                          const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                          const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                         void* const* y_peers, const void* x, int T, int k, cudaStream_t s) {
+                         void* const* y_peers, const void* x, int T, int k, cudaStream_t s,
+                         int32_t* progress, int seq) {
   int st;
   SpMaps maps;
   // tokens: 32/64/128-row boxes of Xp / act (each CTA loads its N/2 rows from the box start), or
@@ -965,6 +980,8 @@ int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* 
   p.k = k;
   p.gather = x != nullptr;
   p.cursor = cursor_out;
+  p.progress = progress;
+  p.seq = seq;
   static uint64_t attr_set = 0;  // devices already configured
   if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_swap_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSP));

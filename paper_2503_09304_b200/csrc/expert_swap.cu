@@ -59,6 +59,8 @@ struct SwapParams {
   int k;               // top-k: gate_up B rows are x[perm[r] / k] when gather != 0
   int gather;          // 1: token rows gathered from X by the producer warp (TMA tile::gather4)
   int32_t* cursor;     // optional cursor_out (written by the last CTA out, ffn_exit)
+  int32_t* progress;   // optional host-mapped per-expert progress words (signal_expert_done)
+  int seq;
 };
 
 template <int NT>
@@ -338,6 +340,10 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(p.done + e, 1);
+      } else if (p.progress != nullptr) {
+        __syncwarp();
+        if (lane == 0)
+          signal_expert_done(p.done, e, map2.m_tiles[e - map2.e_first] * nt2 * p.nsplit * 4, p.progress, p.seq);
       }
     }
   }
@@ -422,7 +428,7 @@ bool use_swap_ab(int xp_rows, int n_experts, int d, int F) {
 int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                    void* const* y_peers, const void* x, int T, int k, cudaStream_t s) {
+                    void* const* y_peers, const void* x, int T, int k, cudaStream_t s, int32_t* progress, int seq) {
   int st;
   // Token tile: 32 rows when experts see ~1-24 rows on average (decode), 64 up to ~64, else 128.
   const double mean_rows = (double)xp_rows / (E > 0 ? E : 1);
@@ -448,6 +454,8 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
   p.k = k;
   p.gather = x != nullptr;
   p.cursor = cursor_out;
+  p.progress = progress;
+  p.seq = seq;
   const int nkb2 = (F + kBK - 1) / kBK;
   const int want = xp_rows <= kSwapRowsMax ? swap_splits(F) : 1;  // partials sized for <= 512 rows
   p.kb_per_split = (nkb2 + want - 1) / want;

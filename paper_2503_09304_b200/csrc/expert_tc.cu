@@ -601,7 +601,7 @@ int launch_tc2(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cu
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                   const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                  void* const* y_peers, cudaStream_t s) {
+                  void* const* y_peers, cudaStream_t s, int32_t* progress, int seq) {
   int st = init_driver();
   if (st) return st;
   QMOE_REQUIRE(d % 64 == 0, "qmoe_expert_ffn(bf16): d must be a multiple of 64 (d=%d)", d);
@@ -610,10 +610,10 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
                "qmoe_expert_ffn(bf16): buffers must be 16-byte aligned");
   if (variant == QMOE_EXPERT_SWIGLU && use_swap_ab(xp_rows, E, d, F))
     return expert_ffn_swap(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
-                           xp_rows, y_peers, nullptr, 0, 0, s);
+                           xp_rows, y_peers, nullptr, 0, 0, s, progress, seq);
   if (variant == QMOE_EXPERT_SWIGLU && use_swap_pair(xp_rows, E, d, F))
     return expert_ffn_swap_pair(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
-                                xp_rows, y_peers, nullptr, 0, 0, s);
+                                xp_rows, y_peers, nullptr, 0, 0, s, progress, seq);
   constexpr int BN = 256;
   TcParams p{};
   p.e_begin = e_begin;
@@ -635,7 +635,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   const bool pair = use_cta_pair(xp_rows, e_end - e_begin);
   if (down_splits(xp_rows, e_end - e_begin, d, F) == 1 && use_fused_tc())
     return expert_ffn_fused(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
-                            xp_rows, y_peers, pair, nullptr, 0, 0, s);
+                            xp_rows, y_peers, pair, nullptr, 0, 0, s, progress, seq);
   // gate_up: act[r, :F] = SiLU(x W1^T) * (x W3^T), expert order rows
   if ((st = make_map(&ta, xp, xp_rows, d, BM)) || (st = make_map(&tb, w1, (uint64_t)E * 2 * F, d, BN / 2))) return st;
   p.N = F; p.K = d; p.b_rows = 2 * F;

@@ -33,6 +33,7 @@ Device plugin interface (model.py implements it; tests may substitute a replay d
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Union
@@ -177,7 +178,15 @@ class InferenceEngine:
         self._pinned_off = None
         self._flags = None
         self._flag_slot = 0
-        self._on_expert_reports = None
+        self._on_expert_report = None
+        self._launch_seq = 0
+        self._stop_marks: list = []
+        self._preempt_at = {"ATTENTION": 0, "ROUTER": 0}
+        self.stats["reports_at_drain"] = 0
+        # wall clock: reports of the experts holding the last report_tail of a launch's rows are
+        # answered without waiting for their drain (keeps the host ahead of the GPU; see
+        # _experts_device_preempt)
+        self.report_tail = float(os.environ.get("QMOE_REPORT_TAIL", "0.15"))
 
     def next_batch_id(self) -> int:
         self._batch_counter += 1
@@ -200,10 +209,12 @@ class InferenceEngine:
 
     # ------------------------------------------------------------------------------------------
     def execute(self, batch: Batch, sequences: list[Sequence], on_report: ReportCallback,
-                on_expert_reports: Optional[Callable[[list[EngineReport]], Optional[int]]] = None) -> IterationOutcome:
-        """on_expert_reports (optional): answers the expert-boundary reports of one grouped launch
-        in order and returns the index of the first PREEMPT (wall-clock device-preempt path)."""
-        self._on_expert_reports = on_expert_reports
+                on_expert_report: Optional[Callable[[EngineReport, Optional[SchedulerDirective]],
+                                                    SchedulerDirective]] = None) -> IterationOutcome:
+        """on_expert_report (optional, wall-clock device-preempt path): answers one expert-boundary
+        report given the previous expert report's answer in the same launch (None for the first),
+        so a driver may skip re-running a pure policy when nothing changed in between."""
+        self._on_expert_report = on_expert_report
         if [s.id for s in sequences] != batch.members:
             raise SimulationError("sequence list does not match batch members")
         st = self._init_state(sequences)
@@ -221,6 +232,7 @@ class InferenceEngine:
                 scanned = sum(self.cache.count(s.cache_handle, layer) for s in st.seqs)
                 self._charge(self.cost.attention_cost(st.T, scanned))
                 if on_report(self._report(batch, Stage.ATTENTION, layer, st)) is PREEMPT:
+                    self._preempt_at["ATTENTION"] += 1
                     return self._preempt(st, layer, Stage.ROUTER)
                 stage = Stage.ROUTER
 
@@ -229,6 +241,7 @@ class InferenceEngine:
                 st.y, st.cursor = m.new_expert_state(st.T)
                 self._charge(self.cost.router_cost)
                 if on_report(self._report(batch, Stage.ROUTER, layer, st)) is PREEMPT:
+                    self._preempt_at["ROUTER"] += 1
                     return self._preempt(st, layer, Stage.EXPERTS)
                 stage = Stage.EXPERTS
 
@@ -277,12 +290,22 @@ class InferenceEngine:
         return stop_dev, preempted
 
     def _experts_device_preempt(self, batch, st, layer, perm, offsets, xp, on_report):
-        """Wall-clock mode: launch ALL experts at once with a fresh device preempt flag (polled by
-        the kernel whenever a CTA moves to a new expert), copy the queue lengths asynchronously,
-        and answer the expert-boundary reports on the host WHILE the grouped GEMM runs.  A PREEMPT
-        answer raises the flag: the kernel stops at the next expert boundary and writes where it
-        stopped (cursor_out), from which the per-token cursors advance on the device — no host
-        round trip between the decision and the stop."""
+        """Device-resident preemption: launch ALL experts at once with a fresh device preempt flag
+        (polled by the kernel whenever a CTA moves to a new expert) and per-expert progress words
+        in pinned host memory (the kernel publishes a launch sequence number into progress[e] when
+        expert e's last output row is stored).
+
+        Wall clock: the report of expert e is answered when the GPU has actually drained expert e
+        (the host polls progress[e]; arrivals are admitted up to that moment), as in the reference
+        where the report follows the drain (engine.py:204-219, sim.py:135-142).  A PREEMPT answer
+        raises the flag: the kernel stops at the next expert boundary and writes where it stopped
+        (cursor_out), from which the per-token cursors advance on the device -- no host round trip
+        between the decision and the stop.  So that the host still enqueues the next layer while
+        the GPU finishes this one, the reports of the experts holding the last `report_tail`
+        fraction of the launch's rows are answered without waiting (the last one's answer is
+        equivalent to the next ATTENTION report: a preemption there resumes at the combine).
+
+        Virtual clock (tests): reports are answered right after the launch, one by one."""
         import torch
 
         m = self.model
@@ -297,46 +320,85 @@ class InferenceEngine:
             self._flags = torch.zeros(1024, dtype=torch.int32, device=dev)
             self._sig_src = torch.zeros(1024, dtype=torch.int32, pin_memory=True)
             self._sig_stream = torch.cuda.Stream(device=dev)
+            # progress words: written by the GPU (system-scope stores), read here through numpy
+            self._progress = torch.zeros(64, dtype=torch.int32, pin_memory=True)
+            self._progress_np = self._progress.numpy()
+            self._stop_log = torch.zeros(4096, dtype=torch.int32, pin_memory=True)
         self._pinned_off.copy_(offsets, non_blocking=True)
         self._off_ready.record()
         slot = self._flag_slot = (self._flag_slot + 1) % 1024
         self._flags[(slot + 512) % 1024].zero_()
         flag = self._flags[slot:slot + 1]
-        stop_dev = m.run_experts(layer, xp, offsets, perm, st.y, 0, E, preempt_flag=flag)
+        self._launch_seq += 1
+        seq = self._launch_seq
+        stop_dev = m.run_experts(layer, xp, offsets, perm, st.y, 0, E, preempt_flag=flag, progress=self._progress,
+                                 progress_seq=seq)
         self.stats["expert_launches"] += 1
         self._off_ready.synchronize()  # waits for the permute only; the GEMM keeps running
         off = self._pinned_off.tolist()
+        hit = [e for e in range(E) if off[e + 1] > off[e]]
         stop = None
-        # batched answers only on a wall clock (charges are no-ops there; a virtual clock charges
-        # experts one by one up to the preempting report, engine.py:215 in the reference)
-        if self._on_expert_reports is not None and not getattr(self.clock, "virtual", True):
-            hit, reports = [], []
-            for e in range(E):
-                n = off[e + 1] - off[e]
-                if n:
-                    self._charge(self.cost.expert_cost(n))
-                    hit.append(e)
-                    reports.append(self._report(batch, Stage.EXPERTS, layer, st, expert_id=e))
-            i = self._on_expert_reports(reports)
-            if i is not None:
-                stop = hit[i] + 1
+        wall = not getattr(self.clock, "virtual", True)
+        if self._on_expert_report is not None and wall:
+            prog = self._progress_np
+            tail_rows = self.report_tail * off[E]
+            last = None
+            for i, e in enumerate(hit):
+                if off[E] - off[e + 1] >= tail_rows and prog[e] != seq:
+                    self._await_progress(prog, e, seq)
+                    self.stats["reports_at_drain"] += 1
+                d = self._on_expert_report(self._report(batch, Stage.EXPERTS, layer, st, expert_id=e), last)
+                if d is PREEMPT:
+                    stop = e + 1
+                    break
+                last = d
         else:
-            for e in range(E):
-                n = off[e + 1] - off[e]
-                if n == 0:
-                    continue
-                self._charge(self.cost.expert_cost(n))
+            for e in hit:
+                self._charge(self.cost.expert_cost(off[e + 1] - off[e]))
                 if self._on_report(batch, st, layer, e, on_report) is PREEMPT:
                     stop = e + 1
                     break
         if stop is not None:
             # raise "stop at the first boundary >= stop" while the kernel runs: an async H2D write
             # on a side stream (copy engine), so the reported expert always completes
+            running = self._progress_np[hit[-1]] != seq
             self._sig_src[slot] = stop
             with torch.cuda.stream(self._sig_stream):
                 flag.copy_(self._sig_src[slot:slot + 1], non_blocking=True)
+            # where the kernel really stopped, read back lazily (preemption_positions())
+            i = len(self._stop_marks) % self._stop_log.numel()
+            self._stop_log[i:i + 1].copy_(stop_dev, non_blocking=True)
+            self._stop_marks.append((i, stop, hit[-1] + 1, running))
             return stop_dev, True
         return stop_dev, False
+
+    def _await_progress(self, prog, e: int, seq: int, timeout_s: float = 30.0) -> None:
+        """Spin on the pinned progress word of expert e (a plain host read, ~100 ns)."""
+        if prog[e] == seq:
+            return
+        t_end = time.perf_counter() + timeout_s
+        n = 0
+        while prog[e] != seq:
+            n += 1
+            if (n & 0xFFFF) == 0 and time.perf_counter() > t_end:
+                raise SimulationError(f"expert {e} never reported completion (launch {seq})")
+
+    def preemption_positions(self) -> dict:
+        """Where preemptions landed: ATTENTION / ROUTER reports, or an expert report -- and for those,
+        whether the device flag stopped the grouped kernel before its last hit expert
+        (EXPERT_MID_LAUNCH) or the kernel had already covered every hit expert (EXPERT_END_OF_LAUNCH).
+        Synchronises the device once."""
+        import torch
+
+        torch.cuda.synchronize()
+        out = dict(self._preempt_at)
+        for (i, asked, end, running) in self._stop_marks:
+            got = int(self._stop_log[i])
+            key = "EXPERT_MID_LAUNCH" if got < end else "EXPERT_END_OF_LAUNCH"
+            out[key] = out.get(key, 0) + 1
+            out["flag_raised_while_running"] = out.get("flag_raised_while_running", 0) + int(running)
+        out["expert_reports_answered_at_drain"] = self.stats["reports_at_drain"]
+        return out
 
     def _on_report(self, batch, st, layer, expert, on_report):
         return on_report(self._report(batch, Stage.EXPERTS, layer, st, expert_id=expert))

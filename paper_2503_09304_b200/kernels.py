@@ -119,12 +119,15 @@ def permute(ids: torch.Tensor, num_experts: int, cursor: Optional[torch.Tensor] 
 def expert_ffn(variant: int, xp: torch.Tensor, offsets: torch.Tensor, perm: torch.Tensor, w1: torch.Tensor,
                w2: torch.Tensor, y: torch.Tensor, e_begin: int = 0, e_end: Optional[int] = None,
                act_ws: Optional[torch.Tensor] = None, preempt_flag: Optional[torch.Tensor] = None,
-               cursor_out: Optional[torch.Tensor] = None) -> None:
+               cursor_out: Optional[torch.Tensor] = None, progress: Optional[torch.Tensor] = None,
+               progress_seq: int = 0) -> None:
     """Run experts [e_begin, e_end) over their rows of xp; results land in y[perm[r]] (slot order).
 
     TANH_AFFINE: w1 = A [E, d, d], w2 = b [E, d].  SWIGLU: w1 = gate_up [E, 2F, d], w2 = down [E, d, F],
     act_ws = [rows, F] scratch.  preempt_flag: int32 device-visible flag polled at expert boundaries;
-    cursor_out: int32 [1] device tensor receiving the first expert not completed."""
+    cursor_out: int32 [1] device tensor receiving the first expert not completed.
+    progress: pinned host int32 [E] (qmoe_expert_ffn_ex): progress[e] = progress_seq once expert e
+    is drained on the device."""
     for name, t in (("xp", xp), ("w1", w1), ("w2", w2), ("y", y)):
         _need(t, name, xp.dtype)
     _need(offsets, "offsets", torch.int32)
@@ -153,9 +156,17 @@ def expert_ffn(variant: int, xp: torch.Tensor, offsets: torch.Tensor, perm: torc
     lib = _lib.load()
     nbytes = lib.qmoe_expert_ffn_workspace_bytes(variant, _code(xp), d, xp.shape[0])
     ws = workspace(nbytes, "ffn", xp.device)
-    check(lib.qmoe_expert_ffn(variant, _code(xp), _ptr(xp), _ptr(offsets), _ptr(perm), E, d, F, _ptr(w1), _ptr(w2),
-                              e_begin, e_end, xp.shape[0], _ptr(act_ws), _ptr(y), _ptr(preempt_flag),
-                              _ptr(cursor_out), _ptr(ws), nbytes, _stream()), "qmoe_expert_ffn")
+    if progress is None:
+        check(lib.qmoe_expert_ffn(variant, _code(xp), _ptr(xp), _ptr(offsets), _ptr(perm), E, d, F, _ptr(w1),
+                                  _ptr(w2), e_begin, e_end, xp.shape[0], _ptr(act_ws), _ptr(y), _ptr(preempt_flag),
+                                  _ptr(cursor_out), _ptr(ws), nbytes, _stream()), "qmoe_expert_ffn")
+        return
+    if not progress.is_pinned() or progress.dtype != torch.int32 or progress.numel() < E:
+        raise ValueError("progress must be a pinned host int32 tensor with >= E entries")
+    check(lib.qmoe_expert_ffn_ex(variant, _code(xp), _ptr(xp), _ptr(offsets), _ptr(perm), E, d, F, _ptr(w1), _ptr(w2),
+                                 e_begin, e_end, xp.shape[0], _ptr(act_ws), _ptr(y), _ptr(preempt_flag),
+                                 _ptr(cursor_out), _ptr(progress), int(progress_seq), _ptr(ws), nbytes, _stream()),
+          "qmoe_expert_ffn_ex")
 
 
 def combine(y: torch.Tensor, w: torch.Tensor, residual: Optional[torch.Tensor], out: Optional[torch.Tensor] = None):

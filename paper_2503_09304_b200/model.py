@@ -198,9 +198,11 @@ class MoEModel:
         return K.permute(ids, self.config.num_experts, cursor=cursor, x=x)
 
     def run_experts(self, layer: int, xp, offsets, perm, y, e_begin: int, e_end: int,
-                    preempt_flag: Optional[torch.Tensor] = None) -> torch.Tensor:
+                    preempt_flag: Optional[torch.Tensor] = None, progress: Optional[torch.Tensor] = None,
+                    progress_seq: int = 0) -> torch.Tensor:
         K.expert_ffn(self.expert_variant, xp, offsets, perm, self.expert_weight[layer], self.expert_bias[layer], y,
-                     e_begin=e_begin, e_end=e_end, preempt_flag=preempt_flag, cursor_out=self._stop)
+                     e_begin=e_begin, e_end=e_end, preempt_flag=preempt_flag, cursor_out=self._stop,
+                     progress=progress, progress_seq=progress_seq)
         return self._stop
 
     def advance_cursor(self, cursor: torch.Tensor, stop_dev: torch.Tensor) -> None:

@@ -57,7 +57,14 @@ def serve_once(model, trace, scheduler: str, max_batch_size: int = 32, slo_ms: f
         "completion_rate_jps": rep.completion_rate_jps, "preemptions": res.probes.preemptions,
         "decode_iter_ms_median": dec[len(dec) // 2] if dec else None,
         "engine": res.engine_stats,
+        "preempt_positions": sim.engine.preemption_positions(),
     }
+    if dec and ls:
+        # the paper's SLO is 10x an A100 decode iteration; the B200 analogue is 10x
+        # this run's measured median decode iteration
+        scaled = 10.0 * dec[len(dec) // 2]
+        out["scaled_slo_ms"] = scaled
+        out["ls_scaled_slo_attainment"] = aggregate(res.records, scaled, res.makespan_ms).ls.slo_attainment
     del sim, res
     gc.collect()  # the run's KV page pools sit in reference cycles; free them before the next run
     torch.cuda.empty_cache()

@@ -89,7 +89,7 @@ class ReplayModel:
         offsets = torch.tensor([0] + list(torch.tensor(counts).cumsum(0).tolist()), dtype=torch.int32)
         return perm, offsets, None
 
-    def run_experts(self, layer, xp, offsets, perm, y, e_begin, e_end, preempt_flag=None):
+    def run_experts(self, layer, xp, offsets, perm, y, e_begin, e_end, preempt_flag=None, **_):
         return torch.tensor([e_end], dtype=torch.int32)
 
     def advance_cursor(self, cursor, stop):
