@@ -233,32 +233,38 @@ def run_serving(args) -> dict:
 
 
 QWEN = (2048, 1408, 60, 4)  # Qwen1.5-MoE-A2.7B routed experts (BASELINE config 4)
+QWEN_SHARED = 5632          # its shared expert's width
 
 
 def run_qwen_layer(dev, flush, world: int) -> dict:
-    """BASELINE config 4: fine-grained experts (60, top-4, F=1408) — small per-expert M.  One MoE
-    layer step (router -> permute -> tcgen05 experts -> combine; routed experts only) at a prefill
-    batch (8192 tokens, ~546 rows per expert) and a decode batch (32 tokens, ~2 rows per expert),
-    L2 flushed before every step.  Roofline: tensor (large batch) / HBM weight streaming (decode)."""
+    """BASELINE config 4: fine-grained experts (60, top-4, F=1408) — small per-expert M — plus the
+    sigmoid-gated shared expert (Fs=5632), i.e. the whole Qwen1.5-MoE-A2.7B MoE layer.  One step =
+    router (+ shared gate) -> permute -> ONE tcgen05 grouped launch over the 60 routed experts and
+    the shared expert as 4 F-wide sub-experts -> combine, at a prefill batch (8192 tokens, ~546
+    rows per routed expert) and a decode batch (32 tokens), L2 flushed before every step.
+    Roofline: tensor (large batch) / HBM weight streaming (decode)."""
     import torch
 
     from paper_2503_09304_b200 import kernels as K
 
     d, F, E, k = QWEN
+    S = QWEN_SHARED // F
     g = torch.Generator(device=dev).manual_seed(7)
-    wr = (torch.randn((E, d), device=dev, generator=g) * d ** -0.5).bfloat16()
-    gu = (torch.randn((E, 2 * F, d), device=dev, generator=g) * d ** -0.5).bfloat16()
-    dn = (torch.randn((E, d, F), device=dev, generator=g) * F ** -0.5).bfloat16()
+    wr = (torch.randn((E + 1, d), device=dev, generator=g) * d ** -0.5).bfloat16()
+    gu = (torch.randn((E + S, 2 * F, d), device=dev, generator=g) * d ** -0.5).bfloat16()
+    dn = (torch.randn((E + S, d, F), device=dev, generator=g) * F ** -0.5).bfloat16()
+    dn[E:] *= (F / QWEN_SHARED) ** 0.5  # shared expert's down ~ N(0, 1/Fs)
     peaks, _ = load_peaks()
-    out = {"shape": f"d={d} F={F} E={E} top-{k} (routed experts; softmax->top-k, no renorm)"}
+    out = {"shape": f"d={d} F={F} E={E} top-{k} (softmax->top-k, no renorm) + shared expert Fs={QWEN_SHARED} "
+                    f"as {S} sub-experts in the same launch"}
     for name, T in (("prefill", 8192), ("decode", 32)):
         x = torch.randn((T, d), device=dev, generator=g).bfloat16()
-        y = torch.empty((T * k, d), dtype=torch.bfloat16, device=dev)
-        act = torch.empty((T * k, F), dtype=torch.bfloat16, device=dev)
+        y = torch.empty((T * (k + S), d), dtype=torch.bfloat16, device=dev)
+        act = torch.empty((T * (k + S), F), dtype=torch.bfloat16, device=dev)
 
         def layer():
-            ids, w = K.router(x, wr, k, K.ROUTE_SOFTMAX_TOPK)
-            perm, offsets, xp = K.permute(ids, E, x=x)
+            ids, w = K.router(x, wr, k, K.ROUTE_SOFTMAX_TOPK, n_shared=S)
+            perm, offsets, xp = K.permute(ids, E + S, x=x)
             K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act)
             return K.combine(y, w, x), offsets
 
@@ -276,8 +282,8 @@ def run_qwen_layer(dev, flush, world: int) -> dict:
             ts.append((a, b))
         torch.cuda.synchronize()
         ms = statistics.median(a.elapsed_time(b) for a, b in ts)
-        flops = 6.0 * T * k * d * F
-        wbytes = hit * 3 * d * F * 2
+        flops = 6.0 * T * (k + S) * d * F  # routed + shared (6 T d Fs)
+        wbytes = hit * 3 * d * F * 2       # hit counts the shared sub-experts
         out[name] = {"tokens": T, "ms": ms, "tflops": flops / ms / 1e9, "weight_gbs": wbytes / ms / 1e6,
                      "tensor_frac_sustained": flops / ms / 1e9 / float(peaks.get("bf16_tflops_sustained",
                                                                                     peaks["bf16_tflops"])),

@@ -94,6 +94,19 @@ QMOE_API const char* qmoe_last_error(void);
  */
 QMOE_API int qmoe_router(const void* x, const void* w_router, int T, int d, int E, int k, int dtype,
                 int route_mode, int32_t* ids_out, void* w_out, void* logits_out, void* stream);
+/*
+ * Router with a sigmoid-gated shared expert folded into the routing (HF Qwen2MoeSparseMoeBlock:
+ * out = sum_j w_j expert_j(h) + sigmoid(shared_expert_gate . h) * shared_expert(h)), for running
+ * the shared expert as n_shared extra "experts" of the routed width in the same grouped launch
+ * (a SwiGLU of width F*n_shared is the sum of n_shared SwiGLUs over its F-wide column blocks).
+ * w_router has E + 1 rows when n_shared > 0: the E routed experts, then the shared gate.
+ * ids_out / w_out are [T, k + n_shared]: the k routed picks (as qmoe_router), then ids
+ * E .. E+n_shared-1 with weight sigmoid(gate logit).  logits_out (optional) is [T, E + 1].
+ * n_shared = 0 is qmoe_router.  Requires k + n_shared <= 8 and E + 1 <= 64.
+ */
+QMOE_API int qmoe_router_shared(const void* x, const void* w_router, int T, int d, int E, int k, int n_shared,
+                                int dtype, int route_mode, int32_t* ids_out, void* w_out, void* logits_out,
+                                void* stream);
 
 /*
  * Permute (replaces _enqueue_expert_work + ExpertQueues.enqueue/drain, engine.py:312-328,
@@ -215,6 +228,14 @@ QMOE_API int qmoe_cursor_advance(int32_t* cursor, int T, const int32_t* stop_exp
  */
 QMOE_API int qmoe_kv_append(void* pool, const int32_t* slot_mapping, const void* rows, int n_rows,
                    size_t row_bytes, void* stream);
+/*
+ * qmoe_kv_append that does nothing when *guard < 0 at the time it runs.  guard is the iteration's
+ * expert preempt flag: a grouped expert launch that stopped early leaves it at -1, so the K/V
+ * rows of the layers a run-ahead host already enqueued behind the preemption point are not
+ * appended (the preempted batch resumes at the expert boundary, engine.py:401-423).
+ */
+QMOE_API int qmoe_kv_append_guarded(void* pool, const int32_t* slot_mapping, const void* rows, int n_rows,
+                                    size_t row_bytes, const int32_t* guard, void* stream);
 /* dst[i] = pool[slot_mapping[i]] (one sequence's entries, ascending entry order). */
 QMOE_API int qmoe_kv_gather(const void* pool, const int32_t* slot_mapping, int n_rows, size_t row_bytes,
                    void* dst, void* stream);

@@ -52,6 +52,8 @@ SIGNATURES = {
     "qmoe_status_string": (ctypes.c_char_p, [_c_int]),
     "qmoe_last_error": (ctypes.c_char_p, []),
     "qmoe_router": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
+    "qmoe_router_shared": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp,
+                                    _vp]),
     "qmoe_permute_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int]),
     "qmoe_permute": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_size, _vp, _vp, _c_size, _vp]),
     "qmoe_expert_ffn_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int, _c_int]),
@@ -64,6 +66,7 @@ SIGNATURES = {
     "qmoe_scatter_rows": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),
     "qmoe_cursor_advance": (_c_int, [_vp, _c_int, _vp, _vp]),
     "qmoe_kv_append": (_c_int, [_vp, _vp, _vp, _c_int, _c_size, _vp]),
+    "qmoe_kv_append_guarded": (_c_int, [_vp, _vp, _vp, _c_int, _c_size, _vp, _vp]),
     "qmoe_kv_gather": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),
     "qmoe_rmsnorm": (_c_int, [_vp, _vp, _vp, ctypes.c_float, _c_int, _c_int, _vp, _vp, _vp]),
     "qmoe_rope": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),

@@ -104,9 +104,11 @@ combine_bf16_kernel(const __nv_bfloat16* __restrict__ y, const float* __restrict
 }
 
 __global__ void gather_rows_kernel(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx,
-                                   int rows, size_t row_bytes, uint8_t* __restrict__ dst, int scatter) {
+                                   int rows, size_t row_bytes, uint8_t* __restrict__ dst, int scatter,
+                                   const volatile int32_t* guard) {
   const int r = blockIdx.x * 8 + warp_id();
   if (r >= rows) return;
+  if (guard != nullptr && *guard < 0) return;  // voided iteration (qmoe_kv_append_guarded)
   const int lane = lane_id();
   const uint8_t* s = scatter ? src + (size_t)r * row_bytes : src + (size_t)idx[r] * row_bytes;
   uint8_t* d = scatter ? dst + (size_t)idx[r] * row_bytes : dst + (size_t)r * row_bytes;
@@ -128,12 +130,12 @@ __global__ void cursor_advance_kernel(int32_t* cursor, int ntok, const int32_t* 
 }
 
 int launch_rows(const void* src, const int32_t* idx, int rows, size_t row_bytes, void* dst, int scatter,
-                cudaStream_t s, const char* what) {
+                cudaStream_t s, const char* what, const int32_t* guard = nullptr) {
   QMOE_REQUIRE(rows >= 0 && row_bytes > 0, "%s: bad sizes", what);
   if (rows == 0) return QMOE_OK;
   QMOE_REQUIRE(src && idx && dst, "%s: null pointer", what);
   gather_rows_kernel<<<(rows + 7) / 8, 256, 0, s>>>((const uint8_t*)src, idx, rows, row_bytes, (uint8_t*)dst,
-                                                    scatter);
+                                                    scatter, guard);
   return check_launch(what);
 }
 
@@ -225,6 +227,12 @@ extern "C" int qmoe_kv_append(void* pool, const int32_t* slot_mapping, const voi
                               size_t row_bytes, void* stream) {
   return qmoe::launch_rows(rows, slot_mapping, n_rows, row_bytes, pool, 1, qmoe::as_stream(stream),
                            "qmoe_kv_append");
+}
+
+extern "C" int qmoe_kv_append_guarded(void* pool, const int32_t* slot_mapping, const void* rows, int n_rows,
+                                      size_t row_bytes, const int32_t* guard, void* stream) {
+  return qmoe::launch_rows(rows, slot_mapping, n_rows, row_bytes, pool, 1, qmoe::as_stream(stream),
+                           "qmoe_kv_append_guarded", guard);
 }
 
 extern "C" int qmoe_kv_gather(const void* pool, const int32_t* slot_mapping, int n_rows, size_t row_bytes,

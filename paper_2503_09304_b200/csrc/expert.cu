@@ -4,12 +4,14 @@
 namespace qmoe {
 namespace {
 
-__global__ void ffn_finalize_kernel(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out) {
+__global__ void ffn_finalize_kernel(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out,
+                                    volatile int32_t* flag) {
   int c = INT_MAX - ws->stop_inv;
   if (c > e_end) c = e_end;
   if (limit != nullptr && *limit < c) c = *limit;
   ws->stop = c;
   if (cursor_out != nullptr) *cursor_out = c;
+  if (flag != nullptr && c < e_end) *flag = -1;  // the iteration is void from here (ffn_exit)
   ws->next = 0;  // leave the slot zeroed for the next launch (workspace invariant, expert_common.cuh)
   ws->stop_inv = 0;
 }
@@ -27,8 +29,9 @@ int ffn_progress_all(int32_t* progress, int seq, int e_begin, int e_end, cudaStr
   return check_launch("qmoe_expert_ffn(progress)");
 }
 
-int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out, cudaStream_t s) {
-  ffn_finalize_kernel<<<1, 1, 0, s>>>(ws, limit, e_end, cursor_out);
+int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out, cudaStream_t s,
+                 const volatile int32_t* flag) {
+  ffn_finalize_kernel<<<1, 1, 0, s>>>(ws, limit, e_end, cursor_out, const_cast<volatile int32_t*>(flag));
   return check_launch("qmoe_expert_ffn(finalize)");
 }
 

@@ -43,7 +43,12 @@ __host__ __device__ inline int* ffn_done(FfnWorkspace* ws) { return reinterpret_
 // Single-launch kernels finalize in-kernel: one thread per CTA calls this after the CTA's last
 // claim and store; the LAST CTA out publishes the stop expert (what ffn_finalize_kernel does for
 // the multi-launch paths), writes cursor_out, and re-zeroes the header for the next launch.
-__device__ __forceinline__ void ffn_exit(FfnWorkspace* ws, int* done, int e_end, int32_t* cursor_out) {
+// A launch that stopped before e_end because of its preempt flag leaves the flag at -1 ("void"):
+// every later launch polling the same flag -- the rest of the preempted iteration, already
+// enqueued by a host that runs ahead -- claims nothing, and guarded KV appends
+// (qmoe_kv_append_guarded) skip, so the abandoned layers leave no state behind.
+__device__ __forceinline__ void ffn_exit(FfnWorkspace* ws, int* done, int e_end, int32_t* cursor_out,
+                                         const volatile int32_t* flag = nullptr) {
   __threadfence();
   const unsigned n = gridDim.x * gridDim.y * gridDim.z;
   if (atomicAdd(&ws->exits, 1) != (int)n - 1) return;
@@ -52,6 +57,7 @@ __device__ __forceinline__ void ffn_exit(FfnWorkspace* ws, int* done, int e_end,
   if (c > e_end) c = e_end;
   ws->stop = c;
   if (cursor_out != nullptr) *cursor_out = c;
+  if (flag != nullptr && c < e_end) *const_cast<volatile int32_t*>(flag) = -1;
   ws->next = 0;
   ws->stop_inv = 0;
   ws->exits = 0;
@@ -164,8 +170,8 @@ __device__ __forceinline__ int ffn_claim(const TileMap& m, FfnWorkspace* ws, con
   const int e = m.expert_of(t, local);
   if (flag != nullptr && e != last_e) {
     const int s = *flag;
-    if (s > 0) {
-      int cand = local == 0 ? e : e + 1;
+    if (s != 0) {  // s < 0: the iteration was preempted by an earlier launch -- stop here
+      int cand = (s < 0 || local == 0) ? e : e + 1;
       if (cand < s) cand = s;
       atomicMax(&ws->stop_inv, INT_MAX - cand);
     }
@@ -202,8 +208,8 @@ __device__ __forceinline__ int resolve_claim(const TileMap& m1, int N2, FfnWorks
     const int e = m1.expert_of(t, local);
     if (flag != nullptr && e != last_e) {
       const int s = *flag;
-      if (s > 0) {
-        int cand = local == 0 ? e : e + 1;
+      if (s != 0) {  // s < 0: the iteration was preempted by an earlier launch -- stop here
+        int cand = (s < 0 || local == 0) ? e : e + 1;
         if (cand < s) cand = s;
         atomicMax(&ws->stop_inv, INT_MAX - cand);
       }
@@ -235,7 +241,9 @@ __device__ __forceinline__ bool expert_ready(const int* done, int e, int need, c
 // Extra workspace the bf16 SwiGLU path needs for split-K partials of the down projection.
 size_t splitk_bytes(int xp_rows, int d);
 // cursor = min(stop of ws, *limit (optional), e_end); written to ws->stop and cursor_out (optional).
-int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out, cudaStream_t s);
+// flag (optional): set to -1 when the stop falls before e_end (see ffn_exit).
+int ffn_finalize(FfnWorkspace* ws, const int32_t* limit, int e_end, int32_t* cursor_out, cudaStream_t s,
+                 const volatile int32_t* flag = nullptr);
 
 int expert_ffn_simt(int variant, int dtype, const void* xp, const int32_t* offsets, const int32_t* perm, int E,
                     int d, int F, const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,

@@ -280,7 +280,7 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor);
+  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor, p.flag);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<2 * kBN>(tmem_base);
@@ -532,7 +532,7 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
-  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor);
+  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor, p.flag);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_cg2<2 * kBN>(tmem_base);
@@ -854,7 +854,7 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
-  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor);
+  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor, p.flag);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_cg2<2 * kTokSP>(tmem_base);

@@ -127,7 +127,7 @@ int run_simt(int variant, const void* xp, const int32_t* offsets, const int32_t*
                                                           (const T*)w2, e_begin, e_end, nullptr, (T*)y, flag,
                                                           ws + 0);
     if ((st = check_launch("qmoe_expert_ffn(simt tanh)"))) return st;
-    return ffn_finalize(ws + 0, nullptr, e_end, cursor_out, s);
+    return ffn_finalize(ws + 0, nullptr, e_end, cursor_out, s, flag);
   }
   ffn_simt_kernel<T, EPI_SWIGLU><<<grid, kThreads, 0, s>>>((const T*)xp, offsets, perm, E, F, d, (const T*)w1,
                                                           nullptr, e_begin, e_end, nullptr, (T*)act_ws, flag,
@@ -138,7 +138,7 @@ int run_simt(int variant, const void* xp, const int32_t* offsets, const int32_t*
   ffn_simt_kernel<T, EPI_DOWN><<<grid, kThreads, 0, s>>>((const T*)act_ws, offsets, perm, E, d, F, (const T*)w2,
                                                         nullptr, e_begin, e_end, &ws[0].stop, (T*)y, flag, ws + 1);
   if ((st = check_launch("qmoe_expert_ffn(simt down)"))) return st;
-  return ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s);
+  return ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s, flag);
 }
 
 }  // namespace

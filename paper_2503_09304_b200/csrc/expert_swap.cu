@@ -348,7 +348,7 @@ ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor);
+  if (threadIdx.x == 0) ffn_exit(p.ws, p.done, p.e_end, p.cursor, p.flag);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::kTmemCols>(tmem_base);

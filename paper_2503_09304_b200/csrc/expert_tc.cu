@@ -630,7 +630,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
     p.out = (__nv_bfloat16*)y; p.out_ld = d;
     p.ws = ws;
     if ((st = launch_tc<BN, EPI_TANH>(ta, tb, p, s))) return st;
-    return ffn_finalize(ws, nullptr, e_end, cursor_out, s);
+    return ffn_finalize(ws, nullptr, e_end, cursor_out, s, flag);
   }
   const bool pair = use_cta_pair(xp_rows, e_end - e_begin);
   if (down_splits(xp_rows, e_end - e_begin, d, F) == 1 && use_fused_tc())
@@ -659,7 +659,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
     p2.part = splitk_buffer(ws);
     p2.part_rows = xp_rows;
     if ((st = launch_tc<BN, EPI_DOWN_PART>(ta2, tb2, p2, s))) return st;
-    if ((st = ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s))) return st;
+    if ((st = ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s, flag))) return st;
     const int grid = xp_rows / 8 + 1 < 148 * 4 ? xp_rows / 8 + 1 : 148 * 4;
     splitk_reduce_kernel<<<grid, 256, 0, s>>>(p2.part, p2.nsplit, xp_rows, d, perm, offsets, e_begin, &ws[1].stop,
                                                (__nv_bfloat16*)y, y_peers);
@@ -667,7 +667,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
   }
   p2.nsplit = 1;
   if ((st = pair ? launch_tc2<EPI_DOWN>(ta2, tb2, p2, s) : launch_tc<BN, EPI_DOWN>(ta2, tb2, p2, s))) return st;
-  return ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s);
+  return ffn_finalize(ws + 1, &ws[0].stop, e_end, cursor_out, s, flag);
 }
 
 int expert_ffn_path(int d, int F, int E, int xp_rows) {

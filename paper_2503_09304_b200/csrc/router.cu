@@ -48,16 +48,25 @@ template <typename A> __device__ __forceinline__ A warp_sum(A v) {
 __device__ __forceinline__ float exp_acc(float v) { return expf(v); }
 __device__ __forceinline__ double exp_acc(double v) { return exp(v); }
 
+// E logit rows.  ns > 0 (Qwen2-MoE shared expert run as ns sub-experts of the routed width): the
+// last logit row is the shared expert's gate; top-k runs over the first E - 1 experts and the
+// token's slots k .. k+ns-1 get ids E-1 .. E-2+ns with weight sigmoid(gate logit)
+// (HF Qwen2MoeSparseMoeBlock: sigmoid(shared_expert_gate(h)) * shared_expert(h)).
+// The kernels carry ns in bits 8.. of `mode` (set by qmoe_router_shared).
 template <typename A>
 __device__ __noinline__ void select_token(const A* lg, A* s_score, int tok, int E, int k, int mode, int lane,
                                              int32_t* __restrict__ ids_out, A* __restrict__ w_out,
                                              A* __restrict__ logits_out) {
-  const bool ok0 = lane < E, ok1 = lane + 32 < E;
-  const A l0 = ok0 ? lg[lane] : A(0), l1 = ok1 ? lg[lane + 32] : A(0);
+  const int ns = mode >> 8;
+  mode &= 0xFF;
   if (logits_out != nullptr) {
-    if (ok0) logits_out[(size_t)tok * E + lane] = l0;
-    if (ok1) logits_out[(size_t)tok * E + lane + 32] = l1;
+    if (lane < E) logits_out[(size_t)tok * E + lane] = lg[lane];
+    if (lane + 32 < E) logits_out[(size_t)tok * E + lane + 32] = lg[lane + 32];
   }
+  const int Er = ns > 0 ? E - 1 : E;  // experts eligible for the top-k
+  const int ko = k + ns;              // slots per token
+  const bool ok0 = lane < Er, ok1 = lane + 32 < Er;
+  const A l0 = ok0 ? lg[lane] : A(0), l1 = ok1 ? lg[lane + 32] : A(0);
   A s0 = l0, s1 = l1;  // value the top-k ranks on
   if (mode == QMOE_ROUTE_SOFTMAX_TOPK) {
     A m = ok0 ? l0 : l1;
@@ -114,8 +123,15 @@ __device__ __noinline__ void select_token(const A* lg, A* s_score, int tok, int 
     for (int j = 0; j < k; ++j) wv[j] = wv[j] / tot;
   }
   for (int j = 0; j < k; ++j) {
-    ids_out[(size_t)tok * k + j] = pick[j];
-    w_out[(size_t)tok * k + j] = wv[j];
+    ids_out[(size_t)tok * ko + j] = pick[j];
+    w_out[(size_t)tok * ko + j] = wv[j];
+  }
+  if (ns > 0) {
+    const A g = A(1) / (A(1) + exp_acc(-lg[Er]));
+    for (int s = 0; s < ns; ++s) {
+      ids_out[(size_t)tok * ko + k + s] = Er + s;
+      w_out[(size_t)tok * ko + k + s] = g;
+    }
   }
 }
 
@@ -451,18 +467,23 @@ int dispatch_router(const void* x, const void* wr, int T_, int d, int E, int k, 
 }  // namespace
 }  // namespace qmoe
 
-extern "C" int qmoe_router(const void* x, const void* w_router, int T, int d, int E, int k, int dtype,
-                           int route_mode, int32_t* ids_out, void* w_out, void* logits_out,
-                           void* stream) {
+extern "C" int qmoe_router_shared(const void* x, const void* w_router, int T, int d, int E, int k, int n_shared,
+                                  int dtype, int route_mode, int32_t* ids_out, void* w_out, void* logits_out,
+                                  void* stream) {
   using namespace qmoe;
   QMOE_REQUIRE(T >= 0 && d >= 1, "qmoe_router: bad sizes T=%d d=%d", T, d);
-  QMOE_REQUIRE(E >= 1 && E <= kMaxE, "qmoe_router: E=%d outside [1, %d]", E, kMaxE);
+  QMOE_REQUIRE(n_shared >= 0 && n_shared <= 8 && k + n_shared <= 8,
+               "qmoe_router_shared: need 0 <= n_shared and k + n_shared <= 8 (k=%d, n_shared=%d)", k, n_shared);
+  const int rows = E + (n_shared > 0 ? 1 : 0);  // logit rows: routed experts (+ the shared gate)
+  QMOE_REQUIRE(E >= 1 && rows <= kMaxE, "qmoe_router: E=%d (+ shared gate) outside [1, %d]", E, kMaxE);
   QMOE_REQUIRE(k >= 1 && k <= E && k <= 8, "qmoe_router: k=%d must satisfy 1 <= k <= min(E, 8)", k);
   QMOE_REQUIRE(route_mode == QMOE_ROUTE_TOPK_SOFTMAX || route_mode == QMOE_ROUTE_SOFTMAX_TOPK,
                "qmoe_router: unknown route_mode %d", route_mode);
   if (T == 0) return QMOE_OK;
   QMOE_REQUIRE(x && w_router && ids_out && w_out, "qmoe_router: null pointer");
   cudaStream_t s = as_stream(stream);
+  E = rows;
+  route_mode |= n_shared << 8;  // mode word: the kernels hand n_shared to select_token in bits 8..
   switch (dtype) {
     case QMOE_BF16:
       return dispatch_router<__nv_bfloat16>(x, w_router, T, d, E, k, route_mode, ids_out, w_out, logits_out, s);
@@ -474,4 +495,10 @@ extern "C" int qmoe_router(const void* x, const void* w_router, int T, int d, in
       set_error("qmoe_router: unknown dtype %d", dtype);
       return QMOE_ERR_INVALID;
   }
+}
+
+extern "C" int qmoe_router(const void* x, const void* w_router, int T, int d, int E, int k, int dtype,
+                           int route_mode, int32_t* ids_out, void* w_out, void* logits_out,
+                           void* stream) {
+  return qmoe_router_shared(x, w_router, T, d, E, k, 0, dtype, route_mode, ids_out, w_out, logits_out, stream);
 }

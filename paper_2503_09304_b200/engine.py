@@ -183,10 +183,15 @@ class InferenceEngine:
         self._stop_marks: list = []
         self._preempt_at = {"ATTENTION": 0, "ROUTER": 0}
         self.stats["reports_at_drain"] = 0
-        # wall clock: reports of the experts holding the last report_tail of a launch's rows are
-        # answered without waiting for their drain (keeps the host ahead of the GPU; see
+        self._active = None   # the running iteration's preempt flag (device-preempt mode)
+        self._flag = None
+        self._prev = None     # the previous layer's state within the running iteration
+        self._ring_i = 0
+        self._last_hit: list = []
+        # wall clock: the reports of the experts holding the last report_tail of a launch's rows
+        # are answered without waiting for their drain (1.0: none waits; see
         # _experts_device_preempt)
-        self.report_tail = float(os.environ.get("QMOE_REPORT_TAIL", "0.15"))
+        self.report_tail = float(os.environ.get("QMOE_REPORT_TAIL", "1.0"))
 
     def next_batch_id(self) -> int:
         self._batch_counter += 1
@@ -218,13 +223,22 @@ class InferenceEngine:
         if [s.id for s in sequences] != batch.members:
             raise SimulationError("sequence list does not match batch members")
         st = self._init_state(sequences)
-        m = self.model
-        L, E = m.config.num_layers, m.config.num_experts
         layer, stage = batch.layer_cursor, batch.stage_cursor
         if stage not in (Stage.ATTENTION, Stage.ROUTER, Stage.EXPERTS):
             raise SimulationError(f"batch cursor at non-executable stage {stage}")
         self.stats["iterations"] += 1
+        if not self._device_preempt:
+            return self._run(batch, st, layer, stage, on_report)
+        self._begin_iteration()
+        try:
+            return self._run(batch, st, layer, stage, on_report)
+        finally:
+            self._end_iteration()
 
+    def _run(self, batch: Batch, st: _State, layer: int, stage: Stage, on_report: ReportCallback) -> IterationOutcome:
+        m = self.model
+        L = m.config.num_layers
+        dev = self._device_preempt
         while layer < L:
             if stage is Stage.ATTENTION:
                 st.x, st.res = m.attention_batch(layer, st.h, st.members, self.cache)
@@ -232,6 +246,8 @@ class InferenceEngine:
                 scanned = sum(self.cache.count(s.cache_handle, layer) for s in st.seqs)
                 self._charge(self.cost.attention_cost(st.T, scanned))
                 if on_report(self._report(batch, Stage.ATTENTION, layer, st)) is PREEMPT:
+                    if dev and self._prev_voided(sync=True):
+                        return self._preempt_void(batch, on_report, layer)
                     self._preempt_at["ATTENTION"] += 1
                     return self._preempt(st, layer, Stage.ROUTER)
                 stage = Stage.ROUTER
@@ -241,27 +257,129 @@ class InferenceEngine:
                 st.y, st.cursor = m.new_expert_state(st.T)
                 self._charge(self.cost.router_cost)
                 if on_report(self._report(batch, Stage.ROUTER, layer, st)) is PREEMPT:
+                    if dev and self._prev_voided(sync=True):
+                        return self._preempt_void(batch, on_report, layer)
                     self._preempt_at["ROUTER"] += 1
                     return self._preempt(st, layer, Stage.EXPERTS)
                 stage = Stage.EXPERTS
 
             # EXPERTS: queue build for the pending slots, boundary decisions, one grouped launch.
             perm, offsets, xp = m.permute(st.ids, st.cursor, st.x)
-            if self._device_preempt:
+            if dev:
                 stop_dev, preempted = self._experts_device_preempt(batch, st, layer, perm, offsets, xp, on_report)
+                if preempted is None:  # the previous layer's launch was stopped by the device flag
+                    return self._preempt_void(batch, on_report, layer)
             else:
                 stop_dev, preempted = self._experts_host_boundary(batch, st, layer, perm, offsets, xp, on_report)
             if preempted:
                 m.advance_cursor(st.cursor, stop_dev)
                 return self._preempt(st, layer, Stage.EXPERTS)
             st.h = m.combine_batch(layer, st.y, st.w, st.res, st.x)
+            if dev:
+                self._prev = _State(st.seqs, st.members, st.T, None, st.x, st.res, st.ids, st.w, st.y, st.cursor,
+                                    st.progress)
+                self._prev.layer, self._prev.ring, self._prev.hit = layer, self._ring_i, self._last_hit
             st.x = st.res = st.ids = st.w = st.y = st.cursor = None
             layer += 1
             stage = Stage.ATTENTION
 
         rows = [mr.row0 + mr.n - 1 for mr in st.members]
-        tokens = m.emit_batch(st.h, rows)
+        tokens = m.emit_batch(st.h, rows)  # synchronises: the last expert launch's stop is in
+        if dev and self._prev_voided(sync=True):
+            return self._preempt_void(batch, on_report, L)
         return Completed({s.id: int(t) for s, t in zip(st.seqs, tokens)})
+
+    # ------------------------------------------------------------------------------------------
+    # Device-resident preemption (wall clock).  One preempt flag per iteration, polled by every
+    # grouped expert launch of the iteration at each expert boundary: 0 = run; s > 0 = stop at the
+    # first boundary >= s; -1 = a launch of this iteration stopped early, so everything enqueued
+    # behind it is void (later launches claim nothing, guarded K/V appends skip).  It is raised
+    # either by the host at an expert report (PREEMPT answer) or, with no host round trip, by
+    # raise_arrival_flag() -- the serving driver's arrival watcher, the moment an LS request
+    # arrives (qllm_policy preempts for a fresh LS prefill, reference sched.py:57-70).  The host
+    # keeps running ahead of the GPU (it enqueues layer l+1 while layer l's experts run) and learns
+    # that layer l stopped one layer later, at layer l+1's queue-length read; it then rolls the
+    # iteration back to layer l's expert boundary (_preempt_void).
+    def _begin_iteration(self) -> None:
+        import torch
+
+        m = self.model
+        if self._flags is None:
+            dev = m.device
+            # Flags live in DEVICE memory (an L2 hit for the polling SMs; host-mapped memory polled
+            # by every CTA serialises on PCIe).  A ring of slots, one per iteration; slot i+512 is
+            # zeroed in stream order so a slot is clean long before reuse.
+            self._flags = torch.zeros(1024, dtype=torch.int32, device=dev)
+            self._sig_src = torch.zeros(1024, dtype=torch.int32, pin_memory=True)
+            self._sig_stream = torch.cuda.Stream(device=dev)
+            self._one = torch.ones(1, dtype=torch.int32, pin_memory=True)
+            self._watch_stream = torch.cuda.Stream(device=dev)
+            # per launch: where it stopped (device copy for the cursor advance, pinned copy + event
+            # for the host), a ring of 256
+            self._stop_dev_ring = torch.zeros(256, dtype=torch.int32, device=dev)
+            self._stop_pinned = torch.zeros(256, dtype=torch.int32, pin_memory=True)
+            self._stop_events = [torch.cuda.Event() for _ in range(256)]
+            # progress words: written by the GPU (system-scope stores), read here through numpy
+            self._progress = torch.zeros(64, dtype=torch.int32, pin_memory=True)
+            self._progress_np = self._progress.numpy()
+            self._stop_log = torch.zeros(4096, dtype=torch.int32, pin_memory=True)
+        slot = self._flag_slot = (self._flag_slot + 1) % 1024
+        self._flags[(slot + 512) % 1024].zero_()
+        self._flag = self._flags[slot:slot + 1]
+        self._prev = None
+        if hasattr(m, "preempt_guard"):
+            m.preempt_guard = self._flag
+        self._active = self._flag  # visible to raise_arrival_flag (another thread)
+
+    def _end_iteration(self) -> None:
+        self._active = None
+        self._prev = None
+        if hasattr(self.model, "preempt_guard"):
+            self.model.preempt_guard = None
+
+    def raise_arrival_flag(self) -> bool:
+        """Thread-safe: ask the running iteration's expert launches to stop at their next expert
+        boundary (flag := 1, an async H2D write on this thread's own stream).  Returns False when no
+        iteration is running (the arrival is then seen at the next report).  A write landing on an
+        iteration that already ended, or on a flag already at -1, is harmless: slots are reused 512
+        iterations later, and a void iteration is rolled back by the host regardless."""
+        import torch
+
+        flag = self._active
+        if flag is None:
+            return False
+        with torch.cuda.stream(self._watch_stream):
+            flag.copy_(self._one, non_blocking=True)
+        self.stats["arrival_flags"] = self.stats.get("arrival_flags", 0) + 1
+        return True
+
+    def _prev_voided(self, sync: bool) -> bool:
+        """Did the previous layer's expert launch of this iteration stop before its last expert?"""
+        p = self._prev
+        if p is None:
+            return False
+        if sync:
+            self._stop_events[p.ring].synchronize()
+        return int(self._stop_pinned[p.ring]) < self.model.config.num_experts
+
+    def _preempt_void(self, batch: Batch, on_report: ReportCallback, layer: int) -> Preempted:
+        """Roll back to the expert boundary where the previous layer's launch stopped: undo the
+        K/V reservation of the layer enqueued behind it (its guarded append was skipped), deliver
+        the report of the last expert that completed (the policy admits the arrival that raised
+        the flag and answers PREEMPT), advance that layer's cursors on the device, checkpoint."""
+        p = self._prev
+        m = self.model
+        if layer < m.config.num_layers:
+            self.cache.unreserve_batch([mr.seq.cache_handle for mr in p.members], layer, [mr.n for mr in p.members])
+        stop = int(self._stop_pinned[p.ring])
+        done = [e for e in p.hit if e < stop]
+        rep = (self._report(batch, Stage.EXPERTS, p.layer, p, expert_id=done[-1]) if done
+               else self._report(batch, Stage.ROUTER, p.layer, p))
+        if on_report(rep) is not PREEMPT:
+            self.stats["flag_policy_disagree"] = self.stats.get("flag_policy_disagree", 0) + 1
+        m.advance_cursor(p.cursor, self._stop_dev_ring[p.ring:p.ring + 1])
+        self._preempt_at["EXPERT_DEVICE_FLAG"] = self._preempt_at.get("EXPERT_DEVICE_FLAG", 0) + 1
+        return self._preempt(p, p.layer, Stage.EXPERTS)
 
     # ------------------------------------------------------------------------------------------
     def _experts_host_boundary(self, batch, st, layer, perm, offsets, xp, on_report):
@@ -290,53 +408,47 @@ class InferenceEngine:
         return stop_dev, preempted
 
     def _experts_device_preempt(self, batch, st, layer, perm, offsets, xp, on_report):
-        """Device-resident preemption: launch ALL experts at once with a fresh device preempt flag
-        (polled by the kernel whenever a CTA moves to a new expert) and per-expert progress words
-        in pinned host memory (the kernel publishes a launch sequence number into progress[e] when
-        expert e's last output row is stored).
+        """Device-resident preemption: launch ALL experts at once under the iteration's preempt
+        flag (polled by the kernel whenever a CTA moves to a new expert) with per-expert progress
+        words in pinned host memory (the kernel publishes a launch sequence number into
+        progress[e] when expert e's last output row is stored).  Returns (stop_dev, preempted),
+        preempted None when the PREVIOUS layer's launch turned out to have stopped early.
 
-        Wall clock: the report of expert e is answered when the GPU has actually drained expert e
-        (the host polls progress[e]; arrivals are admitted up to that moment), as in the reference
-        where the report follows the drain (engine.py:204-219, sim.py:135-142).  A PREEMPT answer
-        raises the flag: the kernel stops at the next expert boundary and writes where it stopped
-        (cursor_out), from which the per-token cursors advance on the device -- no host round trip
-        between the decision and the stop.  So that the host still enqueues the next layer while
-        the GPU finishes this one, the reports of the experts holding the last `report_tail`
-        fraction of the launch's rows are answered without waiting (the last one's answer is
-        equivalent to the next ATTENTION report: a preemption there resumes at the combine).
+        Wall clock: the expert reports are answered right after the queue lengths arrive, while
+        the grouped GEMM runs; with report_tail < 1 the report of expert e instead waits until the
+        GPU has drained expert e (the host polls progress[e]; arrivals are admitted up to that
+        moment, as in the reference where the report follows the drain, engine.py:204-219,
+        sim.py:135-142) -- measured to cost ~30% of decode throughput, because the host then
+        stops running ahead of the GPU.  An LS arrival needs neither: the serving driver raises
+        the flag itself (raise_arrival_flag).  A PREEMPT answer raises the flag to "stop at the
+        first boundary >= e+1": the kernel stops there and writes where it stopped (cursor_out),
+        from which the per-token cursors advance on the device.
 
         Virtual clock (tests): reports are answered right after the launch, one by one."""
         import torch
 
         m = self.model
         E = m.config.num_experts
-        dev = m.device
         if self._pinned_off is None or self._pinned_off.numel() != E + 1:
             self._pinned_off = torch.empty(E + 1, dtype=torch.int32, pin_memory=True)
             self._off_ready = torch.cuda.Event()
-            # Flags live in DEVICE memory (an L2 hit for the polling SMs; host-mapped memory polled
-            # by every CTA serialises on PCIe).  A ring of slots, one per launch; slot i+512 is
-            # zeroed in stream order so a slot is clean long before reuse.
-            self._flags = torch.zeros(1024, dtype=torch.int32, device=dev)
-            self._sig_src = torch.zeros(1024, dtype=torch.int32, pin_memory=True)
-            self._sig_stream = torch.cuda.Stream(device=dev)
-            # progress words: written by the GPU (system-scope stores), read here through numpy
-            self._progress = torch.zeros(64, dtype=torch.int32, pin_memory=True)
-            self._progress_np = self._progress.numpy()
-            self._stop_log = torch.zeros(4096, dtype=torch.int32, pin_memory=True)
         self._pinned_off.copy_(offsets, non_blocking=True)
         self._off_ready.record()
-        slot = self._flag_slot = (self._flag_slot + 1) % 1024
-        self._flags[(slot + 512) % 1024].zero_()
-        flag = self._flags[slot:slot + 1]
+        flag = self._flag
         self._launch_seq += 1
         seq = self._launch_seq
         stop_dev = m.run_experts(layer, xp, offsets, perm, st.y, 0, E, preempt_flag=flag, progress=self._progress,
                                  progress_seq=seq)
+        ring = self._ring_i = (self._ring_i + 1) % 256
+        self._stop_dev_ring[ring:ring + 1].copy_(stop_dev)
+        self._stop_pinned[ring:ring + 1].copy_(stop_dev, non_blocking=True)
+        self._stop_events[ring].record()
         self.stats["expert_launches"] += 1
         self._off_ready.synchronize()  # waits for the permute only; the GEMM keeps running
+        if self._prev_voided(sync=False):  # the permute ran after the previous launch: its stop is in
+            return stop_dev, None
         off = self._pinned_off.tolist()
-        hit = [e for e in range(E) if off[e + 1] > off[e]]
+        hit = self._last_hit = [e for e in range(E) if off[e + 1] > off[e]]
         stop = None
         wall = not getattr(self.clock, "virtual", True)
         if self._on_expert_report is not None and wall:
@@ -362,6 +474,7 @@ class InferenceEngine:
             # raise "stop at the first boundary >= stop" while the kernel runs: an async H2D write
             # on a side stream (copy engine), so the reported expert always completes
             running = self._progress_np[hit[-1]] != seq
+            slot = self._flag_slot
             self._sig_src[slot] = stop
             with torch.cuda.stream(self._sig_stream):
                 flag.copy_(self._sig_src[slot:slot + 1], non_blocking=True)

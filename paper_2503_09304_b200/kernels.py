@@ -69,20 +69,29 @@ def workspace(nbytes: int, tag: str, device: torch.device) -> torch.Tensor:
 
 
 def router(x: torch.Tensor, w_router: torch.Tensor, k: int, mode: int = ROUTE_TOPK_SOFTMAX,
-           want_logits: bool = False):
-    """ids [T,k] int32 (ascending), weights [T,k] (f64 for f64 inputs else f32), optional logits."""
+           want_logits: bool = False, n_shared: int = 0):
+    """ids [T,k] int32 (ascending), weights [T,k] (f64 for f64 inputs else f32), optional logits.
+
+    n_shared > 0 (qmoe_router_shared): w_router is [E + 1, d] with the shared expert's gate as the
+    last row; ids / weights are [T, k + n_shared], the shared slots holding ids E.. with weight
+    sigmoid(gate logit)."""
     _need(x, "x")
     _need(w_router, "w_router", x.dtype)
     T, d = x.shape
-    E = w_router.shape[0]
+    rows = w_router.shape[0]
+    E = rows - (1 if n_shared else 0)
     if w_router.shape[1] != d:
         raise ValueError("w_router must be [E, d]")
-    ids = torch.empty((T, k), dtype=torch.int32, device=x.device)
-    w = torch.empty((T, k), dtype=acc_dtype(x.dtype), device=x.device)
-    logits = torch.empty((T, E), dtype=w.dtype, device=x.device) if want_logits else None
+    ids = torch.empty((T, k + n_shared), dtype=torch.int32, device=x.device)
+    w = torch.empty((T, k + n_shared), dtype=acc_dtype(x.dtype), device=x.device)
+    logits = torch.empty((T, rows), dtype=w.dtype, device=x.device) if want_logits else None
     lib = _lib.load()
-    check(lib.qmoe_router(_ptr(x), _ptr(w_router), T, d, E, k, _code(x), mode, _ptr(ids), _ptr(w), _ptr(logits),
-                          _stream()), "qmoe_router")
+    if n_shared:
+        check(lib.qmoe_router_shared(_ptr(x), _ptr(w_router), T, d, E, k, n_shared, _code(x), mode, _ptr(ids),
+                                     _ptr(w), _ptr(logits), _stream()), "qmoe_router_shared")
+    else:
+        check(lib.qmoe_router(_ptr(x), _ptr(w_router), T, d, E, k, _code(x), mode, _ptr(ids), _ptr(w), _ptr(logits),
+                              _stream()), "qmoe_router")
     return (ids, w, logits) if want_logits else (ids, w)
 
 
@@ -227,14 +236,23 @@ def cursor_advance(cursor: torch.Tensor, stop_dev: torch.Tensor) -> None:
     check(lib.qmoe_cursor_advance(_ptr(cursor), cursor.shape[0], _ptr(stop_dev), _stream()), "qmoe_cursor_advance")
 
 
-def kv_append(pool: torch.Tensor, slot_mapping: torch.Tensor, rows: torch.Tensor) -> None:
+def kv_append(pool: torch.Tensor, slot_mapping: torch.Tensor, rows: torch.Tensor,
+              guard: Optional[torch.Tensor] = None) -> None:
+    """pool[slot_mapping[i]] = rows[i]; with guard (the iteration's int32 device preempt flag) the
+    append is skipped on the device when *guard < 0 (qmoe_kv_append_guarded)."""
     _need(pool, "pool")
     _need(rows, "rows", pool.dtype)
     _need(slot_mapping, "slot_mapping", torch.int32)
     n = rows.shape[0]
     row_bytes = rows[0].numel() * rows.element_size() if n else 1
     lib = _lib.load()
-    check(lib.qmoe_kv_append(_ptr(pool), _ptr(slot_mapping), _ptr(rows), n, row_bytes, _stream()), "qmoe_kv_append")
+    if guard is None:
+        check(lib.qmoe_kv_append(_ptr(pool), _ptr(slot_mapping), _ptr(rows), n, row_bytes, _stream()),
+              "qmoe_kv_append")
+        return
+    _need(guard, "guard", torch.int32)
+    check(lib.qmoe_kv_append_guarded(_ptr(pool), _ptr(slot_mapping), _ptr(rows), n, row_bytes, _ptr(guard),
+                                     _stream()), "qmoe_kv_append_guarded")
 
 
 def kv_gather(pool: torch.Tensor, slot_mapping: torch.Tensor, out: torch.Tensor) -> torch.Tensor:

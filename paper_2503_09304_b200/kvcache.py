@@ -134,6 +134,15 @@ class UnifiedDynamicCache:
         self._ledger += total * self.entry_bytes
         return out
 
+    def unreserve_batch(self, handles, layer: int, ns) -> None:
+        """Undo reserve_batch(handles, layer, ns) (the entries were never written: a layer a run-ahead
+        host enqueued behind a device-side preemption point, whose guarded append was skipped).
+        Pages stay with their sequences."""
+        counts_d = self._counts
+        for h, n in zip(handles, ns):
+            counts_d[h][layer] -= n
+        self._ledger -= sum(ns) * self.entry_bytes
+
     def append_many(self, handle: int, layer: int, rows: torch.Tensor) -> None:
         slots = self.reserve(handle, layer, rows.shape[0])
         K.kv_append(self._pools[layer], torch.tensor(slots, dtype=torch.int32, device=self.device),
@@ -142,13 +151,14 @@ class UnifiedDynamicCache:
     def append(self, handle: int, layer: int, row: torch.Tensor) -> None:
         self.append_many(handle, layer, row.unsqueeze(0))
 
-    def scatter(self, layer: int, slots, rows: torch.Tensor) -> None:
+    def scatter(self, layer: int, slots, rows: torch.Tensor, guard: Optional[torch.Tensor] = None) -> None:
         """One launch for the new rows of many sequences (slots from ``reserve``: a list or an
-        int32 device tensor)."""
+        int32 device tensor).  guard: skip on the device if the iteration was preempted
+        (kernels.kv_append)."""
         if len(slots):
             if not isinstance(slots, torch.Tensor):
                 slots = torch.tensor(slots, dtype=torch.int32, device=self.device)
-            K.kv_append(self._pools[layer], slots, rows.contiguous())
+            K.kv_append(self._pools[layer], slots, rows.contiguous(), guard=guard)
 
     def entries(self, handle: int, layer: int) -> torch.Tensor:
         """All entries of one sequence at one layer, ascending entry order, gathered to [n, *row]."""

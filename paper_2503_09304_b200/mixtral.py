@@ -10,17 +10,19 @@ code, like cuBLAS) on the engine-owned page pool.
 Layer semantics = HF MixtralDecoderLayer / Qwen2MoeDecoderLayer:
   h2 = h + o_proj(attn(rope(q), rope(k), v))          (ATTENTION stage: returns x=norm2(h2), res=h2)
   h' = h2 + sum_j w_j * expert_j(x)  [+ sigmoid(g.x) * shared(x) for Qwen]   (ROUTER + EXPERTS)
+Qwen's shared expert runs inside the grouped expert launch as 4 F-wide sub-experts (moe_block.py).
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 from typing import Optional
 
 import torch
 
 from . import kernels as K
 from .core import Phase, StateCorruptionError
+from .moe_block import pack_shared, shared_sub_experts
 
 
 @dataclass(frozen=True)
@@ -67,7 +69,11 @@ class DecoderMoEModel:
         self.cfg = cfg
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.dtype = dtype
-        self.config = cfg  # engine reads num_layers / hidden_dim / num_experts / top_k / vocab_size
+        # Qwen's shared expert runs as S extra experts of the routed width in the grouped launch
+        # (moe_block.py): the engine sees E + S experts and k + S slots per token
+        S = shared_sub_experts(cfg.shared_ffn_dim, cfg.ffn_dim) if cfg.shared_ffn_dim else 0
+        self.n_shared = S
+        self.config = replace(cfg, num_experts=cfg.num_experts + S, top_k=cfg.top_k + S)  # engine view
         from flash_attn import flash_attn_varlen_func, flash_attn_with_kvcache
 
         self._fa_varlen, self._fa_kvcache = flash_attn_varlen_func, flash_attn_with_kvcache
@@ -86,17 +92,18 @@ class DecoderMoEModel:
             L.ln2 = torch.ones(d, dtype=dtype, device=self.device)
             L.w_qkv = rnd(((H + 2 * KV) * hd, d), d ** -0.5)
             L.w_o = rnd((d, H * hd), (H * hd) ** -0.5)
-            L.w_router = rnd((E, d), d ** -0.5)
-            L.gate_up = torch.empty((E, 2 * F, d), dtype=dtype, device=self.device)
-            L.down = torch.empty((E, d, F), dtype=dtype, device=self.device)
+            L.w_router = torch.empty((E + (1 if S else 0), d), dtype=dtype, device=self.device)
+            L.w_router[:E] = rnd((E, d), d ** -0.5)
+            L.gate_up = torch.empty((E + S, 2 * F, d), dtype=dtype, device=self.device)
+            L.down = torch.empty((E + S, d, F), dtype=dtype, device=self.device)
             for e in range(E):  # per expert to bound the fp32 temporary
                 L.gate_up[e] = rnd((2 * F, d), d ** -0.5)
                 L.down[e] = rnd((d, F), F ** -0.5)
-            if cfg.shared_ffn_dim:
+            if S:
                 Fs = cfg.shared_ffn_dim
-                L.sh_gate_up = rnd((1, 2 * Fs, d), d ** -0.5)
-                L.sh_down = rnd((1, d, Fs), Fs ** -0.5)
-                L.sh_gate = rnd((1, d), d ** -0.5)
+                sh_gate_up = rnd((2 * Fs, d), d ** -0.5)
+                pack_shared(L.gate_up, L.down, E, sh_gate_up[:Fs], sh_gate_up[Fs:], rnd((d, Fs), Fs ** -0.5))
+                L.w_router[E:] = rnd((1, d), d ** -0.5)  # the shared expert's sigmoid gate
             self.layers.append(L)
         self.final_norm = torch.ones(d, dtype=dtype, device=self.device)
         self.lm_head = rnd((cfg.vocab_size, d), d ** -0.5)
@@ -107,7 +114,7 @@ class DecoderMoEModel:
         self._stop = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._meta, self._meta_key = None, None
         self._expect = None  # (handles, members, expected cached entries) of the current pass
-        self._shared_T, self._shared_off, self._shared_ident = -1, None, None
+        self.preempt_guard = None  # set by the engine per iteration (device-preempt mode)
 
     # ------------------------------------------------------------------ cache geometry
     def kv_row_shape(self):
@@ -178,7 +185,9 @@ class DecoderMoEModel:
         q = qkv[:, : H * hd].view(T, H, hd)
         k = qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd)
         v = qkv[:, (H + KV) * hd:].view(T, KV, hd)
-        cache.scatter(layer, meta["slots"], torch.stack([k, v], 1))
+        # guard: the engine's per-iteration preempt flag in device-preempt mode (no append once an
+        # expert launch of this iteration stopped early, see engine._experts_device_preempt)
+        cache.scatter(layer, meta["slots"], torch.stack([k, v], 1), guard=self.preempt_guard)
         if decode:
             pool = cache.pool(layer)
             attn = self._fa_kvcache(q.view(T, 1, H, hd), pool[:, :, 0], pool[:, :, 1], cache_seqlens=meta["lens"],
@@ -190,14 +199,14 @@ class DecoderMoEModel:
         return x_in, h2
 
     def route_batch(self, layer: int, x: torch.Tensor):
-        return K.router(x, self.layers[layer].w_router, self.cfg.top_k, self.cfg.route_mode)
+        return K.router(x, self.layers[layer].w_router, self.cfg.top_k, self.cfg.route_mode, n_shared=self.n_shared)
 
     def new_expert_state(self, T: int):
-        y = torch.empty((T * self.cfg.top_k, self.cfg.hidden_dim), dtype=self.dtype, device=self.device)
+        y = torch.empty((T * self.config.top_k, self.cfg.hidden_dim), dtype=self.dtype, device=self.device)
         return y, torch.zeros(T, dtype=torch.int32, device=self.device)
 
     def permute(self, ids, cursor, x):
-        return K.permute(ids, self.cfg.num_experts, cursor=cursor, x=x)
+        return K.permute(ids, self.config.num_experts, cursor=cursor, x=x)
 
     def run_experts(self, layer: int, xp, offsets, perm, y, e_begin: int, e_end: int, preempt_flag=None,
                     progress=None, progress_seq: int = 0):
@@ -214,24 +223,7 @@ class DecoderMoEModel:
         K.cursor_advance(cursor, stop_dev)
 
     def combine_batch(self, layer: int, y, w, res, x):
-        if self.cfg.shared_ffn_dim:
-            L = self.layers[layer]
-            T = x.shape[0]
-            Fs = self.cfg.shared_ffn_dim
-            # one-expert problem over all T rows; cached per T so no per-layer H2D copy (a pageable
-            # torch.tensor(..., device=cuda) waits for the stream, i.e. for the grouped GEMM)
-            if self._shared_T != T:
-                self._shared_off = torch.arange(0, 2 * T, T, dtype=torch.int32, device=self.device)
-                self._shared_ident = torch.arange(T, dtype=torch.int32, device=self.device)
-                self._shared_T = T
-            offsets, ident = self._shared_off, self._shared_ident
-            ys = torch.empty_like(x)
-            act = K.workspace(T * Fs * 2, "act_shared", self.device).view(self.dtype)[: T * Fs].view(T, Fs)
-            K.expert_ffn(K.EXPERT_SWIGLU, x, offsets, ident, L.sh_gate_up, L.sh_down, ys, act_ws=act)
-            # res + sigmoid(g . x) * shared(x) as a one-slot combine (HF Qwen2MoeSparseMoeBlock)
-            # the gate logit g . x is a one-expert router call (fp32 accumulate, no cuBLAS setup per layer)
-            gate = torch.sigmoid(K.router(x, L.sh_gate, 1, want_logits=True)[2])
-            res = K.combine(ys, gate, res)
+        # routed and (Qwen) shared-expert slots in one weighted sum, residual fused
         return K.combine(y, w, res)
 
     def emit_batch(self, h: torch.Tensor, rows: list[int]) -> list[int]:

@@ -108,6 +108,7 @@ class MoEModel:
         self.b_out = ts(p["b_out"])
         self.side_dtype = side
         self._stop = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.preempt_guard = None  # set by the engine per iteration (device-preempt mode)
 
     # ------------------------------------------------------------------ cache geometry
     def kv_row_shape(self) -> tuple[int, ...]:
@@ -151,7 +152,7 @@ class MoEModel:
                 raise StateCorruptionError(
                     f"sequence {seq.id} layer {layer}: prefill expects an empty layer, found {have} entries")
             slots += cache.reserve(seq.cache_handle, layer, m.n)
-        cache.scatter(layer, slots, kv)
+        cache.scatter(layer, slots, kv, guard=self.preempt_guard)  # guard: engine's device-preempt flag
         out = torch.empty_like(hs)
         decode_ids = {id(m) for m in decode}
         for m in members:

@@ -71,7 +71,7 @@ def record(model: DecoderMoEModel, scheduler: str = "qllm") -> dict:
     finally:
         model.route_batch, model.emit_batch = route_batch, emit_batch
         eng._init_state = init_state
-    cfg = model.cfg
+    cfg = model.config  # the engine's view: Qwen's shared sub-experts count as experts 60..63
     return {
         "scheduler": scheduler, "policy": scheduler, "max_batch_size": MBS,
         # the reference replays with a stub of this shape (d only sizes its toy arrays; costs and
