@@ -184,6 +184,7 @@ class InferenceEngine:
         self._preempt_at = {"ATTENTION": 0, "ROUTER": 0}
         self.stats["reports_at_drain"] = 0
         self._active = None   # the running iteration's preempt flag (device-preempt mode)
+        self.in_rollback = False
         self._flag = None
         self._prev = None     # the previous layer's state within the running iteration
         self._ring_i = 0
@@ -375,8 +376,12 @@ class InferenceEngine:
         done = [e for e in p.hit if e < stop]
         rep = (self._report(batch, Stage.EXPERTS, p.layer, p, expert_id=done[-1]) if done
                else self._report(batch, Stage.ROUTER, p.layer, p))
-        if on_report(rep) is not PREEMPT:
-            self.stats["flag_policy_disagree"] = self.stats.get("flag_policy_disagree", 0) + 1
+        self.in_rollback = True  # the driver admits arrivals up to this report (Simulation._admission_time)
+        try:
+            if on_report(rep) is not PREEMPT:
+                self.stats["flag_policy_disagree"] = self.stats.get("flag_policy_disagree", 0) + 1
+        finally:
+            self.in_rollback = False
         m.advance_cursor(p.cursor, self._stop_dev_ring[p.ring:p.ring + 1])
         self._preempt_at["EXPERT_DEVICE_FLAG"] = self._preempt_at.get("EXPERT_DEVICE_FLAG", 0) + 1
         return self._preempt(p, p.layer, Stage.EXPERTS)

@@ -218,3 +218,30 @@ def test_baseline_fcfs_ignores_priority_and_waits_for_finishers():
     assert b.on_engine_report(report([BE])) is CONT
     with pytest.raises(AdmissionError):
         b.on_preempted({})
+
+
+def test_serving_knob_be_prefill_into_free_slots():
+    """Off (reference Algorithm 1): fresh BE prefills wait behind BE decodes.  On: they run as soon
+    as the decode population leaves batch slots free, capped at the free slots."""
+    for knob in (False, True):
+        s = QllmScheduler(cache(), 4, qllm_policy, be_prefill_into_free_slots=knob)
+        for i in range(2):
+            as_decode(s, i, BE)
+        for i in range(10, 15):
+            arrive(s, i, BE)
+        sel = s.get_next_batch()
+        if knob:
+            assert sel.phase is Phase.PREFILL and sel.seq_ids == [10, 11]
+            assert s.get_next_batch(decode_only=True).seq_ids == [0, 1]  # decode-only never takes prefills
+        else:
+            assert sel.phase is Phase.DECODE and sel.seq_ids == [0, 1]
+
+
+def test_serving_knob_fill_ls_prefill():
+    for fill in (True, False):
+        s = QllmScheduler(cache(), 8, qllm_policy, fill_ls_prefill=fill)
+        arrive(s, 1, BE)
+        arrive(s, 2, LS)
+        arrive(s, 3, BE)
+        sel = s.get_next_batch()
+        assert sel.seq_ids == ([2, 1, 3] if fill else [2])
