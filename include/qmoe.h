@@ -219,6 +219,17 @@ QMOE_API int qmoe_scatter_rows(const void* src, const int32_t* idx, int rows, si
  * read from device memory (the grouped GEMM's cursor_out) so no host sync is needed.
  */
 QMOE_API int qmoe_cursor_advance(int32_t* cursor, int T, const int32_t* stop_expert_dev, void* stream);
+/*
+ * Resume point of a preempted expert stage (replaces the copy-everything checkpoint of
+ * engine.py:401-423 plus the re-enqueue of pending experts at restore, engine.py:151-164,
+ * 312-328): qmoe_cursor_advance, and offsets_out[e] = offsets[max(e, stop)] for e in [0, E] --
+ * the preempted launch's queues with every expert below the stop emptied.  A resumed launch over
+ * the same batch passes offsets_out with the first launch's perm and Xp: the pending slots of
+ * experts >= stop are exactly its rows there, in the same (stable) order, so no re-permute, no
+ * re-gather.  offsets may be NULL (cursor advance only).
+ */
+QMOE_API int qmoe_resume_point(int32_t* cursor, int T, const int32_t* stop_expert_dev, const int32_t* offsets, int E,
+                               int32_t* offsets_out, void* stream);
 
 /*
  * Paged KV ownership (replaces UnifiedDynamicCache storage, model.py:231-329).

@@ -65,6 +65,7 @@ SIGNATURES = {
     "qmoe_gather_rows": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),
     "qmoe_scatter_rows": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),
     "qmoe_cursor_advance": (_c_int, [_vp, _c_int, _vp, _vp]),
+    "qmoe_resume_point": (_c_int, [_vp, _c_int, _vp, _vp, _c_int, _vp, _vp]),
     "qmoe_kv_append": (_c_int, [_vp, _vp, _vp, _c_int, _c_size, _vp]),
     "qmoe_kv_append_guarded": (_c_int, [_vp, _vp, _vp, _c_int, _c_size, _vp, _vp]),
     "qmoe_kv_gather": (_c_int, [_vp, _vp, _c_int, _c_size, _vp, _vp]),

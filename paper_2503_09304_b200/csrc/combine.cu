@@ -129,6 +129,18 @@ __global__ void cursor_advance_kernel(int32_t* cursor, int ntok, const int32_t* 
   }
 }
 
+// Preemption at an expert boundary: cursors advance to the stop (as cursor_advance_kernel) and the
+// launch's queue offsets are rewritten so experts below the stop are empty: out[e] = in[max(e,
+// stop)].  The resumed launch then reuses the first launch's perm / Xp (a stable sort of the
+// pending slots gives the same per-expert order), so a resume needs no re-permute.
+__global__ void resume_point_kernel(int32_t* cursor, int ntok, const int32_t* stop, const int32_t* offsets, int E,
+                                    int32_t* offsets_out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = *stop;
+  if (t < ntok && cursor[t] < s) cursor[t] = s;
+  if (offsets != nullptr && t <= E) offsets_out[t] = offsets[t < s ? s : t];
+}
+
 int launch_rows(const void* src, const int32_t* idx, int rows, size_t row_bytes, void* dst, int scatter,
                 cudaStream_t s, const char* what, const int32_t* guard = nullptr) {
   QMOE_REQUIRE(rows >= 0 && row_bytes > 0, "%s: bad sizes", what);
@@ -221,6 +233,18 @@ extern "C" int qmoe_cursor_advance(int32_t* cursor, int T, const int32_t* stop_e
   QMOE_REQUIRE(cursor && stop_expert_dev, "qmoe_cursor_advance: null pointer");
   cursor_advance_kernel<<<(T + 255) / 256, 256, 0, as_stream(stream)>>>(cursor, T, stop_expert_dev);
   return check_launch("qmoe_cursor_advance");
+}
+
+extern "C" int qmoe_resume_point(int32_t* cursor, int T, const int32_t* stop_expert_dev, const int32_t* offsets, int E,
+                                 int32_t* offsets_out, void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(T >= 0 && E >= 1 && E <= 64, "qmoe_resume_point: bad sizes T=%d E=%d", T, E);
+  QMOE_REQUIRE(stop_expert_dev && (T == 0 || cursor) && (offsets == nullptr || offsets_out),
+               "qmoe_resume_point: null pointer");
+  const int n = T > E + 1 ? T : E + 1;
+  resume_point_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(cursor, T, stop_expert_dev, offsets, E,
+                                                                       offsets_out);
+  return check_launch("qmoe_resume_point");
 }
 
 extern "C" int qmoe_kv_append(void* pool, const int32_t* slot_mapping, const void* rows, int n_rows,

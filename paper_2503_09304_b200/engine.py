@@ -153,6 +153,8 @@ class _State:
     y: object = None
     cursor: object = None
     progress: tuple = ()     # MemberProgress of every member (constant within one execute)
+    q: object = None         # (perm, offsets, xp) of the current expert launch
+    resume_q: object = None  # queues a preempted expert stage resumes with (qmoe_resume_point)
 
 
 class InferenceEngine:
@@ -264,8 +266,15 @@ class InferenceEngine:
                     return self._preempt(st, layer, Stage.EXPERTS)
                 stage = Stage.EXPERTS
 
-            # EXPERTS: queue build for the pending slots, boundary decisions, one grouped launch.
-            perm, offsets, xp = m.permute(st.ids, st.cursor, st.x)
+            # EXPERTS: queue build for the pending slots (or, resuming a whole preempted batch, the
+            # preempted launch's queues with the completed experts emptied), boundary decisions,
+            # one grouped launch.
+            if st.resume_q is not None:
+                perm, offsets, xp = st.resume_q
+                st.resume_q = None
+            else:
+                perm, offsets, xp = m.permute(st.ids, st.cursor, st.x)
+            st.q = (perm, offsets, xp)
             if dev:
                 stop_dev, preempted = self._experts_device_preempt(batch, st, layer, perm, offsets, xp, on_report)
                 if preempted is None:  # the previous layer's launch was stopped by the device flag
@@ -273,13 +282,15 @@ class InferenceEngine:
             else:
                 stop_dev, preempted = self._experts_host_boundary(batch, st, layer, perm, offsets, xp, on_report)
             if preempted:
-                m.advance_cursor(st.cursor, stop_dev)
+                self._resume_point(st, stop_dev)
                 return self._preempt(st, layer, Stage.EXPERTS)
             st.h = m.combine_batch(layer, st.y, st.w, st.res, st.x)
             if dev:
                 self._prev = _State(st.seqs, st.members, st.T, None, st.x, st.res, st.ids, st.w, st.y, st.cursor,
                                     st.progress)
                 self._prev.layer, self._prev.ring, self._prev.hit = layer, self._ring_i, self._last_hit
+                self._prev.q = st.q
+            st.q = None
             st.x = st.res = st.ids = st.w = st.y = st.cursor = None
             layer += 1
             stage = Stage.ATTENTION
@@ -382,7 +393,7 @@ class InferenceEngine:
                 self.stats["flag_policy_disagree"] = self.stats.get("flag_policy_disagree", 0) + 1
         finally:
             self.in_rollback = False
-        m.advance_cursor(p.cursor, self._stop_dev_ring[p.ring:p.ring + 1])
+        self._resume_point(p, self._stop_dev_ring[p.ring:p.ring + 1])
         self._preempt_at["EXPERT_DEVICE_FLAG"] = self._preempt_at.get("EXPERT_DEVICE_FLAG", 0) + 1
         return self._preempt(p, p.layer, Stage.EXPERTS)
 
@@ -490,6 +501,18 @@ class InferenceEngine:
             return stop_dev, True
         return stop_dev, False
 
+    def _resume_point(self, st: _State, stop_dev) -> None:
+        """Cursors advance to the stop on the device.  With a model exposing resume_point, the
+        preempted launch's perm / Xp are kept with the completed experts' queues emptied, so a
+        restore of the whole batch resumes without a re-permute (engine.py:312-328 re-enqueues
+        only pending experts; the pending slots of each expert are the same rows, same order)."""
+        rp = getattr(self.model, "resume_point", None)
+        if rp is None or st.q is None:
+            self.model.advance_cursor(st.cursor, stop_dev)
+            return
+        perm, offsets, xp = st.q
+        st.resume_q = (perm, rp(st.cursor, stop_dev, offsets), xp)
+
     def _await_progress(self, prog, e: int, seq: int, timeout_s: float = 30.0) -> None:
         """Spin on the pinned progress word of expert e (a plain host read, ~100 ns)."""
         if prog[e] == seq:
@@ -543,6 +566,10 @@ class InferenceEngine:
         if ckpts[0].ids is not None:
             st.ids, st.w = self._gather(ckpts, "ids"), self._gather(ckpts, "weights")
             st.y, st.cursor = self._gather(ckpts, "y"), self._gather(ckpts, "cursor")
+            o = ckpts[0].origin if self._contiguous(ckpts) else None
+            if o is not None and o[1] == 0 and ckpts[-1].origin[2] == o[0].T and o[0].resume_q is not None:
+                st.resume_q = o[0].resume_q  # the whole preempted batch, in its order: reuse its queues
+                self.stats["queue_reuse_resumes"] = self.stats.get("queue_reuse_resumes", 0) + 1
         self.stats["zero_copy_restores" if self._contiguous(ckpts) else "copy_restores"] += 1
         for s in sequences:
             s.checkpoint = None  # checkpoints live only while preempted

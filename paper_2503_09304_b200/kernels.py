@@ -229,6 +229,19 @@ def permute_launches(T: int, k: int, gather: bool = True) -> int:
     return (1 if nblk > 1 else 0) + 1 + (1 if gather and S > 32 else 0)
 
 
+def resume_point(cursor: torch.Tensor, stop_dev: torch.Tensor, offsets: torch.Tensor) -> torch.Tensor:
+    """Advance the cursors to the stop and return the resumed launch's offsets (experts below the
+    stop emptied); the launch reuses the preempted launch's perm and Xp."""
+    _need(cursor, "cursor", torch.int32)
+    _need(stop_dev, "stop", torch.int32)
+    _need(offsets, "offsets", torch.int32)
+    out = torch.empty_like(offsets)
+    lib = _lib.load()
+    check(lib.qmoe_resume_point(_ptr(cursor), cursor.shape[0], _ptr(stop_dev), _ptr(offsets), offsets.shape[0] - 1,
+                                _ptr(out), _stream()), "qmoe_resume_point")
+    return out
+
+
 def cursor_advance(cursor: torch.Tensor, stop_dev: torch.Tensor) -> None:
     _need(cursor, "cursor", torch.int32)
     _need(stop_dev, "stop", torch.int32)

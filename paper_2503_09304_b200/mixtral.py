@@ -222,6 +222,9 @@ class DecoderMoEModel:
     def advance_cursor(self, cursor, stop_dev):
         K.cursor_advance(cursor, stop_dev)
 
+    def resume_point(self, cursor, stop_dev, offsets):
+        return K.resume_point(cursor, stop_dev, offsets)
+
     def combine_batch(self, layer: int, y, w, res, x):
         # routed and (Qwen) shared-expert slots in one weighted sum, residual fused
         return K.combine(y, w, res)

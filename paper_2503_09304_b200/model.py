@@ -209,6 +209,9 @@ class MoEModel:
     def advance_cursor(self, cursor: torch.Tensor, stop_dev: torch.Tensor) -> None:
         K.cursor_advance(cursor, stop_dev)
 
+    def resume_point(self, cursor: torch.Tensor, stop_dev: torch.Tensor, offsets: torch.Tensor) -> torch.Tensor:
+        return K.resume_point(cursor, stop_dev, offsets)
+
     def combine_batch(self, layer: int, y, w, res, x) -> torch.Tensor:
         return K.combine(y, w, res)
 

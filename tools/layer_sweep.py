@@ -13,7 +13,10 @@ from paper_2503_09304_b200 import kernels as K
 
 PEAKS = json.load(open("MEASURED_PEAKS.json")) if __import__("os").path.exists("MEASURED_PEAKS.json") else {
     "hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
-SHAPES = {"mixtral": (4096, 14336, 8, 2, K.ROUTE_TOPK_SOFTMAX), "qwen": (2048, 1408, 60, 4, K.ROUTE_SOFTMAX_TOPK)}
+# (d, F, E, k, routing, shared sub-experts): Qwen's shared expert (5632 = 4 x 1408) runs inside the
+# grouped launch as 4 extra experts every token is routed to (moe_block.py)
+SHAPES = {"mixtral": (4096, 14336, 8, 2, K.ROUTE_TOPK_SOFTMAX, 0),
+          "qwen": (2048, 1408, 60, 4, K.ROUTE_SOFTMAX_TOPK, 4)}
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
 
@@ -31,9 +34,13 @@ def timed(fn, reps):
 
 def main():
     out = []
-    for name, (d, F, E, k, mode) in SHAPES.items():
+    only = sys.argv[1] if len(sys.argv) > 1 else None
+    for name, (d, F, E0, k0, mode, S) in SHAPES.items():
+        if only and name != only:
+            continue
         g = torch.Generator(device="cuda").manual_seed(0)
-        wr = (torch.randn((E, d), device="cuda", generator=g) * d ** -0.5).bfloat16()
+        E, k = E0 + S, k0 + S  # experts / slots per token as the grouped launch sees them
+        wr = (torch.randn((E0 + (1 if S else 0), d), device="cuda", generator=g) * d ** -0.5).bfloat16()
         gu = (torch.randn((E, 2 * F, d), device="cuda", generator=g) * d ** -0.5).bfloat16()
         dn = (torch.randn((E, d, F), device="cuda", generator=g) * F ** -0.5).bfloat16()
         for T in [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384]:
@@ -42,24 +49,26 @@ def main():
             y = torch.empty((T * k, d), dtype=torch.bfloat16, device="cuda")
 
             def layer():
-                ids, w = K.router(x, wr, k, mode)
+                ids, w = K.router(x, wr, k0, mode, n_shared=S)
                 perm, offsets, xp = K.permute(ids, E, x=x)
                 K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act)
                 K.combine(y, w, x)
 
-            ids, w = K.router(x, wr, k, mode)
+            ids, w = K.router(x, wr, k0, mode, n_shared=S)
             _, offsets, _ = K.permute(ids, E, x=x)
             off = offsets.tolist()
             hit = [e for e in range(E) if off[e + 1] > off[e]]
 
             def preempt_every_boundary():
+                # the engine's whole-batch resume: the preempted launch's queues are kept and
+                # qmoe_resume_point empties the completed experts (no re-permute / re-gather)
                 cursor = torch.zeros(T, dtype=torch.int32, device="cuda")
                 stop = torch.zeros(1, dtype=torch.int32, device="cuda")
-                for e in hit:  # resume: re-permute pending slots, run exactly one more expert
-                    perm, offs, xp = K.permute(ids, E, cursor=cursor, x=x)
+                perm, offs, xp = K.permute(ids, E, cursor=cursor, x=x)
+                for e in hit:  # run exactly one more expert, then preempt
                     K.expert_ffn(K.EXPERT_SWIGLU, xp, offs, perm, gu, dn, y, e_begin=0, e_end=e + 1, act_ws=act,
                                  cursor_out=stop)
-                    K.cursor_advance(cursor, stop)
+                    offs = K.resume_point(cursor, stop, offs)
                 K.combine(y, w, x)
 
             reps = 10 if T >= 4096 else 20
@@ -69,6 +78,7 @@ def main():
             wbytes = len(hit) * 3 * d * F * 2
             rec = {"shape": name, "T": T, "ms": t, "tflops": flops / t / 1e9,
                    "tensor_frac_sustained": flops / t / 1e9 / PEAKS["bf16_tflops_sustained"],
+                   "tensor_frac_burst": flops / t / 1e9 / PEAKS["bf16_tflops"],
                    "weight_gbs": wbytes / t / 1e6, "hbm_frac": wbytes / t / 1e6 / PEAKS["hbm_gbs"],
                    "experts_hit": len(hit), "preempt_every_boundary_ms": tp, "preempt_overhead_x": tp / t}
             out.append(rec)
@@ -76,7 +86,6 @@ def main():
         del gu, dn
         torch.cuda.empty_cache()
     # LS fraction only changes co-batch member order (LS first): same work, measured once
-    d, F, E, k, mode = SHAPES["mixtral"]
     print(json.dumps({"note": "ls_fraction changes only the member order of the batch rows; the queue build is "
                               "order-agnostic in cost (stable counting sort), so the T sweep above applies to "
                               "every LS fraction"}), flush=True)
