@@ -445,6 +445,137 @@ int launch_router_mma(const void* x, const void* wr, int T_, int d, int E, int k
              : launch_router_mma_np<4, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
 }
 
+// ---- bf16, many tokens: register-streamed logits ------------------------------------------------
+// The router reads X once (T x d bf16) and does E MACs per element: HBM-bound.  Here nothing is
+// staged through shared memory and there is no barrier in the main loop: every lane streams its
+// rows of X from HBM with 16-byte loads straight into mma.sync A fragments.  That works because a
+// dot product may permute k freely as long as A and B use the same permutation: lane (g, t) loads
+// X[row g][8t .. 8t+7] and X[row g+8][8t .. 8t+7] of a 32-wide k step and W[expert g][8t .. 8t+7]
+// from L1/L2, and hands words 0-1 to one m16n8k16 and words 2-3 to a second -- logical k (2t,
+// 2t+1, 2t+8, 2t+9) of each MMA is physical k (8t .. 8t+3) resp. (8t+4 .. 8t+7) for A and B
+// alike.  A CTA owns 16 tokens; its DS x NQ warps split d into DS slices and the experts into NQ
+// groups of NTW n8 tiles (NQ warps re-read the same X rows from L1).  U k-steps of loads are in
+// flight per warp before any MMA.  The DS partial logits are summed in slice order (fixed,
+// deterministic), then the selection is the SIMT kernel's.  16-token CTAs of 4-8 warps put
+// ~2-4k warps in flight at 8k tokens.
+// 16-byte read-only load as a volatile asm statement: the compiler keeps all U steps' loads ahead
+// of the (also volatile) MMAs instead of interleaving them into a short software pipeline.
+// NOALLOC: X rows no other warp reads again (NQ == 1) bypass L1 so W_router stays resident.
+template <bool NOALLOC>
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  if constexpr (NOALLOC)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  else
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+template <int DS, int NQ, int NTW, int U>
+__global__ void __launch_bounds__(DS * NQ * 32)
+router_stream_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr, int ntok, int d,
+                     int E, int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
+                     float* __restrict__ logits_out) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int kWarps = DS * NQ;
+  constexpr int kCols = 8 * NTW * NQ;  // experts covered (padded)
+  __shared__ float s_part[DS][16][kCols];
+  __shared__ float s_logit[16][kMaxE];
+  __shared__ float s_score[16][kMaxE];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int slice = warp / NQ, grp = warp % NQ;
+  const int tok0 = blockIdx.x * 16;
+  const int dq = d / DS, k0 = slice * dq;
+  const uint4* xr0 = reinterpret_cast<const uint4*>(x + (size_t)min(tok0 + g, ntok - 1) * d + k0) + t4;
+  const uint4* xr1 = reinterpret_cast<const uint4*>(x + (size_t)min(tok0 + g + 8, ntok - 1) * d + k0) + t4;
+  const uint4* wp[NTW];
+#pragma unroll
+  for (int j = 0; j < NTW; ++j)
+    wp[j] = reinterpret_cast<const uint4*>(wr + (size_t)min(8 * (grp * NTW + j) + g, E - 1) * d + k0) + t4;
+  float acc[NTW][4];
+#pragma unroll
+  for (int j = 0; j < NTW; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  const int nsteps = dq / 32;  // 32-wide k steps (4 x uint4 per row)
+  for (int s0 = 0; s0 < nsteps; s0 += U) {
+    uint4 a0[U], a1[U], b[U][NTW];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a0[u] = ld_stream<NQ == 1>(xr0 + 4 * (s0 + u));
+      a1[u] = ld_stream<NQ == 1>(xr1 + 4 * (s0 + u));
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) b[u][j] = ld_stream<false>(wp[j] + 4 * (s0 + u));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) {
+        mma_bf16_16816(acc[j], a0[u].x, a1[u].x, a0[u].y, a1[u].y, b[u][j].x, b[u][j].y);
+        mma_bf16_16816(acc[j], a0[u].z, a1[u].z, a0[u].w, a1[u].w, b[u][j].z, b[u][j].w);
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < NTW; ++j) {
+    const int c = 8 * (grp * NTW + j) + 2 * t4;
+    s_part[slice][g][c] = acc[j][0];
+    s_part[slice][g][c + 1] = acc[j][1];
+    s_part[slice][g + 8][c] = acc[j][2];
+    s_part[slice][g + 8][c + 1] = acc[j][3];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 16 * kCols; i += kWarps * 32) {
+    const int t = i / kCols, e = i - t * kCols;
+    float v = s_part[0][t][e];
+#pragma unroll
+    for (int sl = 1; sl < DS; ++sl) v += s_part[sl][t][e];
+    s_logit[t][e] = v;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int ti = warp; ti < 16; ti += kWarps) {
+    const int tok = tok0 + ti;
+    if (tok >= ntok) break;
+    select_token<float>(s_logit[ti], s_score[ti], tok, E, k, mode, lane, ids_out, w_out, logits_out);
+  }
+}
+
+template <int DS, int NQ, int NTW, int U>
+int launch_router_stream(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
+                         void* logits, cudaStream_t s) {
+  return launch_pdl("qmoe_router(stream)", router_stream_kernel<DS, NQ, NTW, U>, dim3((T_ + 15) / 16),
+                    dim3(DS * NQ * 32), 0, s, (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode,
+                    ids, (float*)w, (float*)logits);
+}
+
+// 0 = not applicable (shape), else launched.  QMOE_ROUTER_STREAM=0 keeps the cp.async kernel.
+int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
+                      void* logits, cudaStream_t s, int* st) {
+  static const int env = [] {
+    const char* v = getenv("QMOE_ROUTER_STREAM");
+    return v == nullptr ? 1 : atoi(v);
+  }();
+  if (!env) return 0;
+  if (E <= 8 && d % (4 * 32 * 8) == 0) {
+    *st = launch_router_stream<4, 1, 1, 8>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+    return 1;
+  }
+  if (E <= 16 && d % (4 * 32 * 8) == 0) {
+    *st = launch_router_stream<4, 1, 2, 8>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+    return 1;
+  }
+  if (E <= 32 && d % (2 * 32 * 4) == 0) {
+    *st = launch_router_stream<2, 2, 2, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+    return 1;
+  }
+  if (d % (2 * 32 * 4) == 0) {
+    *st = launch_router_stream<2, 4, 2, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+    return 1;
+  }
+  return 0;
+}
+
 // Few tokens (decode): one token per CTA, all 8 warps on it.  Many tokens: warps own tokens (2
 // each) when the experts fit one or two 8-expert chunks, else 4 tokens share the 8 warps.
 template <typename T>
@@ -453,8 +584,11 @@ int dispatch_router(const void* x, const void* wr, int T_, int d, int E, int k, 
   const int nchunk = (E + kExpChunk - 1) / kExpChunk;
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
     if (T_ >= 256 && d % kMmaK == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
-        reinterpret_cast<uintptr_t>(wr) % 16 == 0)
+        reinterpret_cast<uintptr_t>(wr) % 16 == 0) {
+      int st = QMOE_OK;
+      if (try_router_stream(x, wr, T_, d, E, k, mode, ids, w, logits, s, &st)) return st;
       return launch_router_mma(x, wr, T_, d, E, k, mode, ids, w, logits, s);
+    }
   }
   // decode: 16 warps on one token halve the dependent load rounds over d (Qwen: 8 chunks x 2 slices)
   if (T_ < 148 * 8) return launch_router<T, 1, 1, 16>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
