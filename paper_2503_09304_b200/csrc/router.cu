@@ -498,23 +498,38 @@ router_stream_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* _
   float acc[NTW][4];
 #pragma unroll
   for (int j = 0; j < NTW; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-  const int nsteps = dq / 32;  // 32-wide k steps (4 x uint4 per row)
-  for (int s0 = 0; s0 < nsteps; s0 += U) {
-    uint4 a0[U], a1[U], b[U][NTW];
+  const int nsteps = dq / 32;  // 32-wide k steps (4 x uint4 per row); a multiple of U
+  // two register buffers of U k-steps: the loads of batch n+1 are issued before the MMAs of batch
+  // n, so 2U steps of X are in flight per warp
+  uint4 a0[2][U], a1[2][U], b[2][U][NTW];
+  auto load = [&](int buf, int s0) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      a0[u] = ld_stream<NQ == 1>(xr0 + 4 * (s0 + u));
-      a1[u] = ld_stream<NQ == 1>(xr1 + 4 * (s0 + u));
+      a0[buf][u] = ld_stream<NQ == 1>(xr0 + 4 * (s0 + u));
+      a1[buf][u] = ld_stream<NQ == 1>(xr1 + 4 * (s0 + u));
 #pragma unroll
-      for (int j = 0; j < NTW; ++j) b[u][j] = ld_stream<false>(wp[j] + 4 * (s0 + u));
+      for (int j = 0; j < NTW; ++j) b[buf][u][j] = ld_stream<false>(wp[j] + 4 * (s0 + u));
     }
+  };
+  auto mma = [&](int buf) {
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int j = 0; j < NTW; ++j) {
-        mma_bf16_16816(acc[j], a0[u].x, a1[u].x, a0[u].y, a1[u].y, b[u][j].x, b[u][j].y);
-        mma_bf16_16816(acc[j], a0[u].z, a1[u].z, a0[u].w, a1[u].w, b[u][j].z, b[u][j].w);
+        mma_bf16_16816(acc[j], a0[buf][u].x, a1[buf][u].x, a0[buf][u].y, a1[buf][u].y, b[buf][u][j].x,
+                       b[buf][u][j].y);
+        mma_bf16_16816(acc[j], a0[buf][u].z, a1[buf][u].z, a0[buf][u].w, a1[buf][u].w, b[buf][u][j].z,
+                       b[buf][u][j].w);
       }
+  };
+  load(0, 0);
+  for (int s0 = 0; s0 < nsteps; s0 += 2 * U) {
+    if (s0 + U < nsteps) load(1, s0 + U);
+    mma(0);
+    if (s0 + U < nsteps) {
+      if (s0 + 2 * U < nsteps) load(0, s0 + 2 * U);
+      mma(1);
+    }
   }
 #pragma unroll
   for (int j = 0; j < NTW; ++j) {
@@ -556,23 +571,30 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
     const char* v = getenv("QMOE_ROUTER_STREAM");
     return v == nullptr ? 1 : atoi(v);
   }();
+  static const int cfg = [] {  // QMOE_ROUTER_CFG: tiling variant (measurement sweeps)
+    const char* v = getenv("QMOE_ROUTER_CFG");
+    return v == nullptr ? 0 : atoi(v);
+  }();
   if (!env) return 0;
-  if (E <= 8 && d % (4 * 32 * 8) == 0) {
-    *st = launch_router_stream<4, 1, 1, 8>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
-    return 1;
+#define QMOE_TRY_STREAM(DS, NQ, NTW, U)                                                       \
+  if (d % ((DS) * 32 * (U)) == 0) {                                                          \
+    *st = launch_router_stream<DS, NQ, NTW, U>(x, wr, T_, d, E, k, mode, ids, w, logits, s); \
+    return 1;                                                                                \
   }
-  if (E <= 16 && d % (4 * 32 * 8) == 0) {
-    *st = launch_router_stream<4, 1, 2, 8>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
-    return 1;
+  if (E <= 8) {
+    if (cfg == 1) { QMOE_TRY_STREAM(4, 1, 1, 8) }
+    if (cfg == 2) { QMOE_TRY_STREAM(16, 1, 1, 2) }
+    QMOE_TRY_STREAM(8, 1, 1, 4)
+  } else if (E <= 16) {
+    QMOE_TRY_STREAM(8, 1, 2, 4)
+  } else if (E <= 32) {
+    QMOE_TRY_STREAM(4, 2, 2, 4)
+  } else {
+    if (cfg == 1) { QMOE_TRY_STREAM(2, 4, 2, 4) }
+    if (cfg == 2) { QMOE_TRY_STREAM(2, 8, 1, 4) }
+    QMOE_TRY_STREAM(4, 4, 2, 2)
   }
-  if (E <= 32 && d % (2 * 32 * 4) == 0) {
-    *st = launch_router_stream<2, 2, 2, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
-    return 1;
-  }
-  if (d % (2 * 32 * 4) == 0) {
-    *st = launch_router_stream<2, 4, 2, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
-    return 1;
-  }
+#undef QMOE_TRY_STREAM
   return 0;
 }
 
