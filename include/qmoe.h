@@ -305,6 +305,18 @@ QMOE_API int qmoe_rmsnorm(const void* x, const void* residual_add, const void* w
 QMOE_API int qmoe_rope(void* q, void* k, const int64_t* positions, const float* cos_table, const float* sin_table,
                        int T, int n_heads, int n_kv_heads, int head_dim, int q_stride, int k_stride, void* stream);
 
+/*
+ * Greedy emission on the device (replaces MoEModel.emit_token, model.py:166-169, for the bf16
+ * decoders): tokens_out[t] = argmax_v (w_out[v] . h[t]), lowest id on ties (numpy's first
+ * maximum), fp32 accumulation; the [T, V] logits are never written.  h: [T, d] bf16 (final-normed
+ * hidden rows), w_out: [V, d] bf16.  T <= 64, d % 128 == 0.  workspace:
+ * qmoe_lm_head_argmax_workspace_bytes() bytes of device memory, ZEROED once at allocation (each
+ * launch leaves it zeroed).  One launch; launches sharing a workspace must be stream-ordered.
+ */
+QMOE_API size_t qmoe_lm_head_argmax_workspace_bytes(void);
+QMOE_API int qmoe_lm_head_argmax(const void* h, const void* w_out, int T, int d, int V, int32_t* tokens_out,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -126,6 +126,134 @@ def b200_cost_model(model, cost_model: CostModel = CostModel(), repeats: int = 5
     return cost_model.scaled(scale), {"wall_ms": wall_ms, "wall_ms_all": wall, "virtual_ms": virt, "scale": scale}
 
 
+# ---------------------------------------------------------------------------------------------
+# Per-stage fit: every CostModel term from measured B200 stage times (reference engine.py:48-88
+# charges attention a0 + a1*tokens + a2*cached, router r0, each non-empty expert e0 + e1*entries,
+# checkpoint c0 per preemption, restore c1 per member).
+
+def fit_cost_model(samples: dict) -> tuple[CostModel, dict]:
+    """Non-negative least squares of each stage's linear form on measured samples (ms):
+      attention: [(tokens, cached_entries, ms)]        -> attn_base, attn_per_token, attn_per_cached
+      router:    [ms]                                  -> router_cost (median)
+      experts:   [(non_empty_experts, entries, ms)]    -> expert_base, expert_per_entry
+                 (one grouped launch covers all experts of a layer, so its time is fitted as
+                 n_experts * e0 + entries * e1: the reference's per-expert charges summed)
+      checkpoint: [ms per preemption], restore: [ms per member]  -> medians
+    Returns (CostModel, fit report with R^2 and the worst relative error per stage)."""
+    from scipy.optimize import nnls
+
+    rep = {}
+
+    def lin(rows, names):
+        a = np.array([r[:-1] for r in rows], dtype=np.float64)
+        y = np.array([r[-1] for r in rows], dtype=np.float64)
+        coef, _ = nnls(a, y)
+        pred = a @ coef
+        ss = float(((y - y.mean()) ** 2).sum())
+        rep[names[0]] = {"n": len(rows), "r2": 1.0 - float(((y - pred) ** 2).sum()) / ss if ss > 0 else 1.0,
+                         "max_rel_err": float(np.max(np.abs(pred - y) / np.maximum(y, 1e-9))),
+                         "coef": dict(zip(names, coef.tolist()))}
+        return coef
+
+    att = lin([(1.0, t, c, ms) for t, c, ms in samples["attention"]], ["attn_base", "attn_per_token", "attn_per_cached"])
+    exp = lin([(n, e, ms) for n, e, ms in samples["experts"]], ["expert_base", "expert_per_entry"])
+    med = lambda v: float(statistics.median(v)) if v else 0.0  # noqa: E731
+    cm = CostModel(attn_base=float(att[0]), attn_per_token=float(att[1]), attn_per_cached=float(att[2]),
+                   router_cost=med(samples["router"]), expert_base=float(exp[0]), expert_per_entry=float(exp[1]),
+                   checkpoint_cost=med(samples.get("checkpoint", [])), restore_cost=med(samples.get("restore", [])))
+    rep["router"] = {"n": len(samples["router"]), "median_ms": cm.router_cost}
+    return cm, rep
+
+
+def measure_stage_samples(model, trace, max_batch_size: int = 32, scheduler: str = "qllm") -> dict:
+    """Run `trace` through the engine on a virtual clock (host-boundary expert stage: the host
+    reads each layer's queue lengths, so the device is idle between stages) with CUDA events around
+    every stage of `model`; returns the samples fit_cost_model takes.  Checkpoint / restore are
+    the host time of the engine's _preempt and the device time of the restore gather."""
+    import time as _time
+
+    from .sim import Simulation
+
+    sim = Simulation(trace, model=model, scheduler=scheduler, max_batch_size=max_batch_size)
+    eng = sim.engine
+    out = {"attention": [], "router": [], "experts": [], "checkpoint": [], "restore": []}
+    pending = []  # (kind, start event, end event, extra) resolved after the run
+
+    def timed(kind, fn, extra):
+        def wrap(*a, **kw):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            r = fn(*a, **kw)
+            e.record()
+            pending.append((kind, s, e, extra(a, r)))
+            return r
+        return wrap
+
+    cache = sim.cache
+    att, route, perm, run, comb = (model.attention_batch, model.route_batch, model.permute, model.run_experts,
+                                   model.combine_batch)
+    model.attention_batch = timed("attention", att, lambda a, r: (
+        sum(m.n for m in a[2]), sum(cache.count(m.seq.cache_handle, a[0]) for m in a[2])))
+    model.route_batch = timed("router", route, lambda a, r: None)
+    state = {}
+
+    def perm_hook(*a, **kw):
+        s = torch.cuda.Event(enable_timing=True)
+        s.record()
+        r = perm(*a, **kw)
+        state["start"] = s
+        state["offsets"] = r[1]
+        return r
+
+    def comb_hook(*a, **kw):
+        r = comb(*a, **kw)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        off = state["offsets"].tolist()
+        counts = [off[i + 1] - off[i] for i in range(len(off) - 1)]
+        pending.append(("experts", state["start"], e, (sum(1 for c in counts if c), sum(counts))))
+        return r
+
+    model.permute, model.combine_batch = perm_hook, comb_hook
+    pre, init = eng._preempt, eng._init_state
+
+    def pre_hook(*a, **kw):
+        t = _time.perf_counter()
+        r = pre(*a, **kw)
+        out["checkpoint"].append((_time.perf_counter() - t) * 1e3)
+        return r
+
+    def init_hook(seqs):
+        resumed = seqs[0].checkpoint is not None
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        r = init(seqs)
+        e.record()
+        if resumed:
+            pending.append(("restore", s, e, len(seqs)))
+        return r
+
+    eng._preempt, eng._init_state = pre_hook, init_hook
+    try:
+        sim.run()
+    finally:
+        model.attention_batch, model.route_batch, model.permute, model.run_experts, model.combine_batch = (
+            att, route, perm, run, comb)
+        eng._preempt, eng._init_state = pre, init
+    torch.cuda.synchronize()
+    for kind, s, e, extra in pending:
+        ms = s.elapsed_time(e)
+        if kind == "attention":
+            out["attention"].append((extra[0], extra[1], ms))
+        elif kind == "router":
+            out["router"].append(ms)
+        elif kind == "experts":
+            out["experts"].append((extra[0], extra[1], ms))
+        else:
+            out["restore"].append(ms / max(1, extra))
+    return out
+
+
 def main(argv=None) -> int:
     """python -m paper_2503_09304_b200.calibrate [--model mixtral|qwen] [--repeats N] [--out F]:
     the B200-calibrated CostModel of a random-init bf16 decoder (JSON)."""

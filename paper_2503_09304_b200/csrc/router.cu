@@ -581,9 +581,14 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
     *st = launch_router_stream<DS, NQ, NTW, U>(x, wr, T_, d, E, k, mode, ids, w, logits, s); \
     return 1;                                                                                \
   }
+  // Measured on B200 (tools/router_ab.py, L2 flushed): Mixtral 1-2k tokens 12 us (16 d-slices:
+  // 8 k-steps per warp, one round trip) vs 18 on the cp.async kernel, 8k/16k tokens 27/46 us vs
+  // 35/59 (8 slices).  Qwen's 61 logit rows: 4 expert groups re-read X from L1 and W from L2 per
+  // 16 tokens -- faster up to 2k tokens (17 vs 23 us), slower from 8k (51 vs 39 us), where the
+  // cp.async kernel's 32-token tiles halve the W re-reads.
   if (E <= 8) {
     if (cfg == 1) { QMOE_TRY_STREAM(4, 1, 1, 8) }
-    if (cfg == 2) { QMOE_TRY_STREAM(16, 1, 1, 2) }
+    if (cfg == 2 || (cfg == 0 && T_ < 4096)) { QMOE_TRY_STREAM(16, 1, 1, 2) }
     QMOE_TRY_STREAM(8, 1, 1, 4)
   } else if (E <= 16) {
     QMOE_TRY_STREAM(8, 1, 2, 4)
@@ -592,7 +597,7 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
   } else {
     if (cfg == 1) { QMOE_TRY_STREAM(2, 4, 2, 4) }
     if (cfg == 2) { QMOE_TRY_STREAM(2, 8, 1, 4) }
-    QMOE_TRY_STREAM(4, 4, 2, 2)
+    if (T_ < 4096) { QMOE_TRY_STREAM(4, 4, 2, 2) }
   }
 #undef QMOE_TRY_STREAM
   return 0;

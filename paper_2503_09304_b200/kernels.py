@@ -229,6 +229,25 @@ def permute_launches(T: int, k: int, gather: bool = True) -> int:
     return (1 if nblk > 1 else 0) + 1 + (1 if gather and S > 32 else 0)
 
 
+def lm_head_argmax(h: torch.Tensor, w_out: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Greedy tokens [T] int32 on the device: argmax_v(w_out[v] . h[t]), lowest id on ties."""
+    _need(h, "h", torch.bfloat16)
+    _need(w_out, "w_out", torch.bfloat16)
+    T, d = h.shape
+    V = w_out.shape[0]
+    if w_out.shape[1] != d:
+        raise ValueError("w_out must be [V, d]")
+    if out is None:
+        out = torch.empty(T, dtype=torch.int32, device=h.device)
+    _need(out, "out", torch.int32)
+    lib = _lib.load()
+    nbytes = lib.qmoe_lm_head_argmax_workspace_bytes()
+    ws = workspace(nbytes, "lm_head", h.device)
+    check(lib.qmoe_lm_head_argmax(_ptr(h), _ptr(w_out), T, d, V, _ptr(out), _ptr(ws), nbytes, _stream()),
+          "qmoe_lm_head_argmax")
+    return out
+
+
 def resume_point(cursor: torch.Tensor, stop_dev: torch.Tensor, offsets: torch.Tensor) -> torch.Tensor:
     """Advance the cursors to the stop and return the resumed launch's offsets (experts below the
     stop emptied); the launch reuses the preempted launch's perm and Xp."""

@@ -115,6 +115,7 @@ class DecoderMoEModel:
         self._meta, self._meta_key = None, None
         self._expect = None  # (handles, members, expected cached entries) of the current pass
         self.preempt_guard = None  # set by the engine per iteration (device-preempt mode)
+        self._pinned_tok = None
 
     # ------------------------------------------------------------------ cache geometry
     def kv_row_shape(self):
@@ -230,9 +231,19 @@ class DecoderMoEModel:
         return K.combine(y, w, res)
 
     def emit_batch(self, h: torch.Tensor, rows: list[int]) -> list[int]:
+        """Final norm + LM head + greedy argmax (lowest id on ties, reference model.py:166-169) in
+        two launches (qmoe_rmsnorm, qmoe_lm_head_argmax: no [T, V] logits); the token ids reach
+        the host through one pinned copy -- the scheduler routes them (EOS, lengths) on the host."""
+        if self._pinned_tok is None or self._pinned_tok.numel() < len(rows):
+            self._pinned_tok = torch.empty(max(64, len(rows)), dtype=torch.int32, pin_memory=True)
+            self._tok_ready = torch.cuda.Event()
         hl = h.index_select(0, torch.tensor(rows, dtype=torch.long, device=self.device))
-        logits = (K.rmsnorm(hl.contiguous(), self.final_norm, self.cfg.rms_eps) @ self.lm_head.T).float()
-        return torch.argmax(logits, dim=1).tolist()  # first maximal index: ties to the lowest id
+        tok = K.lm_head_argmax(K.rmsnorm(hl.contiguous(), self.final_norm, self.cfg.rms_eps), self.lm_head)
+        out = self._pinned_tok[: len(rows)]
+        out.copy_(tok, non_blocking=True)
+        self._tok_ready.record()
+        self._tok_ready.synchronize()
+        return out.tolist()
 
     @staticmethod
     def cat_rows(parts):
