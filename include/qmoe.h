@@ -291,6 +291,37 @@ QMOE_API int qmoe_ep_barrier(int32_t* const* flag_peers, int me, int world, int 
 QMOE_API int qmoe_expert_ffn_peer(const void* xp, const int32_t* offsets, const int32_t* ret, int E, int d, int F,
                                   const void* gate_up, const void* down, int xp_rows, void* act_ws,
                                   void* const* y_peers, void* workspace, size_t workspace_bytes, void* stream);
+/*
+ * qmoe_expert_ffn_peer with the received row count left on the device and the preemption
+ * contract of qmoe_expert_ffn: offsets (device, [E+1], e.g. from qmoe_ep_dispatch_dev) delimit the
+ * received rows; capacity_rows bounds the receive / act buffers (TMA maps); rows_hint is the row
+ * count the kernel-path heuristics assume (e.g. the rank's own T*k: with balanced routing a rank
+ * receives about what it sends); experts [e_begin, e_end); preempt_flag / cursor_out as in
+ * qmoe_expert_ffn.  Workspace: qmoe_expert_ffn_workspace_bytes(SWIGLU, BF16, d, capacity_rows).
+ */
+QMOE_API int qmoe_expert_ffn_peer_ex(const void* xp, const int32_t* offsets, const int32_t* ret, int E, int d, int F,
+                                     const void* gate_up, const void* down, int capacity_rows, int rows_hint,
+                                     int e_begin, int e_end, void* act_ws, void* const* y_peers,
+                                     const volatile int32_t* preempt_flag, int32_t* cursor_out, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+/*
+ * Per-layer queue-length exchange over peer memory, no host round trip: every rank stores its E
+ * queue lengths (from its qmoe_permute offsets) into row `me` of every peer's counts[world][E]
+ * (counts_peers[g] = rank g's buffer), then the flag barrier of qmoe_ep_barrier (epoch, timeout,
+ * error_out as there).  Afterwards every rank holds all ranks' counts.
+ */
+QMOE_API int qmoe_ep_exchange_counts(const int32_t* offsets, int E, int me, int world, int32_t* const* counts_peers,
+                                     int32_t* const* flag_peers, int epoch, long long timeout_ns, int32_t* error_out,
+                                     void* stream);
+/*
+ * qmoe_ep_dispatch with the dispatch tables computed on the device from the exchanged counts
+ * (counts: this rank's [world][E] copy; bounds: device int32 [world+1], rank g owns experts
+ * [bounds[g], bounds[g+1])), plus loc_offsets (device int32 [local experts + 1]): the received
+ * row ranges of this rank's own experts, for qmoe_expert_ffn_peer_ex.
+ */
+QMOE_API int qmoe_ep_dispatch_dev(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k, int E,
+                                  size_t row_bytes, int me, int world, const int32_t* counts, const int32_t* bounds,
+                                  void* const* x_peers, int32_t* const* ret_peers, int32_t* loc_offsets, void* stream);
 
 /*
  * Decoder-side fused helpers (outside the north-star path; used by the Mixtral/Qwen serving

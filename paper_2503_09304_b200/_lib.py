@@ -82,6 +82,12 @@ SIGNATURES = {
     "qmoe_ep_barrier": (_c_int, [_vp, _c_int, _c_int, _c_int, ctypes.c_longlong, _vp, _vp]),
     "qmoe_expert_ffn_peer": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp,
                                       _c_size, _vp]),
+    "qmoe_expert_ffn_peer_ex": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int,
+                                         _c_int, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
+    "qmoe_ep_exchange_counts": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, ctypes.c_longlong, _vp,
+                                         _vp]),
+    "qmoe_ep_dispatch_dev": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_size, _c_int, _c_int, _vp, _vp,
+                                      _vp, _vp, _vp, _vp]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

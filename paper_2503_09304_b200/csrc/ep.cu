@@ -90,6 +90,99 @@ __global__ void ep_barrier_kernel(int32_t* const* flag_peers, int me, int world,
   __syncwarp();
 }
 
+// Device-side count exchange (replaces offsets D2H + host all-gather + host dispatch tables + H2D,
+// the NCCL transport's per-layer host round trip): lane e < E of warp 0 reads this rank's queue
+// length of expert e and stores it into row `me` of every peer's counts[world][E]; then the flag
+// barrier of ep_barrier_kernel (system-scope release of the stores, acquire of every peer's).
+__global__ void ep_exchange_counts_kernel(const int32_t* __restrict__ offsets, int E, int me, int world,
+                                          int32_t* const* counts_peers, int32_t* const* flag_peers, int epoch,
+                                          long long timeout_ns, int32_t* error_out) {
+  const int t = threadIdx.x;
+  for (int i = t; i < world * E; i += blockDim.x) {
+    const int g = i / E, e = i - g * E;
+    counts_peers[g][me * E + e] = offsets[e + 1] - offsets[e];
+  }
+  __syncthreads();
+  if (t < 32) {
+    __threadfence_system();
+    if (t < world) {
+      asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(flag_peers[t] + me), "r"(epoch) : "memory");
+      const int32_t* mine = flag_peers[me] + t;
+      const uint64_t t0 = globaltimer_ns();
+      while (true) {
+        int v;
+        asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+        if (v - epoch >= 0) break;
+        if ((long long)(globaltimer_ns() - t0) > timeout_ns) {
+          if (error_out != nullptr) atomicExch(error_out, 1);
+          break;
+        }
+        __nanosleep(128);
+      }
+    }
+  }
+}
+
+// Dispatch with tables built on the device from the exchanged counts (counts[s][e]: rows of expert e
+// rank s sends).  Owner g of expert e (bounds[g] <= e < bounds[g+1]) lays its receive buffer out
+// local-expert-major, then source rank, then queue order (ep.py dispatch_tables / regroup_index),
+// so the first row of this rank's expert-e block there is
+//   sum_{bounds[g] <= e' < e} sum_s counts[s][e']  +  sum_{s < me} counts[s][e].
+// Block 0 also writes this rank's own local offsets (its experts' received row ranges) for the
+// grouped GEMM.
+__global__ void __launch_bounds__(256) ep_dispatch_dev_kernel(const uint8_t* __restrict__ x,
+                                                              const int32_t* __restrict__ perm,
+                                                              const int32_t* __restrict__ offsets, int k, int E,
+                                                              size_t row_bytes, int me, int world,
+                                                              const int32_t* __restrict__ counts,
+                                                              const int32_t* __restrict__ bounds,
+                                                              void* const* __restrict__ x_peers,
+                                                              int32_t* const* __restrict__ ret_peers,
+                                                              int32_t* __restrict__ loc_offsets) {
+  __shared__ int s_off[65], s_rank[64], s_base[64];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int i = lane; i <= E; i += 32) s_off[i] = offsets[i];
+    if (lane == 0) {
+      for (int g = 0; g < world; ++g) {
+        int base = 0;
+        for (int e = bounds[g]; e < bounds[g + 1]; ++e) {
+          int before = 0, all = 0;
+          for (int s2 = 0; s2 < world; ++s2) {
+            const int c = counts[s2 * E + e];
+            all += c;
+            if (s2 < me) before += c;
+          }
+          s_rank[e] = g;
+          s_base[e] = base + before;
+          if (g == me && blockIdx.x == 0) loc_offsets[e - bounds[g]] = base;
+          base += all;
+        }
+        if (g == me && blockIdx.x == 0) loc_offsets[bounds[g + 1] - bounds[g]] = base;
+      }
+    }
+  }
+  __syncthreads();
+  const int R = s_off[E];
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < R; r += warps) {
+    int lo = 0, hi = E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int e = lo;
+    const int slot = perm[r];
+    const int g = s_rank[e];
+    const size_t row = (size_t)s_base[e] + (r - s_off[e]);
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)(slot / k) * row_bytes);
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(x_peers[g]) + row * row_bytes);
+    for (size_t c = lane; c < row_bytes / 16; c += 32) dst[c] = __ldg(src + c);
+    if (lane == 0) ret_peers[g][row] = (me << 24) | slot;
+  }
+}
+
 PFN_cuMemGetAddressRange_v3020 g_range = nullptr;
 std::once_flag g_range_once;
 std::mutex g_ipc_mu;
@@ -167,4 +260,36 @@ extern "C" int qmoe_ep_barrier(int32_t* const* flag_peers, int me, int world, in
   QMOE_REQUIRE(flag_peers != nullptr, "qmoe_ep_barrier: null flag table");
   ep_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(flag_peers, me, world, epoch, timeout_ns, error_out);
   return check_launch("qmoe_ep_barrier");
+}
+
+extern "C" int qmoe_ep_exchange_counts(const int32_t* offsets, int E, int me, int world, int32_t* const* counts_peers,
+                                       int32_t* const* flag_peers, int epoch, long long timeout_ns,
+                                       int32_t* error_out, void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(E >= 1 && E <= 64 && world >= 1 && world <= 32 && me >= 0 && me < world,
+               "qmoe_ep_exchange_counts: bad sizes E=%d me=%d world=%d", E, me, world);
+  QMOE_REQUIRE(offsets && counts_peers && flag_peers, "qmoe_ep_exchange_counts: null pointer");
+  ep_exchange_counts_kernel<<<1, 256, 0, as_stream(stream)>>>(offsets, E, me, world, counts_peers, flag_peers, epoch,
+                                                              timeout_ns, error_out);
+  return check_launch("qmoe_ep_exchange_counts");
+}
+
+extern "C" int qmoe_ep_dispatch_dev(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k, int E,
+                                    size_t row_bytes, int me, int world, const int32_t* counts, const int32_t* bounds,
+                                    void* const* x_peers, int32_t* const* ret_peers, int32_t* loc_offsets,
+                                    void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(T >= 0 && k >= 1 && E >= 1 && E <= 64, "qmoe_ep_dispatch_dev: bad sizes T=%d k=%d E=%d", T, k, E);
+  QMOE_REQUIRE(world >= 1 && world <= 32 && me >= 0 && me < world, "qmoe_ep_dispatch_dev: bad rank %d/%d", me, world);
+  QMOE_REQUIRE((long long)T * k < (1 << 24), "qmoe_ep_dispatch_dev: %d slots exceed the 24-bit return address", T * k);
+  QMOE_REQUIRE(row_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0,
+               "qmoe_ep_dispatch_dev: rows must be 16-byte multiples and aligned");
+  QMOE_REQUIRE(offsets && counts && bounds && loc_offsets && x_peers && ret_peers && (T == 0 || (x && perm)),
+               "qmoe_ep_dispatch_dev: null pointer");
+  const int rows = T * k;
+  const int grid = rows / 8 + 1 < 148 * 4 ? rows / 8 + 1 : 148 * 4;
+  ep_dispatch_dev_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint8_t*>(x), perm, offsets, k, E,
+                                                              row_bytes, me, world, counts, bounds, x_peers,
+                                                              ret_peers, loc_offsets);
+  return check_launch("qmoe_ep_dispatch_dev");
 }

@@ -48,7 +48,7 @@ static int expert_ffn_entry(int variant, int dtype, const void* xp, const int32_
                                int e_begin, int e_end, int xp_rows, void* act_ws, void* y,
                                const volatile int32_t* preempt_flag, int32_t* cursor_out, void* workspace,
                                size_t workspace_bytes, void* const* y_peers, void* stream,
-                               int32_t* progress = nullptr, int progress_seq = 0) {
+                               int32_t* progress = nullptr, int progress_seq = 0, int path_rows = -1) {
   using namespace qmoe;
   QMOE_REQUIRE(variant == QMOE_EXPERT_TANH_AFFINE || variant == QMOE_EXPERT_SWIGLU,
                "qmoe_expert_ffn: unknown variant %d", variant);
@@ -80,12 +80,13 @@ static int expert_ffn_entry(int variant, int dtype, const void* xp, const int32_
     case QMOE_BF16: {
       // the single-launch kernels signal each expert as its last down unit is stored; the others
       // mark the launch's experts done when the stream reaches the end of the launch
-      const int path = variant == QMOE_EXPERT_SWIGLU ? expert_ffn_path(d, F, E, xp_rows) : QMOE_PATH_UNSUPPORTED;
+      const int path = variant == QMOE_EXPERT_SWIGLU ? expert_ffn_path(d, F, E, path_rows < 0 ? xp_rows : path_rows)
+                                                     : QMOE_PATH_UNSUPPORTED;
       const bool signals = path == QMOE_PATH_SWAP_AB || path == QMOE_PATH_SWAP_PAIR || path == QMOE_PATH_FUSED_1CTA ||
                            path == QMOE_PATH_FUSED_PAIR;
       const int st = expert_ffn_tc(variant, xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y,
                                    preempt_flag, cursor_out, ws, xp_rows, y_peers, s, signals ? progress : nullptr,
-                                   progress_seq);
+                                   progress_seq, path_rows);
       return st || signals ? st : ffn_progress_all(progress, progress_seq, e_begin, e_end, s);
     }
     default:
@@ -120,6 +121,19 @@ extern "C" int qmoe_expert_ffn_peer(const void* xp, const int32_t* offsets, cons
   return expert_ffn_entry(QMOE_EXPERT_SWIGLU, QMOE_BF16, xp, offsets, ret, E, d, F, gate_up, down, 0, E, xp_rows,
                           act_ws, const_cast<void*>(static_cast<const void*>(y_peers)), nullptr, nullptr, workspace,
                           workspace_bytes, y_peers, stream);
+}
+
+extern "C" int qmoe_expert_ffn_peer_ex(const void* xp, const int32_t* offsets, const int32_t* ret, int E, int d, int F,
+                                       const void* gate_up, const void* down, int capacity_rows, int rows_hint,
+                                       int e_begin, int e_end, void* act_ws, void* const* y_peers,
+                                       const volatile int32_t* preempt_flag, int32_t* cursor_out, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
+  QMOE_REQUIRE(y_peers != nullptr, "qmoe_expert_ffn_peer_ex: y_peers is null");
+  QMOE_REQUIRE(rows_hint >= 0, "qmoe_expert_ffn_peer_ex: bad rows_hint %d", rows_hint);
+  return expert_ffn_entry(QMOE_EXPERT_SWIGLU, QMOE_BF16, xp, offsets, ret, E, d, F, gate_up, down, e_begin, e_end,
+                          capacity_rows, act_ws, const_cast<void*>(static_cast<const void*>(y_peers)), preempt_flag,
+                          cursor_out, workspace, workspace_bytes, y_peers, stream, nullptr, 0,
+                          rows_hint > 0 ? rows_hint : 1);
 }
 
 extern "C" int qmoe_expert_ffn_path(int d, int F, int E, int xp_rows) { return qmoe::expert_ffn_path(d, F, E, xp_rows); }

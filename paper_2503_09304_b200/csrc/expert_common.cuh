@@ -259,7 +259,7 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
                     void* const* y_peers, const void* x, int T, int k, cudaStream_t s,
-                    int32_t* progress = nullptr, int seq = 0);
+                    int32_t* progress = nullptr, int seq = 0, int path_rows = -1);
 
 // Mid-size and large batches (expert_fused.cu): 128 x 256 (1 CTA) or 256 x 256 (CTA pair) tiles,
 // gate_up and down in one persistent launch.
@@ -283,7 +283,8 @@ int expert_ffn_path(int d, int F, int E, int xp_rows);
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                   const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int total_rows_hint,
-                  void* const* y_peers, cudaStream_t s, int32_t* progress = nullptr, int seq = 0);
+                  void* const* y_peers, cudaStream_t s, int32_t* progress = nullptr, int seq = 0,
+                  int path_rows = -1);
 // Marks experts [e_begin, e_end) done in progress[] once the stream reaches it (paths whose
 // kernels do not signal per expert: SIMT, tanh, two-launch).
 int ffn_progress_all(int32_t* progress, int seq, int e_begin, int e_end, cudaStream_t s);

@@ -428,10 +428,11 @@ bool use_swap_ab(int xp_rows, int n_experts, int d, int F) {
 int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                     const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                     const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                    void* const* y_peers, const void* x, int T, int k, cudaStream_t s, int32_t* progress, int seq) {
+                    void* const* y_peers, const void* x, int T, int k, cudaStream_t s, int32_t* progress, int seq,
+                    int path_rows) {
   int st;
   // Token tile: 32 rows when experts see ~1-24 rows on average (decode), 64 up to ~64, else 128.
-  const double mean_rows = (double)xp_rows / (E > 0 ? E : 1);
+  const double mean_rows = (double)(path_rows < 0 ? xp_rows : path_rows) / (E > 0 ? E : 1);
   const int NT = mean_rows <= 24.0 ? 32 : (mean_rows <= 64.0 ? 64 : 128);
   CUtensorMap maps[4];
   // token rows: NT-row boxes of Xp, or single rows of X for the tile::gather4 loads (x != nullptr)

@@ -601,17 +601,20 @@ int launch_tc2(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cu
 int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
                   const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                   const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
-                  void* const* y_peers, cudaStream_t s, int32_t* progress, int seq) {
+                  void* const* y_peers, cudaStream_t s, int32_t* progress, int seq, int path_rows) {
   int st = init_driver();
+  // path_rows: the row count the kernel-path heuristics see (expert parallel: xp_rows is the
+  // receive buffer's capacity, the received count is only on the device); buffers use xp_rows
+  if (path_rows < 0) path_rows = xp_rows;
   if (st) return st;
   QMOE_REQUIRE(d % 64 == 0, "qmoe_expert_ffn(bf16): d must be a multiple of 64 (d=%d)", d);
   QMOE_REQUIRE(variant != QMOE_EXPERT_SWIGLU || F % 64 == 0, "qmoe_expert_ffn(bf16): F must be a multiple of 64");
   QMOE_REQUIRE(((uintptr_t)xp | (uintptr_t)w1 | (uintptr_t)y | (uintptr_t)(act_ws ? act_ws : y)) % 16 == 0,
                "qmoe_expert_ffn(bf16): buffers must be 16-byte aligned");
-  if (variant == QMOE_EXPERT_SWIGLU && use_swap_ab(xp_rows, E, d, F))
+  if (variant == QMOE_EXPERT_SWIGLU && use_swap_ab(path_rows, E, d, F))
     return expert_ffn_swap(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
-                           xp_rows, y_peers, nullptr, 0, 0, s, progress, seq);
-  if (variant == QMOE_EXPERT_SWIGLU && use_swap_pair(xp_rows, E, d, F))
+                           xp_rows, y_peers, nullptr, 0, 0, s, progress, seq, path_rows);
+  if (variant == QMOE_EXPERT_SWIGLU && use_swap_pair(path_rows, E, d, F))
     return expert_ffn_swap_pair(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
                                 xp_rows, y_peers, nullptr, 0, 0, s, progress, seq);
   constexpr int BN = 256;
@@ -632,7 +635,7 @@ int expert_ffn_tc(int variant, const void* xp, const int32_t* offsets, const int
     if ((st = launch_tc<BN, EPI_TANH>(ta, tb, p, s))) return st;
     return ffn_finalize(ws, nullptr, e_end, cursor_out, s, flag);
   }
-  const bool pair = use_cta_pair(xp_rows, e_end - e_begin);
+  const bool pair = use_cta_pair(path_rows, e_end - e_begin);
   if (down_splits(xp_rows, e_end - e_begin, d, F) == 1 && use_fused_tc())
     return expert_ffn_fused(xp, offsets, perm, E, d, F, w1, w2, e_begin, e_end, act_ws, y, flag, cursor_out, ws,
                             xp_rows, y_peers, pair, nullptr, 0, 0, s, progress, seq);

@@ -586,10 +586,12 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
   // 35/59 (8 slices).  Qwen's 61 logit rows: 4 expert groups re-read X from L1 and W from L2 per
   // 16 tokens -- faster up to 2k tokens (17 vs 23 us), slower from 8k (51 vs 39 us), where the
   // cp.async kernel's 32-token tiles halve the W re-reads.
+  // ncu at 8k tokens: <8,1,1,4> reads 67 MB in 24 us (2.8 TB/s) at 128 registers = 2 CTAs/SM, so
+  // 512 CTAs take 1.7 waves; U = 2 halves the register buffers (4 CTAs/SM: one wave).
   if (E <= 8) {
-    if (cfg == 1) { QMOE_TRY_STREAM(4, 1, 1, 8) }
+    if (cfg == 1) { QMOE_TRY_STREAM(8, 1, 1, 4) }
     if (cfg == 2 || (cfg == 0 && T_ < 4096)) { QMOE_TRY_STREAM(16, 1, 1, 2) }
-    QMOE_TRY_STREAM(8, 1, 1, 4)
+    QMOE_TRY_STREAM(8, 1, 1, 2)
   } else if (E <= 16) {
     QMOE_TRY_STREAM(8, 1, 2, 4)
   } else if (E <= 32) {

@@ -185,12 +185,21 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
         self.flags = torch.zeros(world, dtype=torch.int32, device=dev)
         self.error = torch.zeros(1, dtype=torch.int32, device=dev)
         self.act = torch.empty((cap, intermediate_size), dtype=dtype, device=dev)
+        # per-layer queue lengths of every rank ([world][E], filled by the peers' exchange kernels),
+        # the expert ownership bounds and this rank's received row ranges, all on the device
+        self.counts = torch.zeros(world * num_experts, dtype=torch.int32, device=dev)
+        self.bounds_dev = torch.tensor(self.bounds, dtype=torch.int32, device=dev)
+        self.loc_offsets = torch.zeros(self.e_hi - self.e_lo + 1, dtype=torch.int32, device=dev)
         self.epoch = 0
         self.timeout_s = barrier_timeout_s
         # host_barrier: order the phases with a stream sync + process-group barrier instead of the
         # device flag barrier (debugging aid: isolates the data path from the flag protocol)
         self.host_barrier = host_barrier
         self._peer_tables = None
+        # the barrier kernels time out into self.error instead of hanging; it is read (one sync)
+        # every check_every forward calls and raises (0 disables)
+        self.check_every = 64
+        self._calls = 0
 
     def _comm_device(self):
         backend = dist.get_backend(self.group)
@@ -198,7 +207,7 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
 
     def connect(self) -> None:
         """Exchange CUDA IPC handles of the receive / return / slot / flag buffers (collective)."""
-        bufs = (self.x_recv, self.ret, self.y, self.flags)
+        bufs = (self.x_recv, self.ret, self.y, self.flags, self.counts)
         mine = [K.ipc_export(t) for t in bufs]
         torch.cuda.synchronize(self.device)  # buffers (zeroed flags) materialised before peers map them
         allh = [None] * self.world
@@ -214,7 +223,19 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
         return dispatch_tables(allc, self.bounds, self.rank)
 
     @torch.no_grad()
-    def forward(self, hidden_states: torch.Tensor, residual: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def forward(self, hidden_states: torch.Tensor, residual: Optional[torch.Tensor] = None,
+                preempt_flag: Optional[torch.Tensor] = None, cursor_out: Optional[torch.Tensor] = None,
+                cursor: Optional[torch.Tensor] = None, routing=None) -> torch.Tensor:
+        """One MoE layer with no host round trip: router + permute (local tokens), queue-length
+        exchange over peer memory (every rank gets all ranks' counts), dispatch with device-built
+        tables, barrier, grouped GEMM on the local experts whose epilogue returns rows to their
+        source ranks, barrier, combine.
+
+        Preemption (north_star item 4 under EP): preempt_flag (this rank's int32 device flag, in
+        LOCAL expert ids: s > 0 stops the local launch at the first local boundary >= s) and
+        cursor_out (local stop) as qmoe_expert_ffn; cursor (int32 [T], GLOBAL expert ids) keeps
+        already-completed slots of this rank's tokens out of the dispatch on a resume, with routing
+        = (ids, w) of the preempted layer so the resumed layer routes nothing anew."""
         ops, E, k, d = self.ops, self.E, self.k, self.d
         shape = hidden_states.shape
         x = hidden_states.reshape(-1, d).contiguous()
@@ -223,27 +244,27 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
             raise ValueError(f"{T} tokens exceed max_tokens={self.max_tokens}")
         if self._peer_tables is None:
             self.connect()
-        x_peers, ret_peers, y_peers, flag_peers = self._peer_tables
-        ids, w = ops.router(x, self.w_router, k, self.route_mode)
-        perm, offsets, _ = ops.permute(ids, E)
+        x_peers, ret_peers, y_peers, flag_peers, counts_peers = self._peer_tables
+        ids, w = routing if routing is not None else ops.router(x, self.w_router, k, self.route_mode)
+        perm, offsets, _ = ops.permute(ids, E, cursor=cursor)
         self.last_routing = (ids, w, perm, offsets)
-        off = offsets.tolist()
-        allc = self.exchange_counts([off[e + 1] - off[e] for e in range(E)])
-        dest_rank, dest_base = self.dispatch_tables(allc)
-        tab = torch.tensor([dest_rank, dest_base], dtype=torch.int32).to(self.device, non_blocking=True)
-        ops.ep_dispatch(x, perm, offsets, k, self.rank, tab[0], tab[1], x_peers, ret_peers)
+        self.epoch += 1
+        ops.ep_exchange_counts(offsets, self.rank, self.world, counts_peers, flag_peers, self.epoch, self.error,
+                               self.timeout_s)
+        ops.ep_dispatch_dev(x, perm, offsets, k, self.rank, self.world, self.counts, self.bounds_dev, x_peers,
+                            ret_peers, self.loc_offsets)
         self._barrier(flag_peers)
-        loc = [0]
-        for e in range(self.e_lo, self.e_hi):
-            loc.append(loc[-1] + sum(allc[s][e] for s in range(self.world)))
-        R = loc[-1]
-        if R:
-            loc_off = torch.tensor(loc, dtype=torch.int32).to(self.device, non_blocking=True)
-            ops.expert_ffn_peer(self.x_recv[:R], loc_off, self.ret[:R], self.gate_up, self.down, y_peers,
-                                act_ws=self.act[:R])
+        ops.expert_ffn_peer_ex(self.x_recv, self.loc_offsets, self.ret, self.gate_up, self.down, y_peers,
+                               rows_hint=T * k, act_ws=self.act, preempt_flag=preempt_flag, cursor_out=cursor_out)
         self._barrier(flag_peers)
         res = None if residual is None else residual.reshape(-1, d).contiguous()
-        return ops.combine(self.y[: T * k], w, res).reshape(shape)
+        out = ops.combine(self.y[: T * k], w, res).reshape(shape)
+        self._calls += 1
+        if self.check_every and self._calls % self.check_every == 0 and self.barrier_failed():
+            # a peer never arrived: the layers since the last check ran on partial peer buffers
+            raise RuntimeError(f"rank {self.rank}: an expert-parallel device barrier timed out "
+                               f"(within the last {self.check_every} layers)")
+        return out
 
     def _barrier(self, flag_peers) -> None:
         self.epoch += 1

@@ -391,6 +391,59 @@ def expert_ffn_peer(xp: torch.Tensor, offsets: torch.Tensor, ret: torch.Tensor, 
                                    _ptr(act_ws), _ptr(y_peers), _ptr(ws), nbytes, _stream()), "qmoe_expert_ffn_peer")
 
 
+def ep_exchange_counts(offsets: torch.Tensor, me: int, world: int, counts_peers: torch.Tensor,
+                       flag_peers: torch.Tensor, epoch: int, error: Optional[torch.Tensor] = None,
+                       timeout_s: float = 10.0) -> None:
+    """Publish this rank's queue lengths into every peer's counts[world][E] and barrier (see qmoe.h)."""
+    _need(offsets, "offsets", torch.int32)
+    _need(counts_peers, "counts_peers", torch.int64)
+    _need(flag_peers, "flag_peers", torch.int64)
+    lib = _lib.load()
+    check(lib.qmoe_ep_exchange_counts(_ptr(offsets), offsets.shape[0] - 1, me, world, _ptr(counts_peers),
+                                      _ptr(flag_peers), epoch, int(timeout_s * 1e9), _ptr(error), _stream()),
+          "qmoe_ep_exchange_counts")
+
+
+def ep_dispatch_dev(x: torch.Tensor, perm: torch.Tensor, offsets: torch.Tensor, k: int, me: int, world: int,
+                    counts: torch.Tensor, bounds: torch.Tensor, x_peers: torch.Tensor, ret_peers: torch.Tensor,
+                    loc_offsets: torch.Tensor) -> None:
+    """Dispatch with device-built tables from the exchanged counts; writes loc_offsets."""
+    _need(x, "x")
+    for name, t in (("perm", perm), ("offsets", offsets), ("counts", counts), ("bounds", bounds),
+                    ("loc_offsets", loc_offsets)):
+        _need(t, name, torch.int32)
+    _need(x_peers, "x_peers", torch.int64)
+    _need(ret_peers, "ret_peers", torch.int64)
+    T, d = x.shape
+    lib = _lib.load()
+    check(lib.qmoe_ep_dispatch_dev(_ptr(x), _ptr(perm), _ptr(offsets), T, k, offsets.shape[0] - 1, d * x.element_size(),
+                                   me, world, _ptr(counts), _ptr(bounds), _ptr(x_peers), _ptr(ret_peers),
+                                   _ptr(loc_offsets), _stream()), "qmoe_ep_dispatch_dev")
+
+
+def expert_ffn_peer_ex(xp: torch.Tensor, offsets: torch.Tensor, ret: torch.Tensor, gate_up: torch.Tensor,
+                       down: torch.Tensor, y_peers: torch.Tensor, rows_hint: int, act_ws: torch.Tensor,
+                       e_begin: int = 0, e_end: Optional[int] = None, preempt_flag: Optional[torch.Tensor] = None,
+                       cursor_out: Optional[torch.Tensor] = None) -> None:
+    """Grouped SwiGLU experts over the received rows (count on the device, capacity = xp rows)."""
+    _need(xp, "xp", torch.bfloat16)
+    _need(offsets, "offsets", torch.int32)
+    _need(ret, "ret", torch.int32)
+    _need(y_peers, "y_peers", torch.int64)
+    _need(act_ws, "act_ws", torch.bfloat16)
+    E, twoF, d = gate_up.shape
+    F = twoF // 2
+    cap = xp.shape[0]
+    if e_end is None:
+        e_end = E
+    lib = _lib.load()
+    nbytes = lib.qmoe_expert_ffn_workspace_bytes(EXPERT_SWIGLU, _lib.QMOE_BF16, d, cap)
+    ws = workspace(nbytes, "ffn", xp.device)
+    check(lib.qmoe_expert_ffn_peer_ex(_ptr(xp), _ptr(offsets), _ptr(ret), E, d, F, _ptr(gate_up), _ptr(down), cap,
+                                      int(rows_hint), e_begin, e_end, _ptr(act_ws), _ptr(y_peers), _ptr(preempt_flag),
+                                      _ptr(cursor_out), _ptr(ws), nbytes, _stream()), "qmoe_expert_ffn_peer_ex")
+
+
 # ------------------------------------------------------------------ fused row gather
 
 PATH_SWAP_AB, PATH_FUSED_1CTA, PATH_FUSED_PAIR = _lib.QMOE_PATH_SWAP_AB, _lib.QMOE_PATH_FUSED_1CTA, _lib.QMOE_PATH_FUSED_PAIR

@@ -59,6 +59,17 @@ def serve_once(model, trace, scheduler: str, max_batch_size: int = 32, slo_ms: f
         "engine": res.engine_stats,
         "preempt_positions": sim.engine.preemption_positions(),
     }
+    # where the time went: busy time per phase, decode batch sizes, idle time (no work queued)
+    its = res.probes.iterations
+    dit = [r for r in its if r.phase.name == "DECODE"]
+    pit = [r for r in its if r.phase.name == "PREFILL"]
+    busy = sum(r.duration_ms for r in its)
+    out["iterations"] = {
+        "decode": len(dit), "decode_ms": sum(r.duration_ms for r in dit),
+        "decode_members_mean": sum(r.size for r in dit) / len(dit) if dit else 0.0,
+        "prefill": len(pit), "prefill_ms": sum(r.duration_ms for r in pit),
+        "preempted": sum(1 for r in its if r.preempted), "idle_ms": res.makespan_ms - busy,
+    }
     if dec and ls:
         # the paper's SLO is 10x an A100 decode iteration; the B200 analogue is 10x
         # this run's measured median decode iteration
