@@ -190,9 +190,20 @@ def make_layer(rank: int, world: int, device, transport: str = "p2p", max_tokens
     from paper_2503_09304_b200.ep import ExpertParallelMoE, PeerExpertParallelMoE
 
     if transport == "p2p":
-        return PeerExpertParallelMoE(D, F, E, TOPK, rank, world, max_tokens=max_tokens,
-                                     device=device).init_random(seed=1234)
-    return ExpertParallelMoE(D, F, E, TOPK, rank, world, device=device).init_random(seed=1234)
+        blk = PeerExpertParallelMoE(D, F, E, TOPK, rank, world, max_tokens=max_tokens,
+                                    device=device).init_random(seed=1234)
+    else:
+        blk = ExpertParallelMoE(D, F, E, TOPK, rank, world, device=device).init_random(seed=1234)
+    # per-rank setup (stderr): process group backend, transport, local experts, peer access
+    import torch.distributed as dist
+
+    n = torch.cuda.device_count()
+    peers = [g for g in range(n) if g != device.index and torch.cuda.can_device_access_peer(device.index, g)]
+    print(json.dumps({"rank": rank, "world": world, "device": str(device), "gpu": torch.cuda.get_device_name(device),
+                      "backend": dist.get_backend(), "transport": transport, "experts": [blk.e_lo, blk.e_hi],
+                      "p2p_peers": peers, "nccl": ".".join(map(str, torch.cuda.nccl.version()))}),
+          file=sys.stderr, flush=True)
+    return blk
 
 
 def count_launches(T: int, world: int, transport: str = "p2p") -> int:
@@ -208,7 +219,10 @@ def count_launches(T: int, world: int, transport: str = "p2p") -> int:
     ffn = {K.PATH_SWAP_AB: 1 + (1 if rows <= 512 else 0), K.PATH_SWAP_PAIR: 1, K.PATH_FUSED_1CTA: 1,
            K.PATH_FUSED_PAIR: 1}.get(path, 4)
     if world > 1 and transport == "p2p":
-        return 1 + K.permute_launches(T, TOPK, gather=False) + 1 + 2 + ffn + 1
+        # + queue-length exchange, dispatch, 2 flag barriers; the receive buffer's capacity (> 512
+        # rows) rules out the K-split decode path, so the expert launch is one kernel
+        ffn = 1 if path in (K.PATH_SWAP_AB, K.PATH_SWAP_PAIR, K.PATH_FUSED_1CTA, K.PATH_FUSED_PAIR) else ffn
+        return 1 + K.permute_launches(T, TOPK, gather=False) + 1 + 1 + 2 + ffn + 1
     return 1 + K.permute_launches(T, TOPK) + ffn + 1 + (2 if world > 1 else 0)
 
 

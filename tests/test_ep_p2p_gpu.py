@@ -129,3 +129,66 @@ def test_device_flag_barrier_two_concurrent_ranks(cuda):
     Kn.ep_barrier(table, 0, 2, 61, err, timeout_s=0.2)  # rank 1 never arrives
     torch.cuda.synchronize()
     assert int(err) == 1
+
+
+def _preempt_worker(rank, world, port, q, T, stop_local):
+    """Each rank runs one layer with its local launch stopped at local boundary stop_local (the
+    device flag preset), agrees on the global resume cursor with its peer, resumes the layer with
+    that cursor (same routing, pending slots only), and returns the output bits plus an
+    uninterrupted layer's for comparison."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2503_09304_b200.ep import PeerExpertParallelMoE
+
+        dev = torch.device("cuda", 0)
+        blk = PeerExpertParallelMoE(D, F, E, K, rank, world, max_tokens=1024, device=dev,
+                                    barrier_timeout_s=60.0).init_random(SEED)
+        x = _inputs(rank, 7, T).cuda()
+        full = blk(x, residual=x).clone()
+        ids, w = blk.last_routing[:2]
+        blk.y.fill_(float("nan"))  # every slot must be rewritten by the preempted launch or the resume
+        flag = torch.full((1,), stop_local, dtype=torch.int32, device=dev)
+        stop = torch.zeros(1, dtype=torch.int32, device=dev)
+        blk(x, residual=x, preempt_flag=flag, cursor_out=stop, routing=(ids, w))
+        torch.cuda.synchronize()
+        # global resume point: experts below it completed on every rank (a rank that ran past it
+        # recomputes the rest -- same bits); the ranks' local stops are exchanged on the host here
+        lo, hi = blk.e_lo, blk.e_hi
+        mine = lo + int(stop) if int(stop) < hi - lo else E
+        allst = [None] * world
+        dist.all_gather_object(allst, mine)
+        c = min(allst)
+        cursor = torch.full((T,), c, dtype=torch.int32, device=dev)
+        out = blk(x, residual=x, cursor=cursor, routing=(ids, w))
+        torch.cuda.synchronize()
+        q.put((rank, int(stop), c, torch.equal(out.view(torch.int16), full.view(torch.int16)), blk.barrier_failed(),
+               None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, None, None, None, None, repr(exc)))
+
+
+@pytest.mark.parametrize("T,stop_local", [(40, 1), (700, 2), (600, 1)])
+def test_expert_parallel_preemption_resume_is_bit_identical(cuda, T, stop_local):
+    """Preemption under EP: each rank's grouped launch over its local experts stops
+    at an expert boundary (device flag), the ranks resume from the common global cursor, and the
+    layer output equals an uninterrupted layer's bit for bit on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_preempt_worker, args=(r, 2, port, q, T, stop_local)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    errors = [g[-1] for g in got if g[-1]]
+    assert not errors, errors
+    for rank, stop, c, same, failed, _ in got:
+        assert not failed
+        assert stop is not None and stop <= E // 2
+        assert same, (rank, stop, c)
+    assert any(g[2] < E for g in got)  # the launch really stopped before the last expert somewhere
