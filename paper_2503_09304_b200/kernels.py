@@ -229,6 +229,30 @@ def permute_launches(T: int, k: int, gather: bool = True) -> int:
     return (1 if nblk > 1 else 0) + 1 + (1 if gather and S > 32 else 0)
 
 
+def paged_decode_attention(q: torch.Tensor, pool: torch.Tensor, block_table: torch.Tensor, seq_lens: torch.Tensor,
+                           max_len: int, scale: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """q [B, H, hd] bf16, pool [n_pages, page, 2, KV, hd] bf16, block_table [B, max_pages] int32,
+    seq_lens [B] int32 -> out [B, H, hd] (one query token per sequence, all cached tokens)."""
+    _need(q, "q", torch.bfloat16)
+    _need(pool, "pool", torch.bfloat16)
+    _need(block_table, "block_table", torch.int32)
+    _need(seq_lens, "seq_lens", torch.int32)
+    B, H, hd = q.shape
+    _, page, two, KV, hd2 = pool.shape
+    if two != 2 or hd2 != hd:
+        raise ValueError("pool must be [n_pages, page, 2, KV, head_dim]")
+    max_pages = block_table.shape[1]
+    if out is None:
+        out = torch.empty_like(q)
+    lib = _lib.load()
+    nbytes = lib.qmoe_paged_decode_attention_workspace_bytes(B, KV, max_pages)
+    ws = workspace(nbytes, "attn", q.device)
+    check(lib.qmoe_paged_decode_attention(_ptr(q), _ptr(pool), _ptr(block_table), _ptr(seq_lens), B, H, KV, hd, page,
+                                          max_pages, int(max_len), float(scale), _ptr(out), _ptr(ws), nbytes,
+                                          _stream()), "qmoe_paged_decode_attention")
+    return out
+
+
 def lm_head_argmax(h: torch.Tensor, w_out: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Greedy tokens [T] int32 on the device: argmax_v(w_out[v] . h[t]), lowest id on ties."""
     _need(h, "h", torch.bfloat16)

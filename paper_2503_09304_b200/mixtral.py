@@ -116,6 +116,10 @@ class DecoderMoEModel:
         self._expect = None  # (handles, members, expected cached entries) of the current pass
         self.preempt_guard = None  # set by the engine per iteration (device-preempt mode)
         self._pinned_tok = None
+        # decode attention: libqmoe's paged kernel (default) or flash-attn's (QMOE_FA_DECODE=1, A/B)
+        import os
+
+        self._fa_decode = os.environ.get("QMOE_FA_DECODE", "0") == "1"
 
     # ------------------------------------------------------------------ cache geometry
     def kv_row_shape(self):
@@ -175,6 +179,7 @@ class DecoderMoEModel:
                 meta["bt"] = torch.tensor([t + [0] * (width - len(t)) for t in tables], dtype=torch.int32,
                                           device=self.device)
                 meta["lens"] = torch.tensor([have + n for (_, have, n) in key], dtype=torch.int32, device=self.device)
+                meta["max_len"] = max(have + n for (_, have, n) in key)
             else:
                 cu = [0]
                 for (_, _, n) in key:
@@ -189,7 +194,11 @@ class DecoderMoEModel:
         # guard: the engine's per-iteration preempt flag in device-preempt mode (no append once an
         # expert launch of this iteration stopped early, see engine._experts_device_preempt)
         cache.scatter(layer, meta["slots"], torch.stack([k, v], 1), guard=self.preempt_guard)
-        if decode:
+        if decode and not self._fa_decode:
+            # hand-written paged GQA decode attention on the page pool (csrc/attention.cu)
+            attn = K.paged_decode_attention(q, cache.pool(layer), meta["bt"], meta["lens"], meta["max_len"],
+                                            hd ** -0.5).view(T, H * hd)
+        elif decode:
             pool = cache.pool(layer)
             attn = self._fa_kvcache(q.view(T, 1, H, hd), pool[:, :, 0], pool[:, :, 1], cache_seqlens=meta["lens"],
                                     block_table=meta["bt"], causal=True).view(T, H * hd)
