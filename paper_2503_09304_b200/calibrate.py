@@ -165,16 +165,20 @@ def fit_cost_model(samples: dict) -> tuple[CostModel, dict]:
     return cm, rep
 
 
-def measure_stage_samples(model, trace, max_batch_size: int = 32, scheduler: str = "qllm") -> dict:
-    """Run `trace` through the engine on a virtual clock (host-boundary expert stage: the host
-    reads each layer's queue lengths, so the device is idle between stages) with CUDA events around
-    every stage of `model`; returns the samples fit_cost_model takes.  Checkpoint / restore are
-    the host time of the engine's _preempt and the device time of the restore gather."""
+def measure_stage_samples(model, trace, max_batch_size: int = 32, scheduler: str = "qllm",
+                          wall: bool = True) -> dict:
+    """Run `trace` through the engine with CUDA events around every stage of `model`; returns the
+    samples fit_cost_model takes.  wall=True: the serving configuration (WallClock, device-preempt
+    expert stage: the host runs ahead, so an event pair brackets the stage's device time);
+    wall=False: virtual clock (host-boundary expert stage, one host sync per layer, whose report
+    loop then shows up in the expert stage).  Checkpoint / restore are the host time of the
+    engine's _preempt and the device time of the restore gather."""
     import time as _time
 
     from .sim import Simulation
 
-    sim = Simulation(trace, model=model, scheduler=scheduler, max_batch_size=max_batch_size)
+    sim = Simulation(trace, model=model, scheduler=scheduler, max_batch_size=max_batch_size,
+                     clock=WallClock() if wall else None)
     eng = sim.engine
     out = {"attention": [], "router": [], "experts": [], "checkpoint": [], "restore": []}
     pending = []  # (kind, start event, end event, extra) resolved after the run

@@ -694,6 +694,10 @@ bool use_cta_pair(int xp_rows, int n_experts) {
   }();
   if (forced >= 0) return forced == 1 && xp_rows > kSplitRowsMax;
   if (xp_rows < 1536) return false;  // measured crossover (Mixtral: pair faster from ~768 tokens)
+  // fine-grained experts (Qwen's 60 routed + 4 shared sub-experts): the mean is inflated by the
+  // shared sub-experts' T rows while the routed experts see ~T/15 -- the 1-CTA tiles measured
+  // 0-7% faster at 1k-16k tokens (tools/qwen_ab.py, profiles/qwen_paths_r02.jsonl)
+  if (n_experts > 16) return false;
   const double r = (double)xp_rows / (n_experts > 0 ? n_experts : 1);
   auto eff = [r](int m) { return r / (m * std::ceil(r / m)); };
   return eff(256) >= eff(128) - 0.02;

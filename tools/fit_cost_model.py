@@ -19,12 +19,16 @@ name = sys.argv[2] if len(sys.argv) > 2 else "mixtral"
 model = DecoderMoEModel(QWEN15_MOE_A27B if name == "qwen" else MIXTRAL_8X7B)
 trace = trace_for_rate(WorkloadSpec(duration_s=6.0, output_bounds=(1, 160)), 7.0, seed=11)
 measure_stage_samples(model, trace[:6])  # warm-up (kernels, allocator)
-samples = measure_stage_samples(model, trace)
+samples = measure_stage_samples(model, trace, wall=True)
 cm, rep = fit_cost_model(samples)
+cm_v, rep_v = fit_cost_model(measure_stage_samples(model, trace, wall=False))
 wall = _canonical_iteration_ms(model, WallClock(), CostModel(), 0, model.config.vocab_size, repeats=5)
 virt = _canonical_iteration_ms(model, VirtualClock(), cm, 0, model.config.vocab_size)[0]
+virt_v = _canonical_iteration_ms(model, VirtualClock(), cm_v, 0, model.config.vocab_size)[0]
 out = {"model": model.config.name, "trace": f"paper workload, 7 req/s, 6 s ({len(trace)} jobs, outputs <= 160)",
        "samples": {k: len(v) for k, v in samples.items()}, "fit": rep, "cost_model": cm.__dict__,
+       "virtual_clock_measurement": {"fit": rep_v, "cost_model": cm_v.__dict__,
+                                     "canonical_decode_virtual_ms_fitted": virt_v},
        "reference_cost_model": CostModel().__dict__,
        "validation": {"canonical_decode_wall_ms_median": statistics.median(wall), "wall_ms_all": wall,
                       "canonical_decode_virtual_ms_fitted": virt,
