@@ -347,16 +347,17 @@ QMOE_API int qmoe_rope(void* q, void* k, const int64_t* positions, const float* 
 /*
  * Paged GQA decode attention over the engine's KV page pool (the decoders' attention stage at
  * decode; reference counterpart: the attention stage engine.py:252-301, a toy single-head
- * attention).  q: [B, H, head_dim] bf16 (one query token per sequence, RoPE applied);
+ * attention).  q: B rows of [H, head_dim] bf16, q_stride elements apart (one query token per
+ * sequence, RoPE applied; e.g. rows of a packed qkv projection);
  * pool: [n_pages, page_size, 2, KV, head_dim] bf16 (K then V); block_table: [B, max_pages] int32;
  * seq_lens: [B] cached tokens incl. the new one (the query attends all of them); max_len >=
  * max(seq_lens) (host-known); scale: softmax scale.  out: [B, H, head_dim] bf16.  fp32 scores,
  * online softmax and accumulation; one CTA per (sequence, KV head, page), pages merged in order
- * by the last CTA (deterministic).  head_dim 128, H / KV in {1, 2, 4, 8}.  workspace:
+ * by the last CTA (deterministic).  head_dim 128, H / KV in {1, 2, 4}.  workspace:
  * qmoe_paged_decode_attention_workspace_bytes(B, KV, max_pages) bytes, ZEROED once at allocation.
  */
 QMOE_API size_t qmoe_paged_decode_attention_workspace_bytes(int B, int KV, int max_pages);
-QMOE_API int qmoe_paged_decode_attention(const void* q, const void* pool, const int32_t* block_table,
+QMOE_API int qmoe_paged_decode_attention(const void* q, int q_stride, const void* pool, const int32_t* block_table,
                                          const int32_t* seq_lens, int B, int H, int KV, int head_dim, int page_size,
                                          int max_pages, int max_len, float scale, void* out, void* workspace,
                                          size_t workspace_bytes, void* stream);

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ pool,
                     const int32_t* __restrict__ block_table, const int32_t* __restrict__ seq_lens, int H, int KV,
                     int page, int max_pages, float scale, __nv_bfloat16* __restrict__ out,
-                    AttnPartial* __restrict__ parts, int* __restrict__ arrivals) {
+                    AttnPartial* __restrict__ parts, int* __restrict__ arrivals, int q_stride) {
   pdl_wait();
   pdl_trigger();
   const int b = blockIdx.x, g = blockIdx.y, sp = blockIdx.z;
@@ -60,7 +60,7 @@ paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
   // broadcasts while it walks its own token's K row
   __shared__ __align__(16) float s_q[G][kHd];
   for (int i = threadIdx.x; i < G * kHd; i += blockDim.x)
-    s_q[i / kHd][i % kHd] = __bfloat162float(q[((size_t)b * H + g * G) * kHd + i]) * scale;
+    s_q[i / kHd][i % kHd] = __bfloat162float(q[(size_t)b * q_stride + (size_t)g * G * kHd + i]) * scale;
   __syncthreads();
   if (sp < npages) {
     const int pg = block_table[(size_t)b * max_pages + sp];
@@ -188,13 +188,13 @@ paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
 }
 
 template <int G>
-int launch_decode(const void* q, const void* pool, const int32_t* bt, const int32_t* lens, int B, int H, int KV,
-                  int page, int max_pages, int splits, float scale, void* out, void* ws, cudaStream_t s) {
+int launch_decode(const void* q, int q_stride, const void* pool, const int32_t* bt, const int32_t* lens, int B, int H,
+                  int KV, int page, int max_pages, int splits, float scale, void* out, void* ws, cudaStream_t s) {
   AttnPartial* parts = reinterpret_cast<AttnPartial*>(ws);
   int* arrivals = reinterpret_cast<int*>(parts + (size_t)B * KV * max_pages);
   return launch_pdl("qmoe_paged_decode_attention", paged_decode_kernel<G>, dim3(B, KV, splits),
                     dim3(kAttnWarps * 32), 0, s, (const __nv_bfloat16*)q, (const __nv_bfloat16*)pool, bt, lens, H, KV,
-                    page, max_pages, scale, (__nv_bfloat16*)out, parts, arrivals);
+                    page, max_pages, scale, (__nv_bfloat16*)out, parts, arrivals, q_stride);
 }
 
 }  // namespace
@@ -204,7 +204,7 @@ extern "C" size_t qmoe_paged_decode_attention_workspace_bytes(int B, int KV, int
   return sizeof(qmoe::AttnPartial) * (size_t)B * KV * max_pages + sizeof(int) * (size_t)B * KV;
 }
 
-extern "C" int qmoe_paged_decode_attention(const void* q, const void* pool, const int32_t* block_table,
+extern "C" int qmoe_paged_decode_attention(const void* q, int q_stride, const void* pool, const int32_t* block_table,
                                            const int32_t* seq_lens, int B, int H, int KV, int head_dim,
                                            int page_size, int max_pages, int max_len, float scale, void* out,
                                            void* workspace, size_t workspace_bytes, void* stream) {
@@ -212,6 +212,7 @@ extern "C" int qmoe_paged_decode_attention(const void* q, const void* pool, cons
   QMOE_REQUIRE(head_dim == kHd, "qmoe_paged_decode_attention: head_dim must be %d (got %d)", kHd, head_dim);
   QMOE_REQUIRE(B >= 0 && KV >= 1 && H % KV == 0 && H / KV <= kMaxG, "qmoe_paged_decode_attention: bad heads H=%d KV=%d",
                H, KV);
+  QMOE_REQUIRE(q_stride >= H * head_dim, "qmoe_paged_decode_attention: q_stride %d < H * head_dim", q_stride);
   QMOE_REQUIRE(page_size >= 1 && max_pages >= 1 && max_len >= 1 && max_len <= page_size * max_pages,
                "qmoe_paged_decode_attention: bad paging (page %d, pages %d, max_len %d)", page_size, max_pages,
                max_len);
@@ -223,13 +224,17 @@ extern "C" int qmoe_paged_decode_attention(const void* q, const void* pool, cons
   QMOE_REQUIRE(((uintptr_t)q | (uintptr_t)pool) % 16 == 0, "qmoe_paged_decode_attention: 16-byte alignment");
   const int splits = (max_len + page_size - 1) / page_size;  // one CTA per page of the longest sequence
   cudaStream_t s = as_stream(stream);
+#define QMOE_ATTN_G(G_)                                                                                          \
+  case G_:                                                                                                       \
+    return launch_decode<G_>(q, q_stride, pool, block_table, seq_lens, B, H, KV, page_size, max_pages, splits, \
+                             scale, out, workspace, s);
   switch (H / KV) {
-    case 1: return launch_decode<1>(q, pool, block_table, seq_lens, B, H, KV, page_size, max_pages, splits, scale, out, workspace, s);
-    case 2: return launch_decode<2>(q, pool, block_table, seq_lens, B, H, KV, page_size, max_pages, splits, scale, out, workspace, s);
-    case 4: return launch_decode<4>(q, pool, block_table, seq_lens, B, H, KV, page_size, max_pages, splits, scale, out, workspace, s);
-    case 8: return launch_decode<8>(q, pool, block_table, seq_lens, B, H, KV, page_size, max_pages, splits, scale, out, workspace, s);
+    QMOE_ATTN_G(1)
+    QMOE_ATTN_G(2)
+    QMOE_ATTN_G(4)
     default:
-      set_error("qmoe_paged_decode_attention: group size %d unsupported (1, 2, 4, 8)", H / KV);
+      set_error("qmoe_paged_decode_attention: group size %d unsupported (1, 2, 4)", H / KV);
       return QMOE_ERR_UNSUPPORTED;
   }
+#undef QMOE_ATTN_G
 }

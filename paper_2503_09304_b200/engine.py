@@ -328,13 +328,15 @@ class InferenceEngine:
             self._watch_stream = torch.cuda.Stream(device=dev)
             # per launch: where it stopped (device copy for the cursor advance, pinned copy + event
             # for the host), a ring of 256
-            self._stop_dev_ring = torch.zeros(256, dtype=torch.int32, device=dev)
+            # where each launch stopped: the kernel's cursor_out points into this pinned ring (the
+            # last CTA out stores it through UVA), read by the host after the next queue-length
+            # sync and by the resume-point kernel -- no extra launch or copy per layer
             self._stop_pinned = torch.zeros(256, dtype=torch.int32, pin_memory=True)
-            self._stop_events = [torch.cuda.Event() for _ in range(256)]
             # progress words: written by the GPU (system-scope stores), read here through numpy
             self._progress = torch.zeros(64, dtype=torch.int32, pin_memory=True)
             self._progress_np = self._progress.numpy()
-            self._stop_log = torch.zeros(4096, dtype=torch.int32, pin_memory=True)
+        if self._stop_marks and self._stop_marks[-1][4] is None:
+            self._resolve_stop_marks()  # before the launches of this iteration reuse ring slots
         slot = self._flag_slot = (self._flag_slot + 1) % 1024
         self._flags[(slot + 512) % 1024].zero_()
         self._flag = self._flags[slot:slot + 1]
@@ -370,8 +372,10 @@ class InferenceEngine:
         p = self._prev
         if p is None:
             return False
-        if sync:
-            self._stop_events[p.ring].synchronize()
+        if sync:  # a host-side PREEMPT answer: the iteration ends here anyway
+            import torch
+
+            torch.cuda.current_stream().synchronize()
         return int(self._stop_pinned[p.ring]) < self.model.config.num_experts
 
     def _preempt_void(self, batch: Batch, on_report: ReportCallback, layer: int) -> Preempted:
@@ -393,7 +397,7 @@ class InferenceEngine:
                 self.stats["flag_policy_disagree"] = self.stats.get("flag_policy_disagree", 0) + 1
         finally:
             self.in_rollback = False
-        self._resume_point(p, self._stop_dev_ring[p.ring:p.ring + 1])
+        self._resume_point(p, self._stop_pinned[p.ring:p.ring + 1])
         self._preempt_at["EXPERT_DEVICE_FLAG"] = self._preempt_at.get("EXPERT_DEVICE_FLAG", 0) + 1
         return self._preempt(p, p.layer, Stage.EXPERTS)
 
@@ -453,12 +457,9 @@ class InferenceEngine:
         flag = self._flag
         self._launch_seq += 1
         seq = self._launch_seq
-        stop_dev = m.run_experts(layer, xp, offsets, perm, st.y, 0, E, preempt_flag=flag, progress=self._progress,
-                                 progress_seq=seq)
         ring = self._ring_i = (self._ring_i + 1) % 256
-        self._stop_dev_ring[ring:ring + 1].copy_(stop_dev)
-        self._stop_pinned[ring:ring + 1].copy_(stop_dev, non_blocking=True)
-        self._stop_events[ring].record()
+        stop_dev = m.run_experts(layer, xp, offsets, perm, st.y, 0, E, preempt_flag=flag, progress=self._progress,
+                                 progress_seq=seq, cursor_out=self._stop_pinned[ring:ring + 1])
         self.stats["expert_launches"] += 1
         self._off_ready.synchronize()  # waits for the permute only; the GEMM keeps running
         if self._prev_voided(sync=False):  # the permute ran after the previous launch: its stop is in
@@ -494,10 +495,11 @@ class InferenceEngine:
             self._sig_src[slot] = stop
             with torch.cuda.stream(self._sig_stream):
                 flag.copy_(self._sig_src[slot:slot + 1], non_blocking=True)
-            # where the kernel really stopped, read back lazily (preemption_positions())
-            i = len(self._stop_marks) % self._stop_log.numel()
-            self._stop_log[i:i + 1].copy_(stop_dev, non_blocking=True)
-            self._stop_marks.append((i, stop, hit[-1] + 1, running))
+            # where the kernel really stopped: its ring slot, read once the launch is done (the next
+            # iterations' _begin_iteration, or preemption_positions)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._stop_marks.append([self._ring_i, hit[-1] + 1, running, ev, None])
             return stop_dev, True
         return stop_dev, False
 
@@ -512,6 +514,12 @@ class InferenceEngine:
             return
         perm, offsets, xp = st.q
         st.resume_q = (perm, rp(st.cursor, stop_dev, offsets), xp)
+
+    def _resolve_stop_marks(self) -> None:
+        for mark in self._stop_marks:
+            if mark[4] is None and mark[3].query():
+                mark[4] = int(self._stop_pinned[mark[0]])
+                mark[3] = None
 
     def _await_progress(self, prog, e: int, seq: int, timeout_s: float = 30.0) -> None:
         """Spin on the pinned progress word of expert e (a plain host read, ~100 ns)."""
@@ -532,9 +540,9 @@ class InferenceEngine:
         import torch
 
         torch.cuda.synchronize()
+        self._resolve_stop_marks()
         out = dict(self._preempt_at)
-        for (i, asked, end, running) in self._stop_marks:
-            got = int(self._stop_log[i])
+        for (_, end, running, _, got) in self._stop_marks:
             key = "EXPERT_MID_LAUNCH" if got < end else "EXPERT_END_OF_LAUNCH"
             out[key] = out.get(key, 0) + 1
             out["flag_raised_while_running"] = out.get("flag_raised_while_running", 0) + int(running)

@@ -231,9 +231,11 @@ def permute_launches(T: int, k: int, gather: bool = True) -> int:
 
 def paged_decode_attention(q: torch.Tensor, pool: torch.Tensor, block_table: torch.Tensor, seq_lens: torch.Tensor,
                            max_len: int, scale: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """q [B, H, hd] bf16, pool [n_pages, page, 2, KV, hd] bf16, block_table [B, max_pages] int32,
-    seq_lens [B] int32 -> out [B, H, hd] (one query token per sequence, all cached tokens)."""
-    _need(q, "q", torch.bfloat16)
+    """q [B, H, hd] bf16 (rows may be strided, e.g. a view into a packed qkv projection; the head
+    and feature dimensions must be dense), pool [n_pages, page, 2, KV, hd] bf16, block_table
+    [B, max_pages] int32, seq_lens [B] int32 -> out [B, H, hd] (one query per sequence)."""
+    if not q.is_cuda or q.dtype != torch.bfloat16 or q.stride(2) != 1 or q.stride(1) != q.shape[2]:
+        raise ValueError("q must be a CUDA bf16 [B, H, hd] tensor with dense heads")
     _need(pool, "pool", torch.bfloat16)
     _need(block_table, "block_table", torch.int32)
     _need(seq_lens, "seq_lens", torch.int32)
@@ -243,11 +245,12 @@ def paged_decode_attention(q: torch.Tensor, pool: torch.Tensor, block_table: tor
         raise ValueError("pool must be [n_pages, page, 2, KV, head_dim]")
     max_pages = block_table.shape[1]
     if out is None:
-        out = torch.empty_like(q)
+        out = torch.empty((B, H, hd), dtype=q.dtype, device=q.device)
     lib = _lib.load()
     nbytes = lib.qmoe_paged_decode_attention_workspace_bytes(B, KV, max_pages)
     ws = workspace(nbytes, "attn", q.device)
-    check(lib.qmoe_paged_decode_attention(_ptr(q), _ptr(pool), _ptr(block_table), _ptr(seq_lens), B, H, KV, hd, page,
+    check(lib.qmoe_paged_decode_attention(_ptr(q), q.stride(0), _ptr(pool), _ptr(block_table), _ptr(seq_lens), B, H,
+                                          KV, hd, page,
                                           max_pages, int(max_len), float(scale), _ptr(out), _ptr(ws), nbytes,
                                           _stream()), "qmoe_paged_decode_attention")
     return out
@@ -276,7 +279,7 @@ def resume_point(cursor: torch.Tensor, stop_dev: torch.Tensor, offsets: torch.Te
     """Advance the cursors to the stop and return the resumed launch's offsets (experts below the
     stop emptied); the launch reuses the preempted launch's perm and Xp."""
     _need(cursor, "cursor", torch.int32)
-    _need(stop_dev, "stop", torch.int32)
+    _need_stop(stop_dev)
     _need(offsets, "offsets", torch.int32)
     out = torch.empty_like(offsets)
     lib = _lib.load()
@@ -285,9 +288,16 @@ def resume_point(cursor: torch.Tensor, stop_dev: torch.Tensor, offsets: torch.Te
     return out
 
 
+def _need_stop(t: torch.Tensor) -> None:
+    """A launch's stop word: int32 in device memory or pinned host memory (device-accessible under
+    UVA; the engine's stop ring lives there so the host reads it without a copy)."""
+    if t.dtype != torch.int32 or not (t.is_cuda or t.is_pinned()):
+        raise ValueError("stop must be an int32 CUDA or pinned host tensor")
+
+
 def cursor_advance(cursor: torch.Tensor, stop_dev: torch.Tensor) -> None:
     _need(cursor, "cursor", torch.int32)
-    _need(stop_dev, "stop", torch.int32)
+    _need_stop(stop_dev)
     lib = _lib.load()
     check(lib.qmoe_cursor_advance(_ptr(cursor), cursor.shape[0], _ptr(stop_dev), _stream()), "qmoe_cursor_advance")
 

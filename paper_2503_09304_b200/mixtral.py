@@ -219,15 +219,16 @@ class DecoderMoEModel:
         return K.permute(ids, self.config.num_experts, cursor=cursor, x=x)
 
     def run_experts(self, layer: int, xp, offsets, perm, y, e_begin: int, e_end: int, preempt_flag=None,
-                    progress=None, progress_seq: int = 0):
+                    progress=None, progress_seq: int = 0, cursor_out=None):
         L = self.layers[layer]
         rows = xp.shape[0]
         F = self.cfg.ffn_dim
         act = K.workspace(rows * F * 2, "act", self.device).view(self.dtype)[: rows * F].view(rows, F)
+        stop = self._stop if cursor_out is None else cursor_out
         K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, L.gate_up, L.down, y, e_begin=e_begin, e_end=e_end,
-                     act_ws=act, preempt_flag=preempt_flag, cursor_out=self._stop, progress=progress,
+                     act_ws=act, preempt_flag=preempt_flag, cursor_out=stop, progress=progress,
                      progress_seq=progress_seq)
-        return self._stop
+        return stop
 
     def advance_cursor(self, cursor, stop_dev):
         K.cursor_advance(cursor, stop_dev)

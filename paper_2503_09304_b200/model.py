@@ -200,11 +200,12 @@ class MoEModel:
 
     def run_experts(self, layer: int, xp, offsets, perm, y, e_begin: int, e_end: int,
                     preempt_flag: Optional[torch.Tensor] = None, progress: Optional[torch.Tensor] = None,
-                    progress_seq: int = 0) -> torch.Tensor:
+                    progress_seq: int = 0, cursor_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        stop = self._stop if cursor_out is None else cursor_out  # device or pinned host int32 [1]
         K.expert_ffn(self.expert_variant, xp, offsets, perm, self.expert_weight[layer], self.expert_bias[layer], y,
-                     e_begin=e_begin, e_end=e_end, preempt_flag=preempt_flag, cursor_out=self._stop,
+                     e_begin=e_begin, e_end=e_end, preempt_flag=preempt_flag, cursor_out=stop,
                      progress=progress, progress_seq=progress_seq)
-        return self._stop
+        return stop
 
     def advance_cursor(self, cursor: torch.Tensor, stop_dev: torch.Tensor) -> None:
         K.cursor_advance(cursor, stop_dev)
