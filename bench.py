@@ -234,8 +234,21 @@ def run_serving(args) -> dict:
     from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, DecoderMoEModel
     from paper_2503_09304_b200.serving import compare, warm_up
 
-    model = DecoderMoEModel(MIXTRAL_8X7B)
-    warm_up(model)
+    import torch.distributed as dist
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    clock_factory = None
+    if world > 1:
+        # expert-parallel serving: experts sharded over the ranks, attention replicated, every
+        # rank runs the same scheduler on a clock shared through rank 0 (ep_serving.py)
+        from paper_2503_09304_b200.ep_serving import ExpertParallelDecoder, LockstepClock
+
+        model = ExpertParallelDecoder(MIXTRAL_8X7B, dist.get_rank(), world, device=torch.device("cuda", local_device()))
+        clock_factory = LockstepClock
+    else:
+        model = DecoderMoEModel(MIXTRAL_8X7B)
+    kw = {} if clock_factory is None else {"clock_factory": clock_factory}
+    warm_up(model, **kw)
     scheds = tuple(args.serve_schedulers.split(","))
     rates = [float(r) for r in args.serve_sweep.split(",")] if args.serve_sweep else [args.serve_rate]
     seeds = [int(s) for s in args.serve_seeds.split(",")]
@@ -244,7 +257,7 @@ def run_serving(args) -> dict:
         for seed in seeds:
             sampler = ClockSampler(torch.cuda.current_device())
             out = compare(model, rate, args.serve_duration, seed=seed, schedulers=scheds,
-                          kv_capacity_bytes=KV_GIB * 1024**3)
+                          kv_capacity_bytes=KV_GIB * 1024**3, **kw)
             out["clocks"] = sampler.stop()
             out["seed"] = seed
             for k in scheds:
@@ -257,6 +270,14 @@ def run_serving(args) -> dict:
                     f"iteration), paper workload (20% LS, Poisson), KV ledger {KV_GIB:.0f} GiB; qllm = the reference's "
                     f"Algorithm 1 + policy; qllm-arrival = LS-arrival-only preemption + BE continuous batching "
                     f"(sched.arrival_policy); LS arrivals raise the device preempt flag (no host round trip)")
+    if world > 1:
+        res["model"] = (f"mixtral-8x7b (32 layers, random-init bf16) expert-parallel over {world} GPUs (experts "
+                        f"{model.bounds}, attention replicated, expert outputs all-gathered over peer memory), "
+                        f"batch 32, SLO 3000 ms, paper workload, KV ledger {KV_GIB:.0f} GiB per rank; every rank "
+                        f"runs the same scheduler on rank 0's wall clock (LockstepClock, synced per iteration); "
+                        f"expert boundaries decided on the host before each launch")
+        res["ep"] = {"world": world, "bounds": model.bounds, "exchanges": model.stats["exchanges"],
+                     "backend": dist.get_backend()}
     return res
 
 
@@ -459,9 +480,10 @@ def run_ours(args, rank: int, world: int) -> None:
     dec_ms = statistics.median(a.elapsed_time(b) for a, b in dec)
     qwen = run_qwen_layer(dev, flush, world) if world == 1 else None
     serving = None
-    if world == 1 and args.serve_duration > 0:
+    if args.serve_duration > 0:
         del block, x, xd, flush
-        torch.cuda.empty_cache()
+        if world == 1:  # (N>1: the EP block's buffers are IPC-mapped by the peers; keep them cached)
+            torch.cuda.empty_cache()
         serving = run_serving(args)
     if rank != 0:
         return

@@ -324,6 +324,26 @@ QMOE_API int qmoe_ep_dispatch_dev(const void* x, const int32_t* perm, const int3
                                   void* const* x_peers, int32_t* const* ret_peers, int32_t* loc_offsets, void* stream);
 
 /*
+ * Replicated-attention expert parallelism (ep_serving.py; replaces nothing in the reference, which
+ * is single-process -- SURVEY.md §8(e)): every rank holds the same batch, permutes it over all E
+ * experts (identical perm / offsets on every rank) and runs the grouped GEMM on its own experts
+ * [e_lo, e_hi) only, writing y in slot order.  qmoe_ep_share_rows then stores the rows of queue
+ * positions [offsets[e_lo], offsets[e_hi]) into the same slot perm[r] of every peer's receive
+ * buffer (recv_peers[g], [slots, row_bytes]; recv_peers[me] is not written), NVLink stores, no
+ * host round trip.  After a qmoe_ep_barrier, qmoe_ep_collect_rows copies the rows of queue
+ * positions [offsets[e_begin], offsets[e_end]) minus [offsets[skip_lo], offsets[skip_hi]) (the
+ * rank's own experts) from the local receive buffer into y.  offsets: device [E+1]; max_rows: an
+ * upper bound of the queue rows (grid sizing).  A receive buffer must not be re-written before
+ * every rank collected from it (ep_serving.py alternates two, one barrier apart).
+ */
+QMOE_API int qmoe_ep_share_rows(const void* y, const int32_t* perm, const int32_t* offsets, int E, int e_lo, int e_hi,
+                                int max_rows, size_t row_bytes, void* const* recv_peers, int me, int world,
+                                void* stream);
+QMOE_API int qmoe_ep_collect_rows(const void* recv, void* y, const int32_t* perm, const int32_t* offsets, int E,
+                                  int e_begin, int e_end, int skip_lo, int skip_hi, int max_rows, size_t row_bytes,
+                                  void* stream);
+
+/*
  * Decoder-side fused helpers (outside the north-star path; used by the Mixtral/Qwen serving
  * plugin to cut per-layer launch counts).  bf16 only.
  * qmoe_rmsnorm: out = rmsnorm(x [+ residual_add]) * weight (HF MixtralRMSNorm rounding);
@@ -353,8 +373,10 @@ QMOE_API int qmoe_rope(void* q, void* k, const int64_t* positions, const float* 
  * seq_lens: [B] cached tokens incl. the new one (the query attends all of them); max_len >=
  * max(seq_lens) (host-known); scale: softmax scale.  out: [B, H, head_dim] bf16.  fp32 scores,
  * online softmax and accumulation; one CTA per (sequence, KV head, page), pages merged in order
- * by the last CTA (deterministic).  head_dim 128, H / KV in {1, 2, 4}.  workspace:
- * qmoe_paged_decode_attention_workspace_bytes(B, KV, max_pages) bytes, ZEROED once at allocation.
+ * by the last CTA (deterministic).  head_dim 128, H / KV in {1, 2, 4}, B * KV <= 8192.  workspace:
+ * qmoe_paged_decode_attention_workspace_bytes(B, KV, max_pages) bytes, ZEROED once at allocation;
+ * the arrival counters sit at its head at a fixed offset and each launch leaves them zeroed, so one
+ * workspace (of the largest size needed) serves calls of any shape, stream-ordered.
  */
 QMOE_API size_t qmoe_paged_decode_attention_workspace_bytes(int B, int KV, int max_pages);
 QMOE_API int qmoe_paged_decode_attention(const void* q, int q_stride, const void* pool, const int32_t* block_table,

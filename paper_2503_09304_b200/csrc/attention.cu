@@ -27,6 +27,10 @@ namespace {
 constexpr int kHd = 128;
 constexpr int kAttnWarps = 4;
 constexpr int kMaxG = 8;
+// Arrival counters sit at a FIXED offset (the head of the workspace) with a fixed capacity, so a
+// workspace reused across calls of different shapes keeps them zero: the page partials, which
+// every call fully rewrites before reading, never overlap them.
+constexpr int kMaxCounters = 8192;  // B * KV per call
 
 struct AttnPartial {
   float m[kMaxG], l[kMaxG];
@@ -190,8 +194,8 @@ paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
 template <int G>
 int launch_decode(const void* q, int q_stride, const void* pool, const int32_t* bt, const int32_t* lens, int B, int H,
                   int KV, int page, int max_pages, int splits, float scale, void* out, void* ws, cudaStream_t s) {
-  AttnPartial* parts = reinterpret_cast<AttnPartial*>(ws);
-  int* arrivals = reinterpret_cast<int*>(parts + (size_t)B * KV * max_pages);
+  int* arrivals = reinterpret_cast<int*>(ws);
+  AttnPartial* parts = reinterpret_cast<AttnPartial*>(arrivals + kMaxCounters);
   return launch_pdl("qmoe_paged_decode_attention", paged_decode_kernel<G>, dim3(B, KV, splits),
                     dim3(kAttnWarps * 32), 0, s, (const __nv_bfloat16*)q, (const __nv_bfloat16*)pool, bt, lens, H, KV,
                     page, max_pages, scale, (__nv_bfloat16*)out, parts, arrivals, q_stride);
@@ -201,7 +205,7 @@ int launch_decode(const void* q, int q_stride, const void* pool, const int32_t* 
 }  // namespace qmoe
 
 extern "C" size_t qmoe_paged_decode_attention_workspace_bytes(int B, int KV, int max_pages) {
-  return sizeof(qmoe::AttnPartial) * (size_t)B * KV * max_pages + sizeof(int) * (size_t)B * KV;
+  return sizeof(int) * (size_t)qmoe::kMaxCounters + sizeof(qmoe::AttnPartial) * (size_t)B * KV * max_pages;
 }
 
 extern "C" int qmoe_paged_decode_attention(const void* q, int q_stride, const void* pool, const int32_t* block_table,
@@ -212,6 +216,8 @@ extern "C" int qmoe_paged_decode_attention(const void* q, int q_stride, const vo
   QMOE_REQUIRE(head_dim == kHd, "qmoe_paged_decode_attention: head_dim must be %d (got %d)", kHd, head_dim);
   QMOE_REQUIRE(B >= 0 && KV >= 1 && H % KV == 0 && H / KV <= kMaxG, "qmoe_paged_decode_attention: bad heads H=%d KV=%d",
                H, KV);
+  QMOE_REQUIRE((size_t)B * KV <= (size_t)kMaxCounters, "qmoe_paged_decode_attention: B * KV %d > %d", B * KV,
+               kMaxCounters);
   QMOE_REQUIRE(q_stride >= H * head_dim, "qmoe_paged_decode_attention: q_stride %d < H * head_dim", q_stride);
   QMOE_REQUIRE(page_size >= 1 && max_pages >= 1 && max_len >= 1 && max_len <= page_size * max_pages,
                "qmoe_paged_decode_attention: bad paging (page %d, pages %d, max_len %d)", page_size, max_pages,

@@ -183,6 +183,49 @@ __global__ void __launch_bounds__(256) ep_dispatch_dev_kernel(const uint8_t* __r
   }
 }
 
+// Replicated-attention expert parallelism (ep_serving.py): every rank holds the whole batch (the
+// attention stage is replicated) and runs the grouped GEMM on its own experts only.  Afterwards
+// each rank pushes the output rows of its experts -- queue positions [offsets[e_lo],
+// offsets[e_hi]) of the launch, slot perm[r] -- into the same slot of every peer's receive buffer
+// (one warp per row, 16-byte stores over NVLink), a flag barrier orders the pushes, and each rank
+// copies the rows of the other ranks' experts in the launch range from its receive buffer into its
+// own slot-ordered y (ep_collect).  Slots outside the launch's queues (completed before a
+// preemption, or not routed) are never touched.
+__global__ void __launch_bounds__(256) ep_share_kernel(const uint8_t* __restrict__ y, const int32_t* __restrict__ perm,
+                                                       const int32_t* __restrict__ offsets, int e_lo, int e_hi,
+                                                       size_t row_bytes, void* const* __restrict__ recv_peers,
+                                                       int me, int world) {
+  const int r0 = offsets[e_lo], r1 = offsets[e_hi];
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = r0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < r1; r += warps) {
+    const size_t off = (size_t)perm[r] * row_bytes;
+    const uint4* src = reinterpret_cast<const uint4*>(y + off);
+    for (size_t c = lane; c < row_bytes / 16; c += 32) {
+      const uint4 v = src[c];
+      for (int g = 0; g < world; ++g)
+        if (g != me) reinterpret_cast<uint4*>(static_cast<uint8_t*>(recv_peers[g]) + off)[c] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) ep_collect_kernel(const uint8_t* __restrict__ recv, uint8_t* __restrict__ y,
+                                                         const int32_t* __restrict__ perm,
+                                                         const int32_t* __restrict__ offsets, int e_begin, int e_end,
+                                                         int skip_lo, int skip_hi, size_t row_bytes) {
+  const int r0 = offsets[e_begin], r1 = offsets[e_end];
+  const int s0 = offsets[skip_lo], s1 = offsets[skip_hi];
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = r0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < r1; r += warps) {
+    if (r >= s0 && r < s1) continue;  // this rank's own experts: computed in place
+    const size_t off = (size_t)perm[r] * row_bytes;
+    const uint4* src = reinterpret_cast<const uint4*>(recv + off);
+    uint4* dst = reinterpret_cast<uint4*>(y + off);
+    for (size_t c = lane; c < row_bytes / 16; c += 32) dst[c] = src[c];
+  }
+}
+
 PFN_cuMemGetAddressRange_v3020 g_range = nullptr;
 std::once_flag g_range_once;
 std::mutex g_ipc_mu;
@@ -292,4 +335,40 @@ extern "C" int qmoe_ep_dispatch_dev(const void* x, const int32_t* perm, const in
                                                               row_bytes, me, world, counts, bounds, x_peers,
                                                               ret_peers, loc_offsets);
   return check_launch("qmoe_ep_dispatch_dev");
+}
+
+extern "C" int qmoe_ep_share_rows(const void* y, const int32_t* perm, const int32_t* offsets, int E, int e_lo, int e_hi,
+                                  int max_rows, size_t row_bytes, void* const* recv_peers, int me, int world,
+                                  void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(E >= 1 && 0 <= e_lo && e_lo <= e_hi && e_hi <= E, "qmoe_ep_share_rows: bad expert range [%d, %d) of %d",
+               e_lo, e_hi, E);
+  QMOE_REQUIRE(world >= 1 && world <= 32 && me >= 0 && me < world, "qmoe_ep_share_rows: bad rank %d/%d", me, world);
+  QMOE_REQUIRE(row_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0,
+               "qmoe_ep_share_rows: rows must be 16-byte multiples and aligned");
+  if (e_lo == e_hi || max_rows <= 0 || world == 1) return QMOE_OK;
+  QMOE_REQUIRE(y && perm && offsets && recv_peers, "qmoe_ep_share_rows: null pointer");
+  const int grid = max_rows / 8 + 1 < 148 * 4 ? max_rows / 8 + 1 : 148 * 4;
+  ep_share_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint8_t*>(y), perm, offsets, e_lo, e_hi,
+                                                       row_bytes, recv_peers, me, world);
+  return check_launch("qmoe_ep_share_rows");
+}
+
+extern "C" int qmoe_ep_collect_rows(const void* recv, void* y, const int32_t* perm, const int32_t* offsets, int E,
+                                    int e_begin, int e_end, int skip_lo, int skip_hi, int max_rows, size_t row_bytes,
+                                    void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(E >= 1 && 0 <= e_begin && e_begin <= e_end && e_end <= E && 0 <= skip_lo && skip_lo <= skip_hi &&
+                   skip_hi <= E,
+               "qmoe_ep_collect_rows: bad expert ranges [%d, %d) / [%d, %d) of %d", e_begin, e_end, skip_lo, skip_hi,
+               E);
+  QMOE_REQUIRE(row_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(recv) % 16 == 0,
+               "qmoe_ep_collect_rows: rows must be 16-byte multiples and aligned");
+  if (e_begin == e_end || max_rows <= 0) return QMOE_OK;
+  QMOE_REQUIRE(recv && y && perm && offsets, "qmoe_ep_collect_rows: null pointer");
+  const int grid = max_rows / 8 + 1 < 148 * 4 ? max_rows / 8 + 1 : 148 * 4;
+  ep_collect_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint8_t*>(recv), static_cast<uint8_t*>(y),
+                                                         perm, offsets, e_begin, e_end, skip_lo, skip_hi, row_bytes);
+  return check_launch("qmoe_ep_collect_rows");
 }

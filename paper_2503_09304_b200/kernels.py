@@ -455,6 +455,35 @@ def ep_dispatch_dev(x: torch.Tensor, perm: torch.Tensor, offsets: torch.Tensor, 
                                    _ptr(loc_offsets), _stream()), "qmoe_ep_dispatch_dev")
 
 
+def ep_share_rows(y: torch.Tensor, perm: torch.Tensor, offsets: torch.Tensor, e_lo: int, e_hi: int,
+                  recv_peers: torch.Tensor, me: int, world: int) -> None:
+    """Push the output rows of experts [e_lo, e_hi) (queue positions of the launch) into the same
+    slots of every peer's receive buffer (qmoe.h)."""
+    _need(y, "y")
+    _need(perm, "perm", torch.int32)
+    _need(offsets, "offsets", torch.int32)
+    _need(recv_peers, "recv_peers", torch.int64)
+    lib = _lib.load()
+    check(lib.qmoe_ep_share_rows(_ptr(y), _ptr(perm), _ptr(offsets), offsets.shape[0] - 1, e_lo, e_hi, y.shape[0],
+                                 y.shape[1] * y.element_size(), _ptr(recv_peers), me, world, _stream()),
+          "qmoe_ep_share_rows")
+
+
+def ep_collect_rows(recv: torch.Tensor, y: torch.Tensor, perm: torch.Tensor, offsets: torch.Tensor, e_begin: int,
+                    e_end: int, skip_lo: int, skip_hi: int) -> None:
+    """y[perm[r]] = recv[perm[r]] for the launch's queue positions of the other ranks' experts."""
+    _need(y, "y")
+    _need(recv, "recv", y.dtype)
+    _need(perm, "perm", torch.int32)
+    _need(offsets, "offsets", torch.int32)
+    if recv.shape[0] < y.shape[0] or recv.shape[1] != y.shape[1]:
+        raise ValueError("recv must hold at least y's slots")
+    lib = _lib.load()
+    check(lib.qmoe_ep_collect_rows(_ptr(recv), _ptr(y), _ptr(perm), _ptr(offsets), offsets.shape[0] - 1, e_begin,
+                                   e_end, skip_lo, skip_hi, y.shape[0], y.shape[1] * y.element_size(), _stream()),
+          "qmoe_ep_collect_rows")
+
+
 def expert_ffn_peer_ex(xp: torch.Tensor, offsets: torch.Tensor, ret: torch.Tensor, gate_up: torch.Tensor,
                        down: torch.Tensor, y_peers: torch.Tensor, rows_hint: int, act_ws: torch.Tensor,
                        e_begin: int = 0, e_end: Optional[int] = None, preempt_flag: Optional[torch.Tensor] = None,

@@ -65,7 +65,10 @@ class DecoderMoEModel:
     kv_page_kwargs = {"page_size": 256, "initial_pages": 384}
 
     def __init__(self, cfg: DecoderConfig, device: Optional[torch.device] = None, seed: int = 0,
-                 dtype: torch.dtype = torch.bfloat16):
+                 dtype: torch.dtype = torch.bfloat16, expert_range: Optional[tuple[int, int]] = None):
+        """expert_range: hold the weights of engine-view experts [lo, hi) only (expert parallelism,
+        ep_serving.py); the random draws are those of the full model, so every rank's experts equal
+        the single-GPU model's."""
         self.cfg = cfg
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.dtype = dtype
@@ -74,6 +77,10 @@ class DecoderMoEModel:
         S = shared_sub_experts(cfg.shared_ffn_dim, cfg.ffn_dim) if cfg.shared_ffn_dim else 0
         self.n_shared = S
         self.config = replace(cfg, num_experts=cfg.num_experts + S, top_k=cfg.top_k + S)  # engine view
+        lo, hi = expert_range if expert_range is not None else (0, cfg.num_experts + S)
+        if not 0 <= lo < hi <= cfg.num_experts + S:
+            raise ValueError(f"bad expert range [{lo}, {hi}) of {cfg.num_experts + S}")
+        self.e_lo, self.e_hi = lo, hi
         from flash_attn import flash_attn_varlen_func, flash_attn_with_kvcache
 
         self._fa_varlen, self._fa_kvcache = flash_attn_varlen_func, flash_attn_with_kvcache
@@ -94,15 +101,23 @@ class DecoderMoEModel:
             L.w_o = rnd((d, H * hd), (H * hd) ** -0.5)
             L.w_router = torch.empty((E + (1 if S else 0), d), dtype=dtype, device=self.device)
             L.w_router[:E] = rnd((E, d), d ** -0.5)
-            L.gate_up = torch.empty((E + S, 2 * F, d), dtype=dtype, device=self.device)
-            L.down = torch.empty((E + S, d, F), dtype=dtype, device=self.device)
+            L.gate_up = torch.empty((hi - lo, 2 * F, d), dtype=dtype, device=self.device)
+            L.down = torch.empty((hi - lo, d, F), dtype=dtype, device=self.device)
             for e in range(E):  # per expert to bound the fp32 temporary
-                L.gate_up[e] = rnd((2 * F, d), d ** -0.5)
-                L.down[e] = rnd((d, F), F ** -0.5)
+                gu, dn = rnd((2 * F, d), d ** -0.5), rnd((d, F), F ** -0.5)
+                if lo <= e < hi:
+                    L.gate_up[e - lo], L.down[e - lo] = gu, dn
             if S:
                 Fs = cfg.shared_ffn_dim
                 sh_gate_up = rnd((2 * Fs, d), d ** -0.5)
-                pack_shared(L.gate_up, L.down, E, sh_gate_up[:Fs], sh_gate_up[Fs:], rnd((d, Fs), Fs ** -0.5))
+                if hi - lo == E + S:
+                    pack_shared(L.gate_up, L.down, E, sh_gate_up[:Fs], sh_gate_up[Fs:], rnd((d, Fs), Fs ** -0.5))
+                else:
+                    sgu = torch.empty((S, 2 * F, d), dtype=dtype, device=self.device)
+                    sdn = torch.empty((S, d, F), dtype=dtype, device=self.device)
+                    pack_shared(sgu, sdn, 0, sh_gate_up[:Fs], sh_gate_up[Fs:], rnd((d, Fs), Fs ** -0.5))
+                    for e in range(max(lo, E), hi):
+                        L.gate_up[e - lo], L.down[e - lo] = sgu[e - E], sdn[e - E]
                 L.w_router[E:] = rnd((1, d), d ** -0.5)  # the shared expert's sigmoid gate
             self.layers.append(L)
         self.final_norm = torch.ones(d, dtype=dtype, device=self.device)

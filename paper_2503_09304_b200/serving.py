@@ -31,13 +31,15 @@ def kv_pages_for(model, capacity_bytes: float, max_batch_size: int) -> dict:
 
 
 def serve_once(model, trace, scheduler: str, max_batch_size: int = 32, slo_ms: float = 3000.0,
-               kv_capacity_bytes: Optional[float] = None) -> dict:
+               kv_capacity_bytes: Optional[float] = None, clock_factory=WallClock) -> dict:
+    """clock_factory: WallClock (one GPU) or, for expert-parallel serving, a LockstepClock shared
+    by the ranks (ep_serving.py); every rank then runs this same call."""
     torch.cuda.synchronize()
     extra = {}
     if kv_capacity_bytes is not None:
         extra = {"cache_capacity_bytes": kv_capacity_bytes,
                  "kv_page_kwargs": kv_pages_for(model, kv_capacity_bytes, max_batch_size)}
-    sim = Simulation(trace, model=model, scheduler=scheduler, max_batch_size=max_batch_size, clock=WallClock(),
+    sim = Simulation(trace, model=model, scheduler=scheduler, max_batch_size=max_batch_size, clock=clock_factory(),
                      **extra)
     t0 = time.perf_counter()
     res = sim.run()
@@ -82,18 +84,19 @@ def serve_once(model, trace, scheduler: str, max_batch_size: int = 32, slo_ms: f
     return out
 
 
-def warm_up(model, max_batch_size: int = 32) -> None:
+def warm_up(model, max_batch_size: int = 32, clock_factory=WallClock) -> None:
     """Short run through prefill, decode and preemption so later timings exclude one-time init."""
     warm = trace_for_rate(WorkloadSpec(duration_s=2.0, prompt_mean=64, output_mean=8), 4.0, seed=99)
-    serve_once(model, warm, "qllm", max_batch_size)
+    serve_once(model, warm, "qllm", max_batch_size, clock_factory=clock_factory)
 
 
 def compare(model, rate: float, duration_s: float, seed: int = 0, max_batch_size: int = 32,
             slo_ms: float = 3000.0, schedulers=("baseline", "qllm"), workload: Optional[WorkloadSpec] = None,
-            kv_capacity_bytes: Optional[float] = None) -> dict:
+            kv_capacity_bytes: Optional[float] = None, clock_factory=WallClock) -> dict:
     trace = trace_for_rate(replace(workload or WorkloadSpec(), duration_s=duration_s), rate, seed=seed)
     out = {"rate": rate, "duration_s": duration_s, "jobs": len(trace), "slo_ms": slo_ms,
            "kv_capacity_gib": (kv_capacity_bytes or 8 * 1024**3) / 1024**3}
     for s in schedulers:
-        out["fcfs" if s == "baseline" else s] = serve_once(model, trace, s, max_batch_size, slo_ms, kv_capacity_bytes)
+        out["fcfs" if s == "baseline" else s] = serve_once(model, trace, s, max_batch_size, slo_ms, kv_capacity_bytes,
+                                                            clock_factory)
     return out

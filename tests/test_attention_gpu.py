@@ -51,6 +51,19 @@ def test_paged_decode_matches_torch(cuda, H, KV, lens):
     assert torch.equal(K.paged_decode_attention(q, pool, bt, ln, max(lens), scale), got)
 
 
+def test_workspace_reused_across_shapes(cuda):
+    """Decode batches change shape every iteration and share one workspace: a small call after a
+    large one must not find stale page partials where its arrival counters are (a bug this caught:
+    counters placed after the shape-dependent partials)."""
+    scale = 128 ** -0.5
+    for H, KV, lens in [(32, 8, [700, 3, 129, 512, 1]), (16, 16, [300] * 8), (16, 8, [1]), (32, 8, [5, 260]),
+                        (16, 16, [1, 2]), (32, 8, [900])]:
+        q, pool, bt, ln = _case(H, KV, lens, seed=len(lens))
+        got = K.paged_decode_attention(q, pool, bt, ln, max(lens), scale)
+        ref = _torch_ref(q, pool, bt, ln, scale)
+        assert (got.float() - ref).abs().max().item() < 2e-2, (H, KV, lens)
+
+
 def test_paged_decode_matches_flash_attn(cuda):
     fa = pytest.importorskip("flash_attn")
     lens = [180 + 37 * i for i in range(32)]
