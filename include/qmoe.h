@@ -373,7 +373,7 @@ QMOE_API int qmoe_rope(void* q, void* k, const int64_t* positions, const float* 
  * seq_lens: [B] cached tokens incl. the new one (the query attends all of them); max_len >=
  * max(seq_lens) (host-known); scale: softmax scale.  out: [B, H, head_dim] bf16.  fp32 scores,
  * online softmax and accumulation; one CTA per (sequence, KV head, page), pages merged in order
- * by the last CTA (deterministic).  head_dim 128, H / KV in {1, 2, 4}, B * KV <= 8192.  workspace:
+ * by the last CTA (deterministic).  head_dim 64 or 128, H / KV in {1, 2, 4}, B * KV <= 8192.  workspace:
  * qmoe_paged_decode_attention_workspace_bytes(B, KV, max_pages) bytes, ZEROED once at allocation;
  * the arrival counters sit at its head at a fixed offset and each launch leaves them zeroed, so one
  * workspace (of the largest size needed) serves calls of any shape, stream-ordered.

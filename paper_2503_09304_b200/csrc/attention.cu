@@ -37,7 +37,7 @@ struct AttnPartial {
   float o[kMaxG][kHd];
 };
 
-template <int G>
+template <int G, int HD>
 __global__ void __launch_bounds__(kAttnWarps * 32)
 paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ pool,
                     const int32_t* __restrict__ block_table, const int32_t* __restrict__ seq_lens, int H, int KV,
@@ -50,29 +50,30 @@ paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
   const int npages = (len + page - 1) / page;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ float s_m[kAttnWarps][G], s_l[kAttnWarps][G];
-  __shared__ float s_o[kAttnWarps][G][kHd];
+  constexpr int CPL = HD / 32;  // feature columns per lane in the value pass
+  __shared__ float s_o[kAttnWarps][G][HD];
   __shared__ int s_last;
-  float m[G], l[G], o[G][4];
+  float m[G], l[G], o[G][CPL];
 #pragma unroll
   for (int h = 0; h < G; ++h) {
     m[h] = -INFINITY;
     l[h] = 0.f;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) o[h][c] = 0.f;
+    for (int c = 0; c < CPL; ++c) o[h][c] = 0.f;
   }
   // query heads g*G .. g*G+G-1 (scaled, fp32) in shared memory: every lane reads them as
   // broadcasts while it walks its own token's K row
-  __shared__ __align__(16) float s_q[G][kHd];
-  for (int i = threadIdx.x; i < G * kHd; i += blockDim.x)
-    s_q[i / kHd][i % kHd] = __bfloat162float(q[(size_t)b * q_stride + (size_t)g * G * kHd + i]) * scale;
+  __shared__ __align__(16) float s_q[G][HD];
+  for (int i = threadIdx.x; i < G * HD; i += blockDim.x)
+    s_q[i / HD][i % HD] = __bfloat162float(q[(size_t)b * q_stride + (size_t)g * G * HD + i]) * scale;
   __syncthreads();
   if (sp < npages) {
     const int pg = block_table[(size_t)b * max_pages + sp];
     const int t0 = sp * page;
     const int tn = min(page, len - t0);  // tokens of this page
-    const size_t tok_stride = (size_t)2 * KV * kHd;  // elements between consecutive tokens
-    const __nv_bfloat16* kbase = pool + (size_t)pg * page * tok_stride + (size_t)g * kHd;
-    const __nv_bfloat16* vbase = kbase + (size_t)KV * kHd;
+    const size_t tok_stride = (size_t)2 * KV * HD;  // elements between consecutive tokens
+    const __nv_bfloat16* kbase = pool + (size_t)pg * page * tok_stride + (size_t)g * HD;
+    const __nv_bfloat16* vbase = kbase + (size_t)KV * HD;
     for (int blk = warp * 32; blk < tn; blk += kAttnWarps * 32) {
       const int t = blk + lane;
       const bool valid = t < tn;
@@ -82,7 +83,7 @@ paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
       if (valid) {
         const uint4* kr = reinterpret_cast<const uint4*>(kbase + (size_t)t * tok_stride);
 #pragma unroll 4
-        for (int i = 0; i < kHd / 8; ++i) {
+        for (int i = 0; i < HD / 8; ++i) {
           const uint4 u = __ldg(kr + i);
           const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
           float kf[8];
@@ -116,21 +117,28 @@ paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
         l[h] = l[h] * corr + ps;
         m[h] = mn;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) o[h][c] *= corr;
+        for (int c = 0; c < CPL; ++c) o[h][c] *= corr;
       }
-      // values: lane owns columns 4*lane .. 4*lane+3; token j's V row is read by the whole warp
+      // values: lane owns columns CPL*lane .. CPL*lane+CPL-1; token j's V row is read by the whole warp
       const int nb = min(32, tn - blk);
       for (int j = 0; j < nb; ++j) {
-        const uint2 u = __ldg(reinterpret_cast<const uint2*>(vbase + (size_t)(blk + j) * tok_stride) + lane);
-        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-        const float2 a = __bfloat1622float2(p2[0]), c2 = __bfloat1622float2(p2[1]);
+        float vf[CPL];
+        const __nv_bfloat16* vr = vbase + (size_t)(blk + j) * tok_stride;
+        if constexpr (CPL == 4) {
+          const uint2 u = __ldg(reinterpret_cast<const uint2*>(vr) + lane);
+          const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+          const float2 a = __bfloat1622float2(p2[0]), c2 = __bfloat1622float2(p2[1]);
+          vf[0] = a.x; vf[1] = a.y; vf[2] = c2.x; vf[3] = c2.y;
+        } else {
+          const unsigned u = __ldg(reinterpret_cast<const unsigned*>(vr) + lane);
+          const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+          vf[0] = a.x; vf[1] = a.y;
+        }
 #pragma unroll
         for (int h = 0; h < G; ++h) {
           const float pj = __shfl_sync(0xffffffffu, p[h], j);
-          o[h][0] += pj * a.x;
-          o[h][1] += pj * a.y;
-          o[h][2] += pj * c2.x;
-          o[h][3] += pj * c2.y;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) o[h][c] += pj * vf[c];
         }
       }
     }
@@ -143,12 +151,12 @@ paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
       s_l[warp][h] = l[h];
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) s_o[warp][h][4 * lane + c] = o[h][c];
+    for (int c = 0; c < CPL; ++c) s_o[warp][h][CPL * lane + c] = o[h][c];
   }
   __syncthreads();
   AttnPartial* part = parts + ((size_t)b * KV + g) * max_pages + sp;
-  for (int i = threadIdx.x; i < G * kHd; i += blockDim.x) {
-    const int h = i / kHd, c = i - h * kHd;
+  for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
+    const int h = i / HD, c = i - h * HD;
     float mm = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kAttnWarps; ++w) mm = fmaxf(mm, s_m[w][h]);
@@ -175,8 +183,8 @@ paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
   __threadfence();
   const AttnPartial* ps = parts + ((size_t)b * KV + g) * max_pages;
   const int used = min(npages, nsp);
-  for (int i = threadIdx.x; i < G * kHd; i += blockDim.x) {
-    const int h = i / kHd, c = i - h * kHd;
+  for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
+    const int h = i / HD, c = i - h * HD;
     float mm = -INFINITY;
     for (int s2 = 0; s2 < used; ++s2) mm = fmaxf(mm, ps[s2].m[h]);
     float acc = 0.f, ll = 0.f;
@@ -186,17 +194,17 @@ paged_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
       acc += f * ps[s2].o[h][c];
       ll += f * ps[s2].l[h];
     }
-    out[((size_t)b * H + g * G + h) * kHd + c] = __float2bfloat16_rn(ll > 0.f ? acc / ll : 0.f);
+    out[((size_t)b * H + g * G + h) * HD + c] = __float2bfloat16_rn(ll > 0.f ? acc / ll : 0.f);
   }
   if (threadIdx.x == 0) arrivals[b * KV + g] = 0;
 }
 
-template <int G>
+template <int G, int HD>
 int launch_decode(const void* q, int q_stride, const void* pool, const int32_t* bt, const int32_t* lens, int B, int H,
                   int KV, int page, int max_pages, int splits, float scale, void* out, void* ws, cudaStream_t s) {
   int* arrivals = reinterpret_cast<int*>(ws);
   AttnPartial* parts = reinterpret_cast<AttnPartial*>(arrivals + kMaxCounters);
-  return launch_pdl("qmoe_paged_decode_attention", paged_decode_kernel<G>, dim3(B, KV, splits),
+  return launch_pdl("qmoe_paged_decode_attention", paged_decode_kernel<G, HD>, dim3(B, KV, splits),
                     dim3(kAttnWarps * 32), 0, s, (const __nv_bfloat16*)q, (const __nv_bfloat16*)pool, bt, lens, H, KV,
                     page, max_pages, scale, (__nv_bfloat16*)out, parts, arrivals, q_stride);
 }
@@ -213,7 +221,8 @@ extern "C" int qmoe_paged_decode_attention(const void* q, int q_stride, const vo
                                            int page_size, int max_pages, int max_len, float scale, void* out,
                                            void* workspace, size_t workspace_bytes, void* stream) {
   using namespace qmoe;
-  QMOE_REQUIRE(head_dim == kHd, "qmoe_paged_decode_attention: head_dim must be %d (got %d)", kHd, head_dim);
+  QMOE_REQUIRE(head_dim == 128 || head_dim == 64, "qmoe_paged_decode_attention: head_dim must be 64 or 128 (got %d)",
+               head_dim);
   QMOE_REQUIRE(B >= 0 && KV >= 1 && H % KV == 0 && H / KV <= kMaxG, "qmoe_paged_decode_attention: bad heads H=%d KV=%d",
                H, KV);
   QMOE_REQUIRE((size_t)B * KV <= (size_t)kMaxCounters, "qmoe_paged_decode_attention: B * KV %d > %d", B * KV,
@@ -232,8 +241,10 @@ extern "C" int qmoe_paged_decode_attention(const void* q, int q_stride, const vo
   cudaStream_t s = as_stream(stream);
 #define QMOE_ATTN_G(G_)                                                                                          \
   case G_:                                                                                                       \
-    return launch_decode<G_>(q, q_stride, pool, block_table, seq_lens, B, H, KV, page_size, max_pages, splits, \
-                             scale, out, workspace, s);
+    return head_dim == 128 ? launch_decode<G_, 128>(q, q_stride, pool, block_table, seq_lens, B, H, KV, page_size,   \
+                                                    max_pages, splits, scale, out, workspace, s)                  \
+                           : launch_decode<G_, 64>(q, q_stride, pool, block_table, seq_lens, B, H, KV, page_size,    \
+                                                   max_pages, splits, scale, out, workspace, s);
   switch (H / KV) {
     QMOE_ATTN_G(1)
     QMOE_ATTN_G(2)

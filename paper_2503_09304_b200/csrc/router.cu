@@ -432,6 +432,7 @@ int launch_router_mma(const void* x, const void* wr, int T_, int d, int E, int k
     const char* v = getenv("QMOE_ROUTER_MT");
     return v == nullptr ? 0 : atoi(v);
   }();
+  if (mt_env == 4 && E > 32) return launch_router_mma_np<4, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s);
   const bool two = mt_env ? mt_env == 2 : T_ >= 6144;
   if (E <= 16)
     return d % 256 == 0 ? (two ? launch_router_mma_np<1, 2, 256>(x, wr, T_, d, E, k, mode, ids, w, logits, s)
@@ -472,8 +473,8 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return v;
 }
 
-template <int DS, int NQ, int NTW, int U>
-__global__ void __launch_bounds__(DS * NQ * 32)
+template <int DS, int NQ, int NTW, int U, int MINB = 1>
+__global__ void __launch_bounds__(DS * NQ * 32, MINB)
 router_stream_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr, int ntok, int d,
                      int E, int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
                      float* __restrict__ logits_out) {
@@ -556,10 +557,10 @@ router_stream_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* _
   }
 }
 
-template <int DS, int NQ, int NTW, int U>
+template <int DS, int NQ, int NTW, int U, int MINB = 1>
 int launch_router_stream(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
                          void* logits, cudaStream_t s) {
-  return launch_pdl("qmoe_router(stream)", router_stream_kernel<DS, NQ, NTW, U>, dim3((T_ + 15) / 16),
+  return launch_pdl("qmoe_router(stream)", router_stream_kernel<DS, NQ, NTW, U, MINB>, dim3((T_ + 15) / 16),
                     dim3(DS * NQ * 32), 0, s, (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode,
                     ids, (float*)w, (float*)logits);
 }
@@ -588,8 +589,15 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
   // cp.async kernel's 32-token tiles halve the W re-reads.
   // ncu at 8k tokens: <8,1,1,4> reads 67 MB in 24 us (2.8 TB/s) at 128 registers = 2 CTAs/SM, so
   // 512 CTAs take 1.7 waves; U = 2 halves the register buffers (4 CTAs/SM: one wave).
+#define QMOE_TRY_STREAM_MINB(DS, NQ, NTW, U, MINB)                                                  \
+  if (d % ((DS) * 32 * (U)) == 0) {                                                                  \
+    *st = launch_router_stream<DS, NQ, NTW, U, MINB>(x, wr, T_, d, E, k, mode, ids, w, logits, s); \
+    return 1;                                                                                        \
+  }
   if (E <= 8) {
     if (cfg == 1) { QMOE_TRY_STREAM(8, 1, 1, 4) }
+    if (cfg == 3) { QMOE_TRY_STREAM_MINB(8, 1, 1, 2, 4) }
+    if (cfg == 4) { QMOE_TRY_STREAM_MINB(4, 1, 1, 2, 8) }
     if (cfg == 2 || (cfg == 0 && T_ < 4096)) { QMOE_TRY_STREAM(16, 1, 1, 2) }
     QMOE_TRY_STREAM(8, 1, 1, 2)
   } else if (E <= 16) {
@@ -602,6 +610,7 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
     if (T_ < 4096) { QMOE_TRY_STREAM(4, 4, 2, 2) }
   }
 #undef QMOE_TRY_STREAM
+#undef QMOE_TRY_STREAM_MINB
   return 0;
 }
 

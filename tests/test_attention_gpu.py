@@ -51,6 +51,15 @@ def test_paged_decode_matches_torch(cuda, H, KV, lens):
     assert torch.equal(K.paged_decode_attention(q, pool, bt, ln, max(lens), scale), got)
 
 
+@pytest.mark.parametrize("H,KV", [(8, 2), (4, 4)])
+def test_paged_decode_head_dim_64(cuda, H, KV):
+    lens = [1, 64, 300, 513]
+    q, pool, bt, ln = _case(H, KV, lens, hd=64, seed=9)
+    got = K.paged_decode_attention(q, pool, bt, ln, max(lens), 64 ** -0.5)
+    ref = _torch_ref(q, pool, bt, ln, 64 ** -0.5)
+    assert (got.float() - ref).abs().max().item() < 2e-2
+
+
 def test_workspace_reused_across_shapes(cuda):
     """Decode batches change shape every iteration and share one workspace: a small call after a
     large one must not find stale page partials where its arrival counters are (a bug this caught:

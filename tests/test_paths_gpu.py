@@ -158,7 +158,11 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("env", [{}, {"QMOE_SWAP_PAIR": "0"}], ids=["default-paths", "token-row-tiles"])
+ENVS = {"default-paths": ({}, {1, 6}), "token-row-tiles": ({"QMOE_SWAP_PAIR": "0"}, {1, 2}),
+        "pair-tiles": ({"QMOE_SWAP_PAIR": "0", "QMOE_CTA_PAIR": "1"}, {1, 3})}
+
+
+@pytest.mark.parametrize("env", list(ENVS))
 def test_preempt_flag_raised_mid_launch(cuda, env):
     """The device flag raised by another stream WHILE the grouped GEMM runs (the serving engine's
     wall-clock path) on every bf16 kernel path: the launch stops at an expert boundary >= 2 (or runs
@@ -167,11 +171,12 @@ def test_preempt_flag_raised_mid_launch(cuda, env):
     cases = [(32, 2048, 4096, 8, 2, d) for d in (0, 20000, 200000)]           # swap-AB
     cases += [(1200, 2048, 4096, 8, 2, d) for d in (0, 20000, 60000)]        # swap-AB pair / fused 128-row tiles
     cases += [(3000, 1024, 1408, 60, 4, d) for d in (0, 10000, 30000)]       # swap-AB pair / fused 256-row pair
+    env, paths = ENVS[env]
     out = subprocess.run([sys.executable, "-c", RACE, str(ROOT), json.dumps(cases)], capture_output=True, text=True,
                          env={**os.environ, **env}, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     res = json.loads(out.stdout.strip().splitlines()[-1])
-    assert {r["path"] for r in res} >= ({1, 6} if not env else {1, 2, 3}), res
+    assert {r["path"] for r in res} >= paths, res
     assert any(r["stop"] < 8 for r in res), res  # at least some launches really stopped mid-way
     for r in res:
         assert r["stop"] >= 2, r
