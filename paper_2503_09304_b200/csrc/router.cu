@@ -596,7 +596,9 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
   }
   if (E <= 8) {
     if (cfg == 1) { QMOE_TRY_STREAM(8, 1, 1, 4) }
-    if (cfg == 3) { QMOE_TRY_STREAM_MINB(8, 1, 1, 2, 4) }
+    // from ~6k tokens: 64 registers so 4 CTAs fit an SM and 512+ CTAs run in one wave (the
+    // 3-per-SM build leaves a 15% second wave: 29.5 -> 26.5 us at 8k tokens, 52 -> 44 us at 16k)
+    if (cfg == 3 || (cfg == 0 && T_ >= 6144)) { QMOE_TRY_STREAM_MINB(8, 1, 1, 2, 4) }
     if (cfg == 4) { QMOE_TRY_STREAM_MINB(4, 1, 1, 2, 8) }
     if (cfg == 2 || (cfg == 0 && T_ < 4096)) { QMOE_TRY_STREAM(16, 1, 1, 2) }
     QMOE_TRY_STREAM(8, 1, 1, 2)

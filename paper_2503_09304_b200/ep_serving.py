@@ -44,8 +44,12 @@ from .mixtral import DecoderConfig, DecoderMoEModel
 
 
 class LockstepClock:
-    """Milliseconds shared by the ranks: rank 0's wall clock at every sync(), plus the engine's
-    charges in between.  virtual=True: the engine keeps the host-boundary (replicable) expert
+    """Milliseconds shared by the ranks: rank 0's wall clock at every sync(), advanced in between
+    by the engine's cost-model charges times a scale that tracks the ratio of wall time to charged
+    time over the previous iterations (so any CostModel -- the reference's A100-era default or a
+    fitted B200 one -- keeps report timestamps close to real time between syncs).  Every input of
+    the clock (the broadcast wall time, the replicated charges) is the same on every rank, so the
+    ranks read the same time.  virtual=True: the engine keeps the host-boundary (replicable) expert
     decisions and the driver starts no arrival watcher."""
 
     virtual = True
@@ -60,6 +64,9 @@ class LockstepClock:
         self._t0 = time.perf_counter()
         self.now = 0.0
         self.syncs = 0
+        self.scale = 1.0        # wall ms per charged ms
+        self._charged = 0.0     # charged (unscaled) since the last sync
+        self._last_wall = 0.0
 
     def wall_ms(self) -> float:
         return (time.perf_counter() - self._t0) * 1000.0
@@ -67,13 +74,18 @@ class LockstepClock:
     def sync(self) -> None:
         self._buf.fill_(self.wall_ms() if self._rank == 0 else 0.0)
         dist.broadcast(self._buf, 0, group=self.group)
-        self.now = max(self.now, float(self._buf.item()))
+        w = float(self._buf.item())
+        if self._charged > 0.0 and w > self._last_wall:
+            self.scale = 0.5 * self.scale + 0.5 * (w - self._last_wall) / self._charged
+        self._charged, self._last_wall = 0.0, w
+        self.now = max(self.now, w)
         self.syncs += 1
 
     def advance(self, delta_ms: float) -> None:
         if delta_ms < 0:
             raise ValueError(f"clock cannot move backwards (delta {delta_ms})")
-        self.now += delta_ms
+        self._charged += delta_ms
+        self.now += self.scale * delta_ms
 
     def advance_to(self, timestamp: float) -> None:
         wait = timestamp - self.wall_ms()

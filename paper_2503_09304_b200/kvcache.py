@@ -66,7 +66,10 @@ class UnifiedDynamicCache:
             if not self._free:
                 # grow by half: the copy keeps old and new pools alive at once, and a doubling of
                 # a multi-GB pool next to a 93 GB model runs out of HBM
-                self._grow(self._n_pages + max(1, self._n_pages // 2))
+                grow = self._n_pages + max(1, self._n_pages // 2)
+                if self.max_pages is not None:  # a smaller step that still fits beats a refusal
+                    grow = min(grow, max(self.max_pages, self._n_pages + 1))
+                self._grow(grow)
             pages.append(self._free.pop())
 
     def slots(self, handle: int, start: int, n: int) -> list[int]:

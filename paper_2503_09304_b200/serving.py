@@ -21,12 +21,16 @@ from .workload import WorkloadSpec, trace_for_rate
 
 def kv_pages_for(model, capacity_bytes: float, max_batch_size: int) -> dict:
     """Page-pool kwargs sized for the admission ledger's capacity up front (one allocation, no
-    grow-and-copy next to the model): capacity / (page tokens x layers x entry bytes) pages plus one
-    partially filled page per possible resident sequence."""
+    grow-and-copy next to the model): capacity / (page tokens x layers x entry bytes) full pages
+    plus partially filled pages for 8x the batch size of resident sequences (more resident
+    sequences than that -- the ledger admits up to capacity / lifetime footprint of them -- grow
+    the pool by at most half its size, clamped to max_pages, kvcache._ensure_pages)."""
     kw = dict(getattr(model, "kv_page_kwargs", {}))
     page = kw.get("page_size", 16)
-    per_page = page * model.config.num_layers * model.kv_entry_bytes()
-    kw["initial_pages"] = int(-(-capacity_bytes // per_page)) + 8 * max_batch_size
+    per_token = model.config.num_layers * model.kv_entry_bytes()
+    full = int(-(-capacity_bytes // (page * per_token)))
+    partial = min(int(capacity_bytes // per_token), 8 * max_batch_size)
+    kw["initial_pages"] = full + partial
     return kw
 
 

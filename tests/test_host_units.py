@@ -178,3 +178,16 @@ def test_paged_cache_reserve_batch_equals_member_reserves():
     assert a._counts == b._counts and a.usage_bytes() == b.usage_bytes()
     with pytest.raises(StateCorruptionError):
         b.reserve_batch([0, 99], 0, [1, 1])
+
+
+def test_page_pool_growth_is_clamped_to_max_pages():
+    """A grow-by-half step that would pass max_pages grows to max_pages instead of refusing; only a
+    pool already at max_pages refuses (kvcache._ensure_pages)."""
+    cache = UnifiedDynamicCache(1, (1,), torch.float32, torch.device("cpu"), 4, 1e9, page_size=4, initial_pages=4,
+                                max_pages=5)
+    cache.register(0)
+    cache.reserve(0, 0, 20)  # 5 pages: 4 -> 6 would pass max_pages=5; clamps to 5
+    assert cache.pool(0).shape[0] == 5
+    cache.register(1)
+    with pytest.raises(CacheCapacityError):
+        cache.reserve(1, 0, 1)

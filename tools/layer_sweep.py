@@ -32,6 +32,16 @@ def timed(fn, reps):
     return statistics.median(ts)
 
 
+def graphed(fn):
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    torch.cuda.synchronize()
+    return g.replay
+
+
 def main():
     out = []
     only = sys.argv[1] if len(sys.argv) > 1 else None
@@ -74,13 +84,18 @@ def main():
             reps = 10 if T >= 4096 else 20
             t = timed(layer, reps)
             tp = timed(preempt_every_boundary, max(5, reps // 2))
+            # the same two sequences captured in CUDA graphs: the device-side cost of the boundaries
+            # (launch gaps, per-launch prologue / tail) without the host's per-call Python overhead
+            tg, tpg = timed(graphed(layer), reps), timed(graphed(preempt_every_boundary), max(5, reps // 2))
             flops = 6.0 * T * k * d * F
             wbytes = len(hit) * 3 * d * F * 2
             rec = {"shape": name, "T": T, "ms": t, "tflops": flops / t / 1e9,
                    "tensor_frac_sustained": flops / t / 1e9 / PEAKS["bf16_tflops_sustained"],
                    "tensor_frac_burst": flops / t / 1e9 / PEAKS["bf16_tflops"],
                    "weight_gbs": wbytes / t / 1e6, "hbm_frac": wbytes / t / 1e6 / PEAKS["hbm_gbs"],
-                   "experts_hit": len(hit), "preempt_every_boundary_ms": tp, "preempt_overhead_x": tp / t}
+                   "experts_hit": len(hit), "preempt_every_boundary_ms": tp, "preempt_overhead_x": tp / t,
+                   "graph_ms": tg, "preempt_every_boundary_graph_ms": tpg, "preempt_overhead_x_graph": tpg / tg,
+                   "preempt_us_per_boundary_graph": (tpg - tg) * 1e3 / max(1, len(hit) - 1)}
             out.append(rec)
             print(json.dumps(rec), flush=True)
         del gu, dn
