@@ -115,8 +115,10 @@ struct TileMap {
 // Called by all 32 lanes of ONE warp: per-expert row ranges loaded in parallel, tile counts
 // prefix-summed with warp shuffles (E <= 64).  e_limit (optional, device) caps the covered
 // experts (chained launches).  n_tiles_n already includes any K-split factor.
+// merge > 0: an expert's last M tile absorbs a remainder of <= merge rows into the tile before it
+// (tile of bm + remainder rows; kernels that handle such wide tiles only).
 __device__ __forceinline__ void build_tile_map(TileMap& m, const int32_t* offsets, int e_begin, int e_end,
-                                               const int32_t* e_limit, int bm, int n_tiles_n) {
+                                               const int32_t* e_limit, int bm, int n_tiles_n, int merge = 0) {
   const int lane = threadIdx.x & 31;
   int hi = e_end;
   if (e_limit != nullptr) hi = min(hi, *e_limit);
@@ -129,7 +131,8 @@ __device__ __forceinline__ void build_tile_map(TileMap& m, const int32_t* offset
     int tiles = 0;
     if (i < n) {
       const int r0 = offsets[e_begin + i], r1 = offsets[e_begin + i + 1];
-      const int mt = (r1 - r0 + bm - 1) / bm;
+      int mt = (r1 - r0 + bm - 1) / bm;
+      if (merge > 0 && mt >= 2 && (r1 - r0) - (mt - 1) * bm <= merge) --mt;
       m.row_begin[i] = r0;
       m.m_tiles[i] = mt;
       tiles = mt * n_tiles_n;

@@ -52,6 +52,7 @@ struct FusedParams {
   int32_t* cursor;  // optional cursor_out (written by the last CTA out, ffn_exit)
   int32_t* progress;  // optional host-mapped per-expert progress words (signal_expert_done)
   int seq;
+  int merge;  // swap-AB pair: remainder rows (<= merge) folded into an expert's last token tile
 };
 
 // Token rows of one 128-row A tile for the gather: lane l owns rows [4l, 4l+4) of the tile; rows
@@ -552,6 +553,14 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
 //                  rows to the gate warps through shared memory for SiLU(g) * u;
 //   down unit    = (expert, 256 d columns, <= 256 tokens), CTA c owns d columns + 128c.
 // Same claim / ring / completion-counter / preemption protocol as ffn_fused_pair_kernel.
+// Wide last tile: an expert whose rows leave a remainder of <= p.merge rows after its full
+// 256-row tiles runs that remainder in the same unit as its last full tile (up to 256 + merge
+// token rows): the unit streams its weight rows ONCE and multiplies them into both TMEM
+// accumulators (the first 256 tokens and the remainder), taking two ring stages per K block (the
+// second holds only the remainder's token rows) and two accumulator turns.  Without it a
+// remainder of a few rows costs a whole extra pass over the expert's weights (Mixtral ~1k tokens:
+// about half the experts hold 257-300 rows).  Per-token results are unchanged (same K order per
+// accumulator).
 constexpr int kStagesSP = 6;
 constexpr int kTokSP = 256;                     // token rows per unit
 constexpr int kHalfSP = 128 * kBKf * 2;         // 16 KB: this CTA's weight rows, then its token rows
@@ -591,8 +600,14 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
   const int nt1 = (p.F + 127) / 128, nt2 = (p.d + 255) / 256;
   const int nkb1 = (p.d + kBKf - 1) / kBKf, nkb2 = (p.F + kBKf - 1) / kBKf;
 
-  if (warp == 0) build_tile_map(map1, p.offsets, p.e_begin, p.e_end, nullptr, kTokSP, nt1);
-  if (warp == 3) build_tile_map(map2, p.offsets, p.e_begin, p.e_end, nullptr, kTokSP, nt2);
+  if (warp == 0) build_tile_map(map1, p.offsets, p.e_begin, p.e_end, nullptr, kTokSP, nt1, p.merge);
+  if (warp == 3) build_tile_map(map2, p.offsets, p.e_begin, p.e_end, nullptr, kTokSP, nt2, p.merge);
+  // token rows of the unit starting at row m0 of an expert ending at row_end: a full tile, or the
+  // last (possibly wide) one
+  auto unit_rows = [&](int m0, int row_end) {
+    const int r = row_end - m0;
+    return r > kTokSP + p.merge ? kTokSP : r;
+  };
   if (threadIdx.x == 32) {
     for (int s = 0; s < kStagesSP; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
@@ -669,11 +684,19 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
       if (up) map1.locate(t, kTokSP, nt1, 128, e, m0, n0);
       else map2.locate(t - N1, kTokSP, nt2, 256, e, m0, n0);
       const int row_end = p.offsets[e + 1];
-      const int half = sp_ncols(min(kTokSP, row_end - m0)) >> 1;
+      const int rows = unit_rows(m0, row_end);
+      const bool wide = rows > kTokSP;  // (never with gather: the host sets merge = 0 then)
+      const int half = sp_ncols(min(kTokSP, rows)) >> 1;
       const int tok = m0 + (int)rank * half;  // this CTA's N/2 token rows
       const int bi = half <= 32 ? 0 : (half <= 64 ? 1 : 2);
       const int box = 32 << bi;
       const CUtensorMap* tm = &maps.tok[up ? 0 : 1][up && p.gather ? 0 : bi];
+      // the wide unit's remainder: token rows [m0 + 256, m0 + rows), N2/2 per CTA
+      const int half2 = wide ? sp_ncols(rows - kTokSP) >> 1 : 0;
+      const int bi2 = half2 <= 32 ? 0 : (half2 <= 64 ? 1 : 2);
+      const int box2 = 32 << bi2;
+      const CUtensorMap* tm2 = &maps.tok[up ? 0 : 1][bi2];
+      const int tok2 = m0 + kTokSP + (int)rank * half2;
       const bool gather = up && p.gather;
       int g[4] = {0, 0, 0, 0};
       if (gather) gather_rows4(p, tok, row_end, lane, g);
@@ -696,6 +719,15 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
           ptx::tma_gather4_cg2(tm, &full_bar[stage], sa + kHalfSP + lane * 512, kb * kBKf, g[0], g[1], g[2], g[3],
                                ptx::kEvictNormal);
         if (++stage == kStagesSP) { stage = 0; phase ^= 1; }
+        if (wide) {  // next stage: the remainder's token rows only (its weight half stays unused)
+          ptx::mbar_wait_cluster(&empty_bar[stage], phase ^ 1);
+          uint8_t* sb = smem + stage * kStageBytesSP;
+          if (lane == 0) {
+            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * (box2 * kBKf * 2));
+            ptx::tma_load_2d_cg2(tm2, &full_bar[stage], sb + kHalfSP, kb * kBKf, tok2, ptx::kEvictNormal);
+          }
+          if (++stage == kStagesSP) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -712,25 +744,49 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
         int e, m0, n0;
         if (t < N1) map1.locate(t, kTokSP, nt1, 128, e, m0, n0);
         else map2.locate(t - N1, kTokSP, nt2, 256, e, m0, n0);
-        const uint32_t idesc = ptx::idesc_bf16_f32(256, sp_ncols(min(kTokSP, p.offsets[e + 1] - m0)));
+        const int rows = unit_rows(m0, p.offsets[e + 1]);
+        const bool wide = rows > kTokSP;
+        const uint32_t idesc = ptx::idesc_bf16_f32(256, sp_ncols(min(kTokSP, rows)));
+        const uint32_t idesc2 = wide ? ptx::idesc_bf16_f32(256, sp_ncols(rows - kTokSP)) : 0u;
         const int nkb = t < N1 ? nkb1 : nkb2;
+        // accumulator turn(s): a wide unit takes this turn and the next one
+        const int acc2 = acc ^ 1;
+        const uint32_t aphase2 = acc2 == 0 ? aphase ^ 1 : aphase;
         ptx::mbar_wait_cluster(&tempty_bar[acc], aphase ^ 1);
+        if (wide) ptx::mbar_wait_cluster(&tempty_bar[acc2], aphase2 ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kTokSP;
+        const uint32_t d_tmem2 = tmem_base + acc2 * kTokSP;
         for (int kb = 0; kb < nkb; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
+          const int stage_a = stage;
           const uint32_t a_addr = ptx::smem_u32(smem + stage * kStageBytesSP);
           const uint32_t b_addr = a_addr + kHalfSP;
 #pragma unroll
           for (int k = 0; k < kBKf / 16; ++k)
             ptx::tc_mma_bf16_cg2(d_tmem, ptx::sw128_kmajor_desc(a_addr + k * 32),
                                  ptx::sw128_kmajor_desc(b_addr + k * 32), idesc, (kb | k) != 0);
-          ptx::tc_commit_cg2(&empty_bar[stage], 0x3);
           if (++stage == kStagesSP) { stage = 0; phase ^= 1; }
+          if (wide) {
+            ptx::mbar_wait(&full_bar[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t b2_addr = ptx::smem_u32(smem + stage * kStageBytesSP) + kHalfSP;
+#pragma unroll
+            for (int k = 0; k < kBKf / 16; ++k)
+              ptx::tc_mma_bf16_cg2(d_tmem2, ptx::sw128_kmajor_desc(a_addr + k * 32),
+                                   ptx::sw128_kmajor_desc(b2_addr + k * 32), idesc2, (kb | k) != 0);
+            ptx::tc_commit_cg2(&empty_bar[stage], 0x3);
+            if (++stage == kStagesSP) { stage = 0; phase ^= 1; }
+          }
+          ptx::tc_commit_cg2(&empty_bar[stage_a], 0x3);  // after the MMAs reading its weights
         }
         ptx::tc_commit_cg2(&tfull_bar[acc], 0x3);
         if (++acc == 2) { acc = 0; aphase ^= 1; }
+        if (wide) {
+          ptx::tc_commit_cg2(&tfull_bar[acc], 0x3);
+          if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
       }
     }
     __syncwarp();
@@ -754,93 +810,99 @@ ffn_swap_pair_kernel(const __grid_constant__ SpMaps maps, FusedParams p) {
       int e, m0, n0;
       if (up) map1.locate(t, kTokSP, nt1, 128, e, m0, n0);
       else map2.locate(t - N1, kTokSP, nt2, 256, e, m0, n0);
-      const int rows = min(kTokSP, p.offsets[e + 1] - m0);  // uniform over the CTA
-      ptx::mbar_wait_cluster(&tfull_bar[acc], aphase);
-      ptx::tc_fence_after();
-      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * kTokSP;
-      __nv_bfloat16 (*stg)[32] = sp_w[ew];  // this warp's staging tile (token rows x 32 columns)
+      const int unit = unit_rows(m0, p.offsets[e + 1]);  // uniform over the CTA
+      const int m_unit = m0;
 #pragma unroll 1
-      for (int c = 0; c < rows; c += 32) {
-        uint32_t v[32];
-        ptx::tmem_ld32(t_row + c, v);
-        ptx::tmem_ld_wait();
-        if (up) {
-          // warp pair q = ew & 1 holds gate (ew = q) and up (ew = q + 2) of the same 32 features:
-          // the gate warp finishes tokens [0, 16) of the chunk, the up warp tokens [16, 32); the
-          // halves cross through shared memory under a barrier of the pair only
-          const int q = ew & 1;
-          const bool gate = ew < 2;
-          float4* xs = reinterpret_cast<float4*>(&sp_x[gate ? 0 : 1][q][lane][0]);
+      for (int sub = 0; sub < (unit > kTokSP ? 2 : 1); ++sub) {  // a wide unit's two accumulators
+        const int m0 = m_unit + sub * kTokSP;
+        const int rows = sub ? unit - kTokSP : min(kTokSP, unit);
+        ptx::mbar_wait_cluster(&tfull_bar[acc], aphase);
+        ptx::tc_fence_after();
+        const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * kTokSP;
+        __nv_bfloat16 (*stg)[32] = sp_w[ew];  // this warp's staging tile (token rows x 32 columns)
+#pragma unroll 1
+        for (int c = 0; c < rows; c += 32) {
+          uint32_t v[32];
+          ptx::tmem_ld32(t_row + c, v);
+          ptx::tmem_ld_wait();
+          if (up) {
+            // warp pair q = ew & 1 holds gate (ew = q) and up (ew = q + 2) of the same 32 features:
+            // the gate warp finishes tokens [0, 16) of the chunk, the up warp tokens [16, 32); the
+            // halves cross through shared memory under a barrier of the pair only
+            const int q = ew & 1;
+            const bool gate = ew < 2;
+            float4* xs = reinterpret_cast<float4*>(&sp_x[gate ? 0 : 1][q][lane][0]);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float e4[4];
+            for (int i = 0; i < 4; ++i) {
+              float e4[4];
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) e4[c4] = __uint_as_float(gate ? v[16 + 4 * i + c4] : v[4 * i + c4]);
-            xs[i] = make_float4(e4[0], e4[1], e4[2], e4[3]);
-          }
-          asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-          const float4* xr = reinterpret_cast<const float4*>(&sp_x[gate ? 1 : 0][q][lane][0]);
-          float h[16];
+              for (int c4 = 0; c4 < 4; ++c4) e4[c4] = __uint_as_float(gate ? v[16 + 4 * i + c4] : v[4 * i + c4]);
+              xs[i] = make_float4(e4[0], e4[1], e4[2], e4[3]);
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+            const float4* xr = reinterpret_cast<const float4*>(&sp_x[gate ? 1 : 0][q][lane][0]);
+            float h[16];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 t4 = xr[i];
-            const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+            for (int i = 0; i < 4; ++i) {
+              const float4 t4 = xr[i];
+              const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-              const int j = 4 * i + c4;
-              const float gv = gate ? __uint_as_float(v[j]) : tv[c4];
-              const float uv = gate ? tv[c4] : __uint_as_float(v[16 + j]);
-              h[j] = gv / (1.f + __expf(-gv)) * uv;
+              for (int c4 = 0; c4 < 4; ++c4) {
+                const int j = 4 * i + c4;
+                const float gv = gate ? __uint_as_float(v[j]) : tv[c4];
+                const float uv = gate ? tv[c4] : __uint_as_float(v[16 + j]);
+                h[j] = gv / (1.f + __expf(-gv)) * uv;
+              }
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // sp_x is rewritten by the next chunk
+            // transpose through the warp's staging tile: lane pairs (2m, 2m+1) swap one value per
+            // token pair so each lane stores one 32-bit word (rows j, j+1 land 16 banks apart)
+#pragma unroll
+            for (int j = 0; j < 16; j += 2) {
+              const float recv = __shfl_xor_sync(0xffffffffu, (lane & 1) ? h[j] : h[j + 1], 1);
+              *reinterpret_cast<uint32_t*>(&stg[j + (lane & 1)][lane & ~1]) =
+                  (lane & 1) ? pack2(recv, h[j + 1]) : pack2(h[j], recv);
+            }
+            __syncwarp();
+            // 16 token rows x 32 features (64 B) of act, 16-byte stores
+            const int t0 = c + (gate ? 0 : 16);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int idx = lane + 32 * i, r = idx >> 2, vq = idx & 3;
+              if (t0 + r < rows)
+                *reinterpret_cast<uint4*>(p.act + (size_t)(m0 + t0 + r) * p.F + n0 + (int)rank * 64 + 32 * q + 8 * vq) =
+                    *reinterpret_cast<const uint4*>(&stg[r][8 * vq]);
+            }
+          } else {
+            const int pr = c + lane < rows ? p.perm[m0 + c + lane] : 0;  // slot of token c + lane
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const float a0 = __uint_as_float(v[j]), a1 = __uint_as_float(v[j + 1]);
+              const float recv = __shfl_xor_sync(0xffffffffu, (lane & 1) ? a0 : a1, 1);
+              *reinterpret_cast<uint32_t*>(&stg[j + (lane & 1)][lane & ~1]) = (lane & 1) ? pack2(recv, a1) : pack2(a0, recv);
+            }
+            __syncwarp();
+            // 32 token rows x 32 output columns (64 B) scattered to the token slots, 16-byte stores
+            const int col = n0 + (int)rank * 128 + 32 * ew;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int idx = lane + 32 * i, r = idx >> 2, vq = idx & 3;
+              const int slot = __shfl_sync(0xffffffffu, pr, r);
+              if (c + r < rows)
+                *reinterpret_cast<uint4*>(out_row(p.y, p.peers, slot, p.d) + col + 8 * vq) =
+                    *reinterpret_cast<const uint4*>(&stg[r][8 * vq]);
             }
           }
-          asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // sp_x is rewritten by the next chunk
-          // transpose through the warp's staging tile: lane pairs (2m, 2m+1) swap one value per
-          // token pair so each lane stores one 32-bit word (rows j, j+1 land 16 banks apart)
-#pragma unroll
-          for (int j = 0; j < 16; j += 2) {
-            const float recv = __shfl_xor_sync(0xffffffffu, (lane & 1) ? h[j] : h[j + 1], 1);
-            *reinterpret_cast<uint32_t*>(&stg[j + (lane & 1)][lane & ~1]) =
-                (lane & 1) ? pack2(recv, h[j + 1]) : pack2(h[j], recv);
-          }
-          __syncwarp();
-          // 16 token rows x 32 features (64 B) of act, 16-byte stores
-          const int t0 = c + (gate ? 0 : 16);
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int idx = lane + 32 * i, r = idx >> 2, vq = idx & 3;
-            if (t0 + r < rows)
-              *reinterpret_cast<uint4*>(p.act + (size_t)(m0 + t0 + r) * p.F + n0 + (int)rank * 64 + 32 * q + 8 * vq) =
-                  *reinterpret_cast<const uint4*>(&stg[r][8 * vq]);
-          }
-        } else {
-          const int pr = c + lane < rows ? p.perm[m0 + c + lane] : 0;  // slot of token c + lane
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float a0 = __uint_as_float(v[j]), a1 = __uint_as_float(v[j + 1]);
-            const float recv = __shfl_xor_sync(0xffffffffu, (lane & 1) ? a0 : a1, 1);
-            *reinterpret_cast<uint32_t*>(&stg[j + (lane & 1)][lane & ~1]) = (lane & 1) ? pack2(recv, a1) : pack2(a0, recv);
-          }
-          __syncwarp();
-          // 32 token rows x 32 output columns (64 B) scattered to the token slots, 16-byte stores
-          const int col = n0 + (int)rank * 128 + 32 * ew;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int idx = lane + 32 * i, r = idx >> 2, vq = idx & 3;
-            const int slot = __shfl_sync(0xffffffffu, pr, r);
-            if (c + r < rows)
-              *reinterpret_cast<uint4*>(out_row(p.y, p.peers, slot, p.d) + col + 8 * vq) =
-                  *reinterpret_cast<const uint4*>(&stg[r][8 * vq]);
-          }
+          __syncwarp();  // the staging tile is rewritten by the next chunk
         }
-        __syncwarp();  // the staging tile is rewritten by the next chunk
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) ptx::mbar_arrive(&tempty_bar[acc]);
+          else ptx::mbar_arrive_remote(&tempty_bar[acc], 0);
+        }
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (leader) ptx::mbar_arrive(&tempty_bar[acc]);
-        else ptx::mbar_arrive_remote(&tempty_bar[acc], 0);
-      }
-      if (++acc == 2) { acc = 0; aphase ^= 1; }
       if (up) {
         fence_proxy_async_global();
         __threadfence();
@@ -982,6 +1044,12 @@ int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* 
   p.cursor = cursor_out;
   p.progress = progress;
   p.seq = seq;
+  // remainder rows folded into an expert's last token tile (wide unit); QMOE_SP_MERGE overrides
+  static const int merge_env = [] {
+    const char* v = getenv("QMOE_SP_MERGE");
+    return v == nullptr ? -1 : atoi(v);
+  }();
+  p.merge = p.gather ? 0 : (merge_env >= 0 ? std::min(merge_env, kTokSP) : 128);
   static uint64_t attr_set = 0;  // devices already configured
   if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_swap_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSP));
