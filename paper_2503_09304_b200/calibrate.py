@@ -165,6 +165,45 @@ def fit_cost_model(samples: dict) -> tuple[CostModel, dict]:
     return cm, rep
 
 
+def fit_cost_model_iterations(samples: dict, stage_fit: Optional[CostModel] = None) -> tuple[CostModel, dict]:
+    """The CostModel whose virtual iterations match measured whole-iteration wall times: non-negative
+    least squares of each completed iteration's wall ms on per-iteration sums of the linear model's
+    features -- layers (attention base + router), tokens x layers, cached entries scanned and
+    non-empty experts (reference engine.py:48-88).  Expert entries are k x tokens x layers in a
+    whole iteration, so the per-token term is one coefficient; it is split between attn_per_token
+    and expert_per_entry in the proportion of the stage-level fit (stage_fit; all to attention when
+    absent).  router_cost keeps its measured stage median and the layer term pays the rest;
+    checkpoint / restore keep the stage medians.  Stage-level event brackets overstate an iteration
+    (overlapping launches, host run-ahead); this is the fit a virtual-clock study needs.
+    samples: measure_stage_samples(...) output (its "iterations" rows: layers, tokens x layers,
+    cached, non-empty experts, entries, wall ms)."""
+    from scipy.optimize import nnls
+
+    rows = samples["iterations"]
+    a = np.array([r[:4] for r in rows], dtype=np.float64)
+    y = np.array([r[5] for r in rows], dtype=np.float64)
+    coef, _ = nnls(a, y)
+    pred = a @ coef
+    ss = float(((y - y.mean()) ** 2).sum())
+    med = lambda v: float(statistics.median(v)) if v else 0.0  # noqa: E731
+    router = min(med(samples["router"]), float(coef[0]))
+    tl = sum(r[1] for r in rows)
+    k_eff = (sum(r[4] for r in rows) / tl) if tl else 1.0  # expert entries per token-layer
+    share = 0.0
+    if stage_fit is not None:
+        te = stage_fit.expert_per_entry * k_eff
+        share = te / (te + stage_fit.attn_per_token) if te + stage_fit.attn_per_token > 0 else 0.0
+    cm = CostModel(attn_base=float(coef[0]) - router, attn_per_token=float(coef[1]) * (1.0 - share),
+                   attn_per_cached=float(coef[2]), router_cost=router, expert_base=float(coef[3]),
+                   expert_per_entry=float(coef[1]) * share / k_eff if k_eff > 0 else 0.0,
+                   checkpoint_cost=med(samples.get("checkpoint", [])), restore_cost=med(samples.get("restore", [])))
+    rep = {"n": len(rows), "r2": 1.0 - float(((y - pred) ** 2).sum()) / ss if ss > 0 else 1.0,
+           "median_abs_rel_err": float(np.median(np.abs(pred - y) / np.maximum(y, 1e-9))),
+           "entries_per_token_layer": k_eff, "per_token_split_to_experts": share,
+           "coef": dict(zip(["per_layer", "per_token_layer", "per_cached", "per_expert"], coef.tolist()))}
+    return cm, rep
+
+
 def measure_stage_samples(model, trace, max_batch_size: int = 32, scheduler: str = "qllm",
                           wall: bool = True) -> dict:
     """Run `trace` through the engine with CUDA events around every stage of `model`; returns the
@@ -196,8 +235,21 @@ def measure_stage_samples(model, trace, max_batch_size: int = 32, scheduler: str
     cache = sim.cache
     att, route, perm, run, comb = (model.attention_batch, model.route_batch, model.permute, model.run_experts,
                                    model.combine_batch)
-    model.attention_batch = timed("attention", att, lambda a, r: (
-        sum(m.n for m in a[2]), sum(cache.count(m.seq.cache_handle, a[0]) for m in a[2])))
+    # per-iteration feature sums of the reference's linear model (engine.py:48-88) and the
+    # iteration's wall time, for the iteration-level fit
+    it = {"f": None}
+    out["iterations"] = []
+
+    def att_extra(a, r):
+        T, cached = sum(m.n for m in a[2]), sum(cache.count(m.seq.cache_handle, a[0]) for m in a[2])
+        if it["f"] is not None:
+            f = it["f"]
+            f[0] += 1
+            f[1] += T
+            f[2] += cached
+        return T, cached
+
+    model.attention_batch = timed("attention", att, att_extra)
     model.route_batch = timed("router", route, lambda a, r: None)
     state = {}
 
@@ -216,6 +268,9 @@ def measure_stage_samples(model, trace, max_batch_size: int = 32, scheduler: str
         off = state["offsets"].tolist()
         counts = [off[i + 1] - off[i] for i in range(len(off) - 1)]
         pending.append(("experts", state["start"], e, (sum(1 for c in counts if c), sum(counts))))
+        if it["f"] is not None:
+            it["f"][3] += sum(1 for c in counts if c)
+            it["f"][4] += sum(counts)
         return r
 
     model.permute, model.combine_batch = perm_hook, comb_hook
@@ -237,13 +292,26 @@ def measure_stage_samples(model, trace, max_batch_size: int = 32, scheduler: str
             pending.append(("restore", s, e, len(seqs)))
         return r
 
-    eng._preempt, eng._init_state = pre_hook, init_hook
+    execute = eng.execute
+
+    def exec_hook(*a, **kw):
+        it["f"] = [0, 0, 0, 0, 0]
+        torch.cuda.synchronize()
+        t = _time.perf_counter()
+        r = execute(*a, **kw)
+        torch.cuda.synchronize()
+        if r.__class__.__name__ == "Completed":  # whole iterations only
+            out["iterations"].append(tuple(it["f"]) + ((_time.perf_counter() - t) * 1e3,))
+        it["f"] = None
+        return r
+
+    eng._preempt, eng._init_state, eng.execute = pre_hook, init_hook, exec_hook
     try:
         sim.run()
     finally:
         model.attention_batch, model.route_batch, model.permute, model.run_experts, model.combine_batch = (
             att, route, perm, run, comb)
-        eng._preempt, eng._init_state = pre, init
+        eng._preempt, eng._init_state, eng.execute = pre, init, execute
     torch.cuda.synchronize()
     for kind, s, e, extra in pending:
         ms = s.elapsed_time(e)

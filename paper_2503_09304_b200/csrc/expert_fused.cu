@@ -553,7 +553,8 @@ ffn_fused_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
 //                  rows to the gate warps through shared memory for SiLU(g) * u;
 //   down unit    = (expert, 256 d columns, <= 256 tokens), CTA c owns d columns + 128c.
 // Same claim / ring / completion-counter / preemption protocol as ffn_fused_pair_kernel.
-// Wide last tile: an expert whose rows leave a remainder of <= p.merge rows after its full
+// Wide last tile (QMOE_SP_MERGE=n, off by default, see expert_ffn_swap_pair): an expert whose rows
+// leave a remainder of <= p.merge rows after its full
 // 256-row tiles runs that remainder in the same unit as its last full tile (up to 256 + merge
 // token rows): the unit streams its weight rows ONCE and multiplies them into both TMEM
 // accumulators (the first 256 tokens and the remainder), taking two ring stages per K block (the
@@ -1044,12 +1045,16 @@ int expert_ffn_swap_pair(const void* xp, const int32_t* offsets, const int32_t* 
   p.cursor = cursor_out;
   p.progress = progress;
   p.seq = seq;
-  // remainder rows folded into an expert's last token tile (wide unit); QMOE_SP_MERGE overrides
+  // remainder rows folded into an expert's last token tile (wide unit): off by default.  Same-box
+  // A/B (profiles/ffn_wide_ab_r02.json, FFN alone, L2 flushed): QMOE_SP_MERGE=128 is 7-12% faster
+  // where experts hold 270-320 rows (Mixtral 1.1-1.3k tokens) but 2-9% slower at 1k, 2k, 3k and
+  // 16k tokens -- consecutive wide units cannot overlap one unit's epilogue with the next unit's
+  // MMAs (both TMEM accumulators busy), which costs more than the saved weight pass.
   static const int merge_env = [] {
     const char* v = getenv("QMOE_SP_MERGE");
-    return v == nullptr ? -1 : atoi(v);
+    return v == nullptr ? 0 : atoi(v);
   }();
-  p.merge = p.gather ? 0 : (merge_env >= 0 ? std::min(merge_env, kTokSP) : 128);
+  p.merge = p.gather ? 0 : std::max(0, std::min(merge_env, kTokSP));
   static uint64_t attr_set = 0;  // devices already configured
   if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_swap_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSP));

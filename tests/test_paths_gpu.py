@@ -198,12 +198,12 @@ def test_all_single_launch_kernels_agree_bit_for_bit(cuda):
 
 
 def test_swap_pair_wide_last_tile_is_bit_identical(cuda):
-    """The swap-AB pair folds an expert's remainder rows (<= 128 after its full 256-row tiles) into
-    its last token tile (one weight pass, two TMEM accumulators, two ring stages per K block):
+    """With QMOE_SP_MERGE=128 the swap-AB pair folds an expert's remainder rows (<= 128 after its
+    full 256-row tiles) into its last token tile (one weight pass, two TMEM accumulators, two ring stages per K block):
     outputs, preemption stops and resumes are bit-identical to running the remainder as its own
     tile (QMOE_SP_MERGE=0)."""
     shapes = [(1100, 1024, 2048, 8, 2), (1200, 512, 1408, 8, 2), (2500, 512, 1024, 8, 2), (300, 512, 1024, 2, 2)]
     env = {"QMOE_SWAP_AB": "0", "QMOE_SWAP_PAIR": "1"}
-    wide = _run(env, shapes)
+    wide = _run({**env, "QMOE_SP_MERGE": "128"}, shapes)
     narrow = _run({**env, "QMOE_SP_MERGE": "0"}, shapes)
     assert [r["sha"] for r in wide] == [r["sha"] for r in narrow]

@@ -7,3 +7,5 @@ for m in 128 0 256 64; do
 done
 timeout 900 python bench.py --serve-duration 0 > gpurun_out/bench_wide.log 2>&1
 tail -3 gpurun_out/t_paths.log
+timeout 900 python tools/fit_cost_model.py gpurun_out/cost_model_b200_r02.json mixtral > gpurun_out/fit_mixtral.log 2>&1
+timeout 900 python tools/fit_cost_model.py gpurun_out/cost_model_b200_r02_qwen.json qwen > gpurun_out/fit_qwen.log 2>&1
