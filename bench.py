@@ -257,27 +257,28 @@ def run_serving(args) -> dict:
         for seed in seeds:
             sampler = ClockSampler(torch.cuda.current_device())
             out = compare(model, rate, args.serve_duration, seed=seed, schedulers=scheds,
-                          kv_capacity_bytes=KV_GIB * 1024**3, **kw)
+                          kv_capacity_bytes=args.serve_kv_gib * 1024**3, **kw)
             out["clocks"] = sampler.stop()
             out["seed"] = seed
             for k in scheds:
                 out["fcfs" if k == "baseline" else k].pop("engine", None)
             runs.append(out)
+    ep_info = ({"world": world, "bounds": model.bounds, "exchanges": model.stats["exchanges"],
+                "backend": dist.get_backend()} if world > 1 else None)
     del model
     torch.cuda.empty_cache()
     res = runs[0] if len(runs) == 1 else {"runs": runs}
     res["model"] = (f"mixtral-8x7b (32 layers, random-init bf16), batch 32, SLO 3000 ms (and 10x the measured decode "
-                    f"iteration), paper workload (20% LS, Poisson), KV ledger {KV_GIB:.0f} GiB; qllm = the reference's "
+                    f"iteration), paper workload (20% LS, Poisson), KV ledger {args.serve_kv_gib:.0f} GiB; qllm = the reference's "
                     f"Algorithm 1 + policy; qllm-arrival = LS-arrival-only preemption + BE continuous batching "
                     f"(sched.arrival_policy); LS arrivals raise the device preempt flag (no host round trip)")
     if world > 1:
         res["model"] = (f"mixtral-8x7b (32 layers, random-init bf16) expert-parallel over {world} GPUs (experts "
-                        f"{model.bounds}, attention replicated, expert outputs all-gathered over peer memory), "
-                        f"batch 32, SLO 3000 ms, paper workload, KV ledger {KV_GIB:.0f} GiB per rank; every rank "
+                        f"{ep_info['bounds']}, attention replicated, expert outputs all-gathered over peer memory), "
+                        f"batch 32, SLO 3000 ms, paper workload, KV ledger {args.serve_kv_gib:.0f} GiB per rank; every rank "
                         f"runs the same scheduler on rank 0's wall clock (LockstepClock, synced per iteration); "
                         f"expert boundaries decided on the host before each launch")
-        res["ep"] = {"world": world, "bounds": model.bounds, "exchanges": model.stats["exchanges"],
-                     "backend": dist.get_backend()}
+        res["ep"] = ep_info
     return res
 
 
@@ -567,6 +568,8 @@ def main():
     ap.add_argument("--serve-sweep", default="",
                     help="comma-separated req/s rates (e.g. 1,2,3,4,5,6,7,8,10) instead of --serve-rate")
     ap.add_argument("--serve-seeds", default="0")
+    ap.add_argument("--serve-kv-gib", type=float, default=KV_GIB,
+                    help="KV admission ledger per rank in GiB (the page pool is sized for it up front)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
