@@ -380,6 +380,16 @@ def run_ours(args, rank: int, world: int) -> None:
         ffn_events.append((s, e))
 
     K.expert_ffn_peer = timed_ffn_peer
+    orig_peer_ex = K.expert_ffn_peer_ex
+
+    def timed_ffn_peer_ex(*a, **kw):  # the peer-memory transport's grouped GEMM (device-side counts)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        orig_peer_ex(*a, **kw)
+        e.record()
+        ffn_events.append((s, e))
+
+    K.expert_ffn_peer_ex = timed_ffn_peer_ex
 
     def barrier():
         if world > 1:
@@ -413,6 +423,7 @@ def run_ours(args, rank: int, world: int) -> None:
         total_ms = float(t)
     K.expert_ffn = orig
     K.expert_ffn_peer = orig_peer
+    K.expert_ffn_peer_ex = orig_peer_ex
 
     # e2e through the public block API with HOST buffers: every step uploads its own pinned input,
     # runs SparseMoeBlock.forward and downloads its output.  Steps are pipelined the way a server
