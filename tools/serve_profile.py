@@ -1,0 +1,47 @@
+"""Serving-time breakdown (Mixtral plugin, paper workload, wall clock): a short run under torch.profiler
+(CUPTI kernel timeline -> GPU busy vs span, per decode iteration) and a second one under cProfile (host
+hot spots).  python tools/serve_profile.py [rate] [seconds] [scheduler] > out.txt"""
+import cProfile
+import io
+import json
+import pstats
+import sys
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, DecoderMoEModel  # noqa: E402
+from paper_2503_09304_b200.serving import compare, warm_up  # noqa: E402
+
+rate = float(sys.argv[1]) if len(sys.argv) > 1 else 7.0
+secs = float(sys.argv[2]) if len(sys.argv) > 2 else 10.0
+sched = sys.argv[3] if len(sys.argv) > 3 else "baseline"
+m = DecoderMoEModel(MIXTRAL_8X7B)
+warm_up(m)
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    out = compare(m, rate, secs, schedulers=(sched,), kv_capacity_bytes=40 * 1024**3)
+r = out["fcfs" if sched == "baseline" else sched]
+ev = sorted((e.time_range.start, e.time_range.end) for e in prof.events()
+            if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0)
+busy, cs, ce = 0.0, None, None
+for s, e in ev:
+    if ce is None or s > ce:
+        if ce is not None:
+            busy += ce - cs
+        cs, ce = s, e
+    else:
+        ce = max(ce, e)
+if ce is not None:
+    busy += ce - cs
+span = ev[-1][1] - ev[0][0]
+print(json.dumps({"rate": rate, "seconds": secs, "scheduler": sched, "gpu_busy_ms": busy / 1e3, "gpu_span_ms": span / 1e3,
+                  "busy_frac": busy / span, "decode_iter_ms_median": r["decode_iter_ms_median"],
+                  "iterations": r["iterations"], "be_tokens_per_s": r["be_tokens_per_s"]}), flush=True)
+pr = cProfile.Profile()
+pr.enable()
+compare(m, rate, secs, schedulers=(sched,), kv_capacity_bytes=40 * 1024**3)
+pr.disable()
+buf = io.StringIO()
+pstats.Stats(pr, stream=buf).sort_stats("tottime").print_stats(30)
+print(buf.getvalue()[:9000])
