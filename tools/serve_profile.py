@@ -35,9 +35,26 @@ for s, e in ev:
 if ce is not None:
     busy += ce - cs
 span = ev[-1][1] - ev[0][0]
+# idle gaps of the GPU timeline by size: short ones inside an iteration (host enqueue behind the GPU),
+# long ones at iteration boundaries (token sync -> scheduler -> next iteration's first launch)
+gaps, ce = [], None
+for s, e in ev:
+    if ce is not None and s > ce:
+        gaps.append(s - ce)
+    ce = e if ce is None else max(ce, e)
+bins = {"<20us": 0.0, "20-100us": 0.0, "100-500us": 0.0, "0.5-2ms": 0.0, ">2ms": 0.0}
+cnt = dict.fromkeys(bins, 0)
+for g in gaps:
+    k = ("<20us" if g < 20 else "20-100us" if g < 100 else "100-500us" if g < 500 else "0.5-2ms" if g < 2000
+         else ">2ms")
+    bins[k] += g / 1e3
+    cnt[k] += 1
 print(json.dumps({"rate": rate, "seconds": secs, "scheduler": sched, "gpu_busy_ms": busy / 1e3, "gpu_span_ms": span / 1e3,
-                  "busy_frac": busy / span, "decode_iter_ms_median": r["decode_iter_ms_median"],
+                  "busy_frac": busy / span, "idle_ms_by_gap_size": bins, "gaps_by_size": cnt,
+                  "decode_iter_ms_median": r["decode_iter_ms_median"],
                   "iterations": r["iterations"], "be_tokens_per_s": r["be_tokens_per_s"]}), flush=True)
+if "--no-cprofile" in sys.argv:
+    sys.exit(0)
 pr = cProfile.Profile()
 pr.enable()
 compare(m, rate, secs, schedulers=(sched,), kv_capacity_bytes=40 * 1024**3)
