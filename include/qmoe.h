@@ -247,6 +247,12 @@ QMOE_API int qmoe_kv_append(void* pool, const int32_t* slot_mapping, const void*
  */
 QMOE_API int qmoe_kv_append_guarded(void* pool, const int32_t* slot_mapping, const void* rows, int n_rows,
                                     size_t row_bytes, const int32_t* guard, void* stream);
+/*
+ * qmoe_kv_append(_guarded) with source rows row_stride bytes apart (>= row_bytes): the K|V part of
+ * packed qkv projection rows goes to the pool with no staging copy.  guard may be null.
+ */
+QMOE_API int qmoe_kv_append_strided(void* pool, const int32_t* slot_mapping, const void* rows, int n_rows,
+                                    size_t row_bytes, size_t row_stride, const int32_t* guard, void* stream);
 /* dst[i] = pool[slot_mapping[i]] (one sequence's entries, ascending entry order). */
 QMOE_API int qmoe_kv_gather(const void* pool, const int32_t* slot_mapping, int n_rows, size_t row_bytes,
                    void* dst, void* stream);

@@ -91,6 +91,7 @@ SIGNATURES = {
                                          _vp]),
     "qmoe_ep_dispatch_dev": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_size, _c_int, _c_int, _vp, _vp,
                                       _vp, _vp, _vp, _vp]),
+    "qmoe_kv_append_strided": (_c_int, [_vp, _vp, _vp, _c_int, _c_size, _c_size, _vp, _vp]),
     "qmoe_ep_share_rows": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_size, _vp, _c_int, _c_int,
                                     _vp]),
     "qmoe_ep_collect_rows": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_size,

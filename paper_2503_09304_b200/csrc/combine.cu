@@ -103,14 +103,18 @@ combine_bf16_kernel(const __nv_bfloat16* __restrict__ y, const float* __restrict
   }
 }
 
+// src_stride: bytes between consecutive source rows in scatter mode (row_bytes when dense; e.g. the
+// K|V part of packed qkv rows for the KV append)
 __global__ void gather_rows_kernel(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx,
                                    int rows, size_t row_bytes, uint8_t* __restrict__ dst, int scatter,
-                                   const volatile int32_t* guard) {
+                                   const volatile int32_t* guard, size_t src_stride) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x * 8 + warp_id();
   if (r >= rows) return;
   if (guard != nullptr && *guard < 0) return;  // voided iteration (qmoe_kv_append_guarded)
   const int lane = lane_id();
-  const uint8_t* s = scatter ? src + (size_t)r * row_bytes : src + (size_t)idx[r] * row_bytes;
+  const uint8_t* s = scatter ? src + (size_t)r * src_stride : src + (size_t)idx[r] * row_bytes;
   uint8_t* d = scatter ? dst + (size_t)idx[r] * row_bytes : dst + (size_t)r * row_bytes;
   if ((row_bytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0) {
     const uint4* s4 = reinterpret_cast<const uint4*>(s);
@@ -142,13 +146,14 @@ __global__ void resume_point_kernel(int32_t* cursor, int ntok, const int32_t* st
 }
 
 int launch_rows(const void* src, const int32_t* idx, int rows, size_t row_bytes, void* dst, int scatter,
-                cudaStream_t s, const char* what, const int32_t* guard = nullptr) {
+                cudaStream_t s, const char* what, const int32_t* guard = nullptr, size_t src_stride = 0) {
   QMOE_REQUIRE(rows >= 0 && row_bytes > 0, "%s: bad sizes", what);
+  if (src_stride == 0) src_stride = row_bytes;
+  QMOE_REQUIRE(src_stride >= row_bytes, "%s: source row stride %zu < row bytes %zu", what, src_stride, row_bytes);
   if (rows == 0) return QMOE_OK;
   QMOE_REQUIRE(src && idx && dst, "%s: null pointer", what);
-  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, s>>>((const uint8_t*)src, idx, rows, row_bytes, (uint8_t*)dst,
-                                                    scatter, guard);
-  return check_launch(what);
+  return launch_pdl(what, gather_rows_kernel, dim3((rows + 7) / 8), dim3(256), 0, s, (const uint8_t*)src, idx, rows,
+                    row_bytes, (uint8_t*)dst, scatter, (const volatile int32_t*)guard, src_stride);
 }
 
 }  // namespace
@@ -257,6 +262,12 @@ extern "C" int qmoe_kv_append_guarded(void* pool, const int32_t* slot_mapping, c
                                       size_t row_bytes, const int32_t* guard, void* stream) {
   return qmoe::launch_rows(rows, slot_mapping, n_rows, row_bytes, pool, 1, qmoe::as_stream(stream),
                            "qmoe_kv_append_guarded", guard);
+}
+
+extern "C" int qmoe_kv_append_strided(void* pool, const int32_t* slot_mapping, const void* rows, int n_rows,
+                                      size_t row_bytes, size_t row_stride, const int32_t* guard, void* stream) {
+  return qmoe::launch_rows(rows, slot_mapping, n_rows, row_bytes, pool, 1, qmoe::as_stream(stream),
+                           "qmoe_kv_append_strided", guard, row_stride);
 }
 
 extern "C" int qmoe_kv_gather(const void* pool, const int32_t* slot_mapping, int n_rows, size_t row_bytes,

@@ -14,6 +14,8 @@ __global__ void __launch_bounds__(kNormThreads)
 rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ add,
                const __nv_bfloat16* __restrict__ w, float eps, int d, __nv_bfloat16* __restrict__ out,
                __nv_bfloat16* __restrict__ sum_out) {
+  pdl_wait();  // launched with programmatic dependent launch (launch_pdl): x comes from the predecessor
+  pdl_trigger();
   const int row = blockIdx.x;
   const __nv_bfloat16* xr = x + (size_t)row * d;
   const __nv_bfloat16* ar = add ? add + (size_t)row * d : nullptr;
@@ -85,6 +87,8 @@ rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restr
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k, const int64_t* __restrict__ pos,
                             const float* __restrict__ cos_t, const float* __restrict__ sin_t, int T, int H, int KV,
                             int hd, int q_stride, int k_stride) {
+  pdl_wait();
+  pdl_trigger();
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int heads = H + KV;
   if (gw >= T * heads) return;
@@ -109,10 +113,9 @@ extern "C" int qmoe_rmsnorm(const void* x, const void* residual_add, const void*
   QMOE_REQUIRE(T >= 0 && d > 0 && d % 8 == 0 && d <= 8 * 4 * kNormThreads, "qmoe_rmsnorm: bad sizes T=%d d=%d", T, d);
   QMOE_REQUIRE((residual_add == nullptr) == (sum_out == nullptr), "qmoe_rmsnorm: residual_add and sum_out go together");
   if (T == 0) return QMOE_OK;
-  rmsnorm_kernel<<<T, kNormThreads, 0, as_stream(stream)>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)residual_add,
-                                                            (const __nv_bfloat16*)weight, eps, d, (__nv_bfloat16*)out,
-                                                            (__nv_bfloat16*)sum_out);
-  return check_launch("qmoe_rmsnorm");
+  return launch_pdl("qmoe_rmsnorm", rmsnorm_kernel, dim3(T), dim3(kNormThreads), 0, as_stream(stream),
+                    (const __nv_bfloat16*)x, (const __nv_bfloat16*)residual_add, (const __nv_bfloat16*)weight, eps, d,
+                    (__nv_bfloat16*)out, (__nv_bfloat16*)sum_out);
 }
 
 extern "C" int qmoe_rope(void* q, void* k, const int64_t* positions, const float* cos_table, const float* sin_table,
@@ -121,8 +124,7 @@ extern "C" int qmoe_rope(void* q, void* k, const int64_t* positions, const float
   QMOE_REQUIRE(T >= 0 && head_dim % 2 == 0, "qmoe_rope: bad sizes");
   if (T == 0) return QMOE_OK;
   const int warps = T * (n_heads + n_kv_heads);
-  rope_kernel<<<(warps + 7) / 8, 256, 0, as_stream(stream)>>>((__nv_bfloat16*)q, (__nv_bfloat16*)k, positions, cos_table,
-                                                             sin_table, T, n_heads, n_kv_heads, head_dim, q_stride,
-                                                             k_stride);
-  return check_launch("qmoe_rope");
+  return launch_pdl("qmoe_rope", rope_kernel, dim3((warps + 7) / 8), dim3(256), 0, as_stream(stream), (__nv_bfloat16*)q,
+                    (__nv_bfloat16*)k, positions, cos_table, sin_table, T, n_heads, n_kv_heads, head_dim, q_stride,
+                    k_stride);
 }

@@ -195,6 +195,15 @@ class InferenceEngine:
         # are answered without waiting for their drain (1.0: none waits; see
         # _experts_device_preempt)
         self.report_tail = float(os.environ.get("QMOE_REPORT_TAIL", "1.0"))
+        # Report elision (set by the driver, wall clock only): when every answer within an iteration
+        # is provably the answer of its first report -- a built-in policy reads only the queues and
+        # the batch's priorities, and the driver admits no request inside an iteration (the arrival
+        # watcher defers admission to the iteration start and stops the GPU through the device flag)
+        # -- the reports after a CONTINUE first report are answered CONTINUE without the callback
+        # round trip (Qwen: 66 reports per layer).  Rollback reports are always delivered.
+        self.elide_reports = False
+        self._elide = False
+        self.stats["reports_elided"] = 0
 
     def next_batch_id(self) -> int:
         self._batch_counter += 1
@@ -238,17 +247,29 @@ class InferenceEngine:
         finally:
             self._end_iteration()
 
+    def _ask(self, on_report: ReportCallback, report_fn):
+        """Deliver one report (report_fn builds it) unless this iteration's reports are elided."""
+        if self._elide:
+            self.stats["reports_elided"] += 1
+            return SchedulerDirective.CONTINUE
+        d = on_report(report_fn())
+        if self.elide_reports and d is not PREEMPT:
+            self._elide = True
+        return d
+
     def _run(self, batch: Batch, st: _State, layer: int, stage: Stage, on_report: ReportCallback) -> IterationOutcome:
         m = self.model
         L = m.config.num_layers
         dev = self._device_preempt
+        self._elide = False
         while layer < L:
             if stage is Stage.ATTENTION:
                 st.x, st.res = m.attention_batch(layer, st.h, st.members, self.cache)
                 st.h = None
-                scanned = sum(self.cache.count(s.cache_handle, layer) for s in st.seqs)
-                self._charge(self.cost.attention_cost(st.T, scanned))
-                if on_report(self._report(batch, Stage.ATTENTION, layer, st)) is PREEMPT:
+                if not self._elide:
+                    scanned = sum(self.cache.count(s.cache_handle, layer) for s in st.seqs)
+                    self._charge(self.cost.attention_cost(st.T, scanned))
+                if self._ask(on_report, lambda: self._report(batch, Stage.ATTENTION, layer, st)) is PREEMPT:
                     if dev and self._prev_voided(sync=True):
                         return self._preempt_void(batch, on_report, layer)
                     self._preempt_at["ATTENTION"] += 1
@@ -259,7 +280,7 @@ class InferenceEngine:
                 st.ids, st.w = m.route_batch(layer, st.x)
                 st.y, st.cursor = m.new_expert_state(st.T)
                 self._charge(self.cost.router_cost)
-                if on_report(self._report(batch, Stage.ROUTER, layer, st)) is PREEMPT:
+                if self._ask(on_report, lambda: self._report(batch, Stage.ROUTER, layer, st)) is PREEMPT:
                     if dev and self._prev_voided(sync=True):
                         return self._preempt_void(batch, on_report, layer)
                     self._preempt_at["ROUTER"] += 1
@@ -468,7 +489,9 @@ class InferenceEngine:
         hit = self._last_hit = [e for e in range(E) if off[e + 1] > off[e]]
         stop = None
         wall = not getattr(self.clock, "virtual", True)
-        if self._on_expert_report is not None and wall:
+        if self._elide:
+            self.stats["reports_elided"] += len(hit)
+        elif self._on_expert_report is not None and wall:
             prog = self._progress_np
             tail_rows = self.report_tail * off[E]
             last = None

@@ -305,13 +305,23 @@ def cursor_advance(cursor: torch.Tensor, stop_dev: torch.Tensor) -> None:
 def kv_append(pool: torch.Tensor, slot_mapping: torch.Tensor, rows: torch.Tensor,
               guard: Optional[torch.Tensor] = None) -> None:
     """pool[slot_mapping[i]] = rows[i]; with guard (the iteration's int32 device preempt flag) the
-    append is skipped on the device when *guard < 0 (qmoe_kv_append_guarded)."""
+    append is skipped on the device when *guard < 0 (qmoe_kv_append_guarded).  rows [n, ...] may
+    have a row stride (each row itself dense, e.g. a slice of packed qkv rows): no staging copy."""
     _need(pool, "pool")
-    _need(rows, "rows", pool.dtype)
     _need(slot_mapping, "slot_mapping", torch.int32)
     n = rows.shape[0]
     row_bytes = rows[0].numel() * rows.element_size() if n else 1
     lib = _lib.load()
+    if not rows.is_contiguous():
+        if not rows.is_cuda or rows.dtype != pool.dtype or not rows[0].is_contiguous():
+            raise ValueError("rows must be CUDA rows of the pool dtype, each row dense")
+        stride = rows.stride(0) * rows.element_size()
+        if (stride | rows.data_ptr()) % 16:
+            raise ValueError("strided rows must be 16-byte aligned")
+        check(lib.qmoe_kv_append_strided(_ptr(pool), _ptr(slot_mapping), _ptr(rows), n, row_bytes, stride,
+                                         _ptr(guard), _stream()), "qmoe_kv_append_strided")
+        return
+    _need(rows, "rows", pool.dtype)
     if guard is None:
         check(lib.qmoe_kv_append(_ptr(pool), _ptr(slot_mapping), _ptr(rows), n, row_bytes, _stream()),
               "qmoe_kv_append")

@@ -161,7 +161,7 @@ class UnifiedDynamicCache:
         if len(slots):
             if not isinstance(slots, torch.Tensor):
                 slots = torch.tensor(slots, dtype=torch.int32, device=self.device)
-            K.kv_append(self._pools[layer], slots, rows.contiguous(), guard=guard)
+            K.kv_append(self._pools[layer], slots, rows if rows.is_cuda else rows.contiguous(), guard=guard)
 
     def entries(self, handle: int, layer: int) -> torch.Tensor:
         """All entries of one sequence at one layer, ascending entry order, gathered to [n, *row]."""

@@ -127,8 +127,7 @@ class DecoderMoEModel:
         emb = torch.cat([ang, ang], -1)
         self._cos, self._sin = emb.cos(), emb.sin()
         self._stop = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self._meta, self._meta_key = None, None
-        self._expect = None  # (handles, members, expected cached entries) of the current pass
+        self._pass = None  # (members, handles, ns, decode, expected cached entries, metadata) of the pass
         self.preempt_guard = None  # set by the engine per iteration (device-preempt mode)
         self._pinned_tok = None
         # decode attention: libqmoe's paged kernel (default) or flash-attn's (QMOE_FA_DECODE=1, A/B)
@@ -164,51 +163,51 @@ class DecoderMoEModel:
         T = h.shape[0]
         x = K.rmsnorm(h, L.ln1, cfg.rms_eps)
         qkv = x @ L.w_qkv.T
-        # Per-iteration metadata (positions, slot mapping, block table, lengths) is identical in
-        # every layer of a decode/prefill pass, so it is built once and reused across layers.
-        handles = [m.seq.cache_handle for m in members]
-        ns = [m.n for m in members]
-        haves = cache.counts_at(handles, layer)
-        key = tuple(zip(handles, haves, ns))
-        meta = self._meta if self._meta_key == key else None
-        decode = members[0].seq.phase is Phase.DECODE
-        # every member must hold exactly its fed tokens at this layer: the expectation is built
-        # once per pass (all layers expect the same counts) and compared as one list per layer
-        exp = self._expect
-        if exp is None or exp[0] != handles or exp[1] is not members:
+        # Per-pass state (handles, expected cached counts) and metadata (positions, slot mapping,
+        # block table, lengths) are identical in every layer of a decode/prefill pass: built at the
+        # pass's first layer (keyed by the engine's member list, one object per pass) and reused.
+        pas = self._pass
+        if pas is None or pas[0] is not members:
+            decode = members[0].seq.phase is Phase.DECODE
             for m in members:
                 if (m.seq.phase is Phase.DECODE) != decode:
                     raise StateCorruptionError(f"sequence {m.seq.id}: mixed phases in one batch")
-            exp = self._expect = (handles, members, [m.seq.tokens_fed() for m in members] if decode else [0] * len(members))
-        if haves != exp[2]:
-            bad = next(i for i, (a, b) in enumerate(zip(haves, exp[2])) if a != b)
+            handles = [m.seq.cache_handle for m in members]
+            expect = [m.seq.tokens_fed() for m in members] if decode else [0] * len(members)
+            pas = self._pass = (members, handles, [m.n for m in members], decode, expect, {})
+        _, handles, ns, decode, expect, meta = pas
+        # every member must hold exactly its fed tokens at this layer (one list comparison)
+        haves = cache.counts_at(handles, layer)
+        if haves != expect:
+            bad = next(i for i, (a, b) in enumerate(zip(haves, expect)) if a != b)
             raise StateCorruptionError(f"sequence {members[bad].seq.id} layer {layer}: {haves[bad]} cached entries")
-        slots = cache.reserve_batch(handles, layer, ns, want_slots=meta is None)
-        if meta is None:
-            pos = [p for (_, have, n) in key for p in range(have, have + n)]
-            meta = {"pos": torch.tensor(pos, dtype=torch.long, device=self.device),
-                    "slots": torch.tensor(slots, dtype=torch.int32, device=self.device)}
+        slots = cache.reserve_batch(handles, layer, ns, want_slots=not meta)
+        if not meta:
+            pos = [p for have, n in zip(expect, ns) for p in range(have, have + n)]
+            meta["pos"] = torch.tensor(pos, dtype=torch.long, device=self.device)
+            meta["slots"] = torch.tensor(slots, dtype=torch.int32, device=self.device)
             if decode:
-                tables = [cache.page_table(h_) for (h_, _, _) in key]
+                tables = [cache.page_table(h_) for h_ in handles]
                 width = max(len(t) for t in tables)
                 meta["bt"] = torch.tensor([t + [0] * (width - len(t)) for t in tables], dtype=torch.int32,
                                           device=self.device)
-                meta["lens"] = torch.tensor([have + n for (_, have, n) in key], dtype=torch.int32, device=self.device)
-                meta["max_len"] = max(have + n for (_, have, n) in key)
+                lens = [have + n for have, n in zip(expect, ns)]
+                meta["lens"] = torch.tensor(lens, dtype=torch.int32, device=self.device)
+                meta["max_len"] = max(lens)
             else:
                 cu = [0]
-                for (_, _, n) in key:
+                for n in ns:
                     cu.append(cu[-1] + n)
                 meta["cu"] = torch.tensor(cu, dtype=torch.int32, device=self.device)
-                meta["max"] = max(n for (_, _, n) in key)
-            self._meta, self._meta_key = meta, key
+                meta["max"] = max(ns)
         K.rope_(qkv, meta["pos"], self._cos, self._sin, H, KV, hd)
         q = qkv[:, : H * hd].view(T, H, hd)
         k = qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd)
         v = qkv[:, (H + KV) * hd:].view(T, KV, hd)
         # guard: the engine's per-iteration preempt flag in device-preempt mode (no append once an
         # expert launch of this iteration stopped early, see engine._experts_device_preempt)
-        cache.scatter(layer, meta["slots"], torch.stack([k, v], 1), guard=self.preempt_guard)
+        # the K|V half of each packed qkv row is the pool's [2, KV, hd] entry layout: appended in place
+        cache.scatter(layer, meta["slots"], qkv[:, H * hd:].view(T, 2, KV, hd), guard=self.preempt_guard)
         if decode and not self._fa_decode:
             # hand-written paged GQA decode attention on the page pool (csrc/attention.cu)
             attn = K.paged_decode_attention(q, cache.pool(layer), meta["bt"], meta["lens"], meta["max_len"],
@@ -262,7 +261,10 @@ class DecoderMoEModel:
         if self._pinned_tok is None or self._pinned_tok.numel() < len(rows):
             self._pinned_tok = torch.empty(max(64, len(rows)), dtype=torch.int32, pin_memory=True)
             self._tok_ready = torch.cuda.Event()
-        hl = h.index_select(0, torch.tensor(rows, dtype=torch.long, device=self.device))
+        if len(rows) == h.shape[0] and rows[-1] == len(rows) - 1:  # decode: every row is a last token
+            hl = h
+        else:
+            hl = h.index_select(0, torch.tensor(rows, dtype=torch.long, device=self.device))
         tok = K.lm_head_argmax(K.rmsnorm(hl.contiguous(), self.final_norm, self.cfg.rms_eps), self.lm_head)
         out = self._pinned_tok[: len(rows)]
         out.copy_(tok, non_blocking=True)

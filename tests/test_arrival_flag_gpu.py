@@ -99,6 +99,10 @@ def test_arrival_flags_are_transparent_on_the_reference_traces(cuda, name):
     pos = sim.engine.preemption_positions()
     print(name, pos, sim.engine.stats)
     assert pos.get("EXPERT_DEVICE_FLAG", 0) > 0
+    # report elision was on (wall clock, built-in policy, arrival watcher, no log): the reports after
+    # each iteration's first CONTINUE were answered without the callback, and the rollback reports
+    # of the flag-stopped launches still reached the scheduler
+    assert sim.engine.elide_reports and sim.engine.stats["reports_elided"] > 0
     assert {str(k): s.generated for k, s in sorted(res.sequences.items())} == rec["tokens"]
 
 
