@@ -1,4 +1,4 @@
-"""Serving-time breakdown (Mixtral plugin, paper workload, wall clock): a short run under torch.profiler
+"""Serving-time breakdown (Mixtral plugin, or Qwen with --qwen; paper workload, wall clock): a short run under torch.profiler
 (CUPTI kernel timeline -> GPU busy vs span, per decode iteration) and a second one under cProfile (host
 hot spots).  python tools/serve_profile.py [rate] [seconds] [scheduler] > out.txt"""
 import cProfile
@@ -11,13 +11,13 @@ sys.path.insert(0, ".")
 import torch  # noqa: E402
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
-from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, DecoderMoEModel  # noqa: E402
+from paper_2503_09304_b200.mixtral import MIXTRAL_8X7B, QWEN15_MOE_A27B, DecoderMoEModel  # noqa: E402
 from paper_2503_09304_b200.serving import compare, warm_up  # noqa: E402
 
 rate = float(sys.argv[1]) if len(sys.argv) > 1 else 7.0
 secs = float(sys.argv[2]) if len(sys.argv) > 2 else 10.0
 sched = sys.argv[3] if len(sys.argv) > 3 else "baseline"
-m = DecoderMoEModel(MIXTRAL_8X7B)
+m = DecoderMoEModel(QWEN15_MOE_A27B if "--qwen" in sys.argv else MIXTRAL_8X7B)
 warm_up(m)
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     out = compare(m, rate, secs, schedulers=(sched,), kv_capacity_bytes=40 * 1024**3)
