@@ -234,6 +234,8 @@ class InferenceEngine:
         self._on_expert_report = on_expert_report
         if [s.id for s in sequences] != batch.members:
             raise SimulationError("sequence list does not match batch members")
+        if hasattr(self.model, "pass_serial"):
+            self.model.pass_serial += 1  # per-pass buffers of the plugin (DecoderMoEModel.new_expert_state)
         st = self._init_state(sequences)
         layer, stage = batch.layer_cursor, batch.stage_cursor
         if stage not in (Stage.ATTENTION, Stage.ROUTER, Stage.EXPERTS):

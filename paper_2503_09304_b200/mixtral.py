@@ -128,6 +128,8 @@ class DecoderMoEModel:
         self._cos, self._sin = emb.cos(), emb.sin()
         self._stop = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._pass = None  # (members, handles, ns, decode, expected cached entries, metadata) of the pass
+        self.pass_serial = 0  # bumped by the engine at every execute (new_expert_state buffers)
+        self._pass_bufs = None
         self.preempt_guard = None  # set by the engine per iteration (device-preempt mode)
         self._pinned_tok = None
         # decode attention: libqmoe's paged kernel (default) or flash-attn's (QMOE_FA_DECODE=1, A/B)
@@ -226,8 +228,16 @@ class DecoderMoEModel:
         return K.router(x, self.layers[layer].w_router, self.cfg.top_k, self.cfg.route_mode, n_shared=self.n_shared)
 
     def new_expert_state(self, T: int):
-        y = torch.empty((T * self.config.top_k, self.cfg.hidden_dim), dtype=self.dtype, device=self.device)
-        return y, torch.zeros(T, dtype=torch.int32, device=self.device)
+        """Expert outputs y and per-token cursors of a layer.  One pair serves every layer of an
+        engine pass (pass_serial, set by the engine per execute): within a pass the cursors stay zero
+        (only a preemption advances them, and it ends the pass), layer l's y is consumed by its
+        combine before layer l + 1's grouped launch writes (stream order; a launch behind an early
+        stop claims nothing), and a checkpoint keeps views of its own pass's pair only."""
+        b = self._pass_bufs
+        if b is None or b[0] != self.pass_serial or b[1] != T:
+            y = torch.empty((T * self.config.top_k, self.cfg.hidden_dim), dtype=self.dtype, device=self.device)
+            b = self._pass_bufs = (self.pass_serial, T, y, torch.zeros(T, dtype=torch.int32, device=self.device))
+        return b[2], b[3]
 
     def permute(self, ids, cursor, x):
         return K.permute(ids, self.config.num_experts, cursor=cursor, x=x)
