@@ -228,16 +228,17 @@ class DecoderMoEModel:
         return K.router(x, self.layers[layer].w_router, self.cfg.top_k, self.cfg.route_mode, n_shared=self.n_shared)
 
     def new_expert_state(self, T: int):
-        """Expert outputs y and per-token cursors of a layer.  One pair serves every layer of an
-        engine pass (pass_serial, set by the engine per execute): within a pass the cursors stay zero
-        (only a preemption advances them, and it ends the pass), layer l's y is consumed by its
-        combine before layer l + 1's grouped launch writes (stream order; a launch behind an early
-        stop claims nothing), and a checkpoint keeps views of its own pass's pair only."""
+        """Expert outputs y (fresh per layer) and per-token cursors.  One cursor vector serves every
+        layer of an engine pass (pass_serial, set by the engine per execute): within a pass the
+        cursors stay zero (only a preemption advances them, and it ends the pass), and a checkpoint
+        keeps views of its own pass's vector only -- one fill kernel per pass instead of per layer.
+        (y is not shared: a launch behind an early stop, run ahead by the host, may still write its
+        split-K reduction rows.)"""
+        y = torch.empty((T * self.config.top_k, self.cfg.hidden_dim), dtype=self.dtype, device=self.device)
         b = self._pass_bufs
         if b is None or b[0] != self.pass_serial or b[1] != T:
-            y = torch.empty((T * self.config.top_k, self.cfg.hidden_dim), dtype=self.dtype, device=self.device)
-            b = self._pass_bufs = (self.pass_serial, T, y, torch.zeros(T, dtype=torch.int32, device=self.device))
-        return b[2], b[3]
+            b = self._pass_bufs = (self.pass_serial, T, torch.zeros(T, dtype=torch.int32, device=self.device))
+        return y, b[2]
 
     def permute(self, ids, cursor, x):
         return K.permute(ids, self.config.num_experts, cursor=cursor, x=x)
