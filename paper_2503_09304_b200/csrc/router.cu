@@ -565,6 +565,99 @@ int launch_router_stream(const void* x, const void* wr, int T_, int d, int E, in
                     ids, (float*)w, (float*)logits);
 }
 
+// ---- bf16, many tokens, <= 8 experts: persistent CTAs with W_router held in registers ------------
+// The streamed kernel above re-reads W_router (8 x d) from L2 for every 16-token tile: a read probe
+// of the same access pattern (tools/scratch/stream_probe.cu) streams X alone in 12.9 us at 8k
+// tokens but 16.4 us with the W reads.  Here each warp loads its d slice of W_router ONCE into
+// registers (KS k32 steps x 16 B per lane, in the same k permutation as the X fragments), and the
+// CTAs (2 per SM) walk 16-token tiles in a grid stride, so only X streams from HBM.  Same per-warp
+// k order and slice reduction as router_stream_kernel<8, 1, 1, U>: bit-identical logits.
+template <int KS, int U>
+__global__ void __launch_bounds__(256, 2)
+router_wreg_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr, int ntok, int d,
+                   int E, int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
+                   float* __restrict__ logits_out) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int DS = 8;
+  __shared__ float s_part[DS][16][8];
+  __shared__ float s_logit[16][kMaxE];
+  __shared__ float s_score[16][kMaxE];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int k0 = warp * KS * 32;  // this warp's d slice: KS k32 steps
+  uint4 wf[KS];                   // W_router[g][k0 + 32 s + 8 t4 .. +8] for every step s
+  {
+    const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)min(g, E - 1) * d + k0) + t4;
+#pragma unroll
+    for (int st = 0; st < KS; ++st) wf[st] = __ldg(wp + 4 * st);
+  }
+  const int ntiles = (ntok + 15) / 16;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int tok0 = tile * 16;
+    const uint4* xr0 = reinterpret_cast<const uint4*>(x + (size_t)min(tok0 + g, ntok - 1) * d + k0) + t4;
+    const uint4* xr1 = reinterpret_cast<const uint4*>(x + (size_t)min(tok0 + g + 8, ntok - 1) * d + k0) + t4;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint4 a0[2][U], a1[2][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a0[0][u] = ld_stream<true>(xr0 + 4 * u);
+      a1[0][u] = ld_stream<true>(xr1 + 4 * u);
+    }
+#pragma unroll
+    for (int s0 = 0; s0 < KS; s0 += U) {
+      const int buf = (s0 / U) & 1;
+      if (s0 + U < KS) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          a0[buf ^ 1][u] = ld_stream<true>(xr0 + 4 * (s0 + U + u));
+          a1[buf ^ 1][u] = ld_stream<true>(xr1 + 4 * (s0 + U + u));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint4 b = wf[s0 + u];
+        mma_bf16_16816(acc, a0[buf][u].x, a1[buf][u].x, a0[buf][u].y, a1[buf][u].y, b.x, b.y);
+        mma_bf16_16816(acc, a0[buf][u].z, a1[buf][u].z, a0[buf][u].w, a1[buf][u].w, b.z, b.w);
+      }
+    }
+    const int c = 2 * t4;
+    s_part[warp][g][c] = acc[0];
+    s_part[warp][g][c + 1] = acc[1];
+    s_part[warp][g + 8][c] = acc[2];
+    s_part[warp][g + 8][c + 1] = acc[3];
+    __syncthreads();
+    if (threadIdx.x < 16 * 8) {
+      const int t = threadIdx.x >> 3, e = threadIdx.x & 7;
+      float v = s_part[0][t][e];
+#pragma unroll
+      for (int sl = 1; sl < DS; ++sl) v += s_part[sl][t][e];
+      s_logit[t][e] = v;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int ti = warp; ti < 16; ti += 8) {
+      const int tok = tok0 + ti;
+      if (tok >= ntok) break;
+      select_token<float>(s_logit[ti], s_score[ti], tok, E, k, mode, lane, ids_out, w_out, logits_out);
+    }
+    __syncthreads();  // s_part / s_logit are rewritten by the next tile
+  }
+}
+
+int device_sm_count() {
+  static int counts[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (counts[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    counts[dev] = n > 0 ? n : 148;
+  }
+  return counts[dev];
+}
+
 // 0 = not applicable (shape), else launched.  QMOE_ROUTER_STREAM=0 keeps the cp.async kernel.
 int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
                       void* logits, cudaStream_t s, int* st) {
@@ -595,6 +688,16 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
     return 1;                                                                                        \
   }
   if (E <= 8) {
+    // W_router in registers, persistent CTAs (d = 4096: 16 k32 steps per warp); QMOE_ROUTER_CFG=5
+    // forces it at any size, -1 keeps the streamed tilings
+    if (d == 4096 && (cfg == 5 || (cfg == 0 && T_ >= 4096))) {  // (8 d slices: the streamed kernels' order)
+      const int ntiles = (T_ + 15) / 16;
+      const int grid = std::min(ntiles, 2 * device_sm_count());
+      *st = launch_pdl("qmoe_router(wreg)", router_wreg_kernel<16, 2>, dim3(grid), dim3(256), 0, s,
+                       (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,
+                       (float*)logits);
+      return 1;
+    }
     if (cfg == 1) { QMOE_TRY_STREAM(8, 1, 1, 4) }
     // from ~6k tokens: 64 registers so 4 CTAs fit an SM and 512+ CTAs run in one wave (the
     // 3-per-SM build leaves a 15% second wave: 29.5 -> 26.5 us at 8k tokens, 52 -> 44 us at 16k)
