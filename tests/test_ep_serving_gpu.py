@@ -37,7 +37,7 @@ def _trace():
     return trace_for_rate(spec, 12.0, seed=4)
 
 
-def _run(model):
+def _run(model, clock=None):
     import numpy as np
 
     from paper_2503_09304_b200.core import SchedulerDirective
@@ -49,7 +49,8 @@ def _run(model):
         return (SchedulerDirective.PREEMPT_AT_NEXT_BOUNDARY if rng.random() < 0.15
                 else SchedulerDirective.CONTINUE)
 
-    sim = Simulation(_trace(), model=model, scheduler="qllm", max_batch_size=6, policy=policy, record_log=True)
+    sim = Simulation(_trace(), model=model, scheduler="qllm", max_batch_size=6, policy=policy, record_log=True,
+                     clock=clock)
     res = sim.run()
     return {"log": [list(e) for e in res.log], "tokens": {k: s.generated for k, s in sorted(res.sequences.items())},
             "records": [[r.seq_id, r.first_token_ms, r.finish_ms] for r in res.records],
@@ -74,6 +75,13 @@ def _worker(rank, world, port, kind, q):
         model = ExpertParallelDecoder(_cfg(kind), rank, world, device=torch.device("cuda", 0), seed=5,
                                       barrier_timeout_s=60.0)
         out = _run(model)
+        # the same trace on the ranks' shared wall clock: timing-dependent decisions, but every rank
+        # must take the same ones (replicated state, one clock)
+        from paper_2503_09304_b200.ep_serving import LockstepClock
+
+        lock = _run(model, clock=LockstepClock())
+        out["lockstep_log"] = lock["log"]
+        out["lockstep_tokens"] = lock["tokens"]
         torch.cuda.synchronize()
         out["barrier_error"] = int(model.error.item())
         out["exchanges"] = model.stats["exchanges"]
@@ -112,3 +120,5 @@ def test_expert_parallel_serving_equals_single_gpu(cuda, kind):
         assert g["log"] == want["log"], f"rank {rank}: decision log differs from the single-GPU run"
         assert g["tokens"] == want["tokens"]
         assert g["records"] == want["records"]
+    assert got[0]["lockstep_log"] == got[1]["lockstep_log"] and len(got[0]["lockstep_log"]) > 0
+    assert got[0]["lockstep_tokens"] == got[1]["lockstep_tokens"]
