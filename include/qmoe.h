@@ -350,6 +350,28 @@ QMOE_API int qmoe_ep_collect_rows(const void* recv, void* y, const int32_t* perm
                                   void* stream);
 
 /*
+ * qmoe_permute with the row gather limited to the queues of experts [0, gather_e_end) (Xp rows of
+ * later experts are left unwritten), for qmoe_expert_ffn_xs.
+ */
+QMOE_API int qmoe_permute_ex(const int32_t* ids, const int32_t* cursor, int T, int k, int E, int gather_e_end,
+                             int32_t* perm_out, int32_t* offsets_out, void* workspace, size_t workspace_bytes,
+                             const void* x, void* xp, size_t row_bytes, void* stream);
+/*
+ * qmoe_expert_ffn_ex (bf16 SwiGLU) where experts [x_first, E) read their token rows straight from
+ * x [T, d] instead of Xp: each such expert's queue must hold every token once in token order
+ * (Qwen's shared sub-experts -- every token has one slot per sub-expert, and the stable permute
+ * keeps token order), so queue row r of expert e is x row r - offsets[e] and the permute need not
+ * gather it (qmoe_permute_ex with gather_e_end = x_first).  Same tiles and MMA order as the
+ * gathered path (identical results).  Only the single-launch 1-CTA path
+ * (QMOE_PATH_FUSED_1CTA for these d, F, E, xp_rows) supports it; otherwise QMOE_ERR_UNSUPPORTED.
+ */
+QMOE_API int qmoe_expert_ffn_xs(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
+                                const void* gate_up, const void* down, int e_begin, int e_end, int xp_rows,
+                                void* act_ws, void* y, const volatile int32_t* preempt_flag, int32_t* cursor_out,
+                                int32_t* progress, int32_t progress_seq, const void* x, int T, int x_first,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Decoder-side fused helpers (outside the north-star path; used by the Mixtral/Qwen serving
  * plugin to cut per-layer launch counts).  bf16 only.
  * qmoe_rmsnorm: out = rmsnorm(x [+ residual_add]) * weight (HF MixtralRMSNorm rounding);

@@ -91,6 +91,10 @@ SIGNATURES = {
                                          _vp]),
     "qmoe_ep_dispatch_dev": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_size, _c_int, _c_int, _vp, _vp,
                                       _vp, _vp, _vp, _vp]),
+    "qmoe_permute_ex": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_size, _vp, _vp, _c_size,
+                                 _vp]),
+    "qmoe_expert_ffn_xs": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _vp,
+                                    _vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_size, _vp]),
     "qmoe_kv_append_strided": (_c_int, [_vp, _vp, _vp, _c_int, _c_size, _c_size, _vp, _vp]),
     "qmoe_ep_share_rows": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_size, _vp, _c_int, _c_int,
                                     _vp]),

@@ -176,3 +176,37 @@ extern "C" int qmoe_expert_ffn_gather(const void* x, int T, int k, const int32_t
   return expert_ffn_fused(nullptr, offsets, perm, E, d, F, gate_up, down, e_begin, e_end, act_ws, y, preempt_flag,
                           cursor_out, ws, rows, nullptr, path == QMOE_PATH_FUSED_PAIR, x, T, k, s);
 }
+
+extern "C" int qmoe_expert_ffn_xs(const void* xp, const int32_t* offsets, const int32_t* perm, int E, int d, int F,
+                                  const void* gate_up, const void* down, int e_begin, int e_end, int xp_rows,
+                                  void* act_ws, void* y, const volatile int32_t* preempt_flag, int32_t* cursor_out,
+                                  int32_t* progress, int32_t progress_seq, const void* x, int T, int x_first,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace qmoe;
+  QMOE_REQUIRE(E >= 1 && E <= 64 && d >= 1 && F >= 1, "qmoe_expert_ffn_xs: bad sizes E=%d d=%d F=%d", E, d, F);
+  QMOE_REQUIRE(0 <= e_begin && e_begin <= e_end && e_end <= E, "qmoe_expert_ffn_xs: bad expert range [%d, %d)",
+               e_begin, e_end);
+  QMOE_REQUIRE(0 <= x_first && x_first <= E && T >= 0, "qmoe_expert_ffn_xs: bad x_first %d / T %d", x_first, T);
+  QMOE_REQUIRE(workspace != nullptr &&
+                   workspace_bytes >= qmoe_expert_ffn_workspace_bytes(QMOE_EXPERT_SWIGLU, QMOE_BF16, d, xp_rows),
+               "qmoe_expert_ffn_xs: workspace too small");
+  FfnWorkspace* ws = reinterpret_cast<FfnWorkspace*>(workspace);
+  cudaStream_t s = as_stream(stream);
+  if (xp_rows == 0 || e_begin == e_end) {
+    const int st = ffn_finalize(ws, nullptr, e_end, cursor_out, s);
+    return st ? st : ffn_progress_all(progress, progress_seq, e_begin, e_end, s);
+  }
+  QMOE_REQUIRE(xp && x && offsets && perm && gate_up && down && act_ws && y, "qmoe_expert_ffn_xs: null pointer");
+  QMOE_REQUIRE(((uintptr_t)xp | (uintptr_t)x | (uintptr_t)gate_up | (uintptr_t)y | (uintptr_t)act_ws) % 16 == 0,
+               "qmoe_expert_ffn_xs: buffers must be 16-byte aligned");
+  if (expert_ffn_path(d, F, E, xp_rows) != QMOE_PATH_FUSED_1CTA || !use_fused_tc()) {
+    set_error("qmoe_expert_ffn_xs: direct-X rows need the single-launch 1-CTA path (this shape takes path %d)",
+              expert_ffn_path(d, F, E, xp_rows));
+    return QMOE_ERR_UNSUPPORTED;
+  }
+  int st = tc_init_driver();
+  if (st) return st;
+  return expert_ffn_fused(xp, offsets, perm, E, d, F, gate_up, down, e_begin, e_end, act_ws, y, preempt_flag,
+                          cursor_out, ws, xp_rows, nullptr, false, nullptr, T, 0, s, progress, progress_seq, x,
+                          x_first);
+}

@@ -271,7 +271,8 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
                      const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
                      void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s,
-                     int32_t* progress = nullptr, int seq = 0);
+                     int32_t* progress = nullptr, int seq = 0, const void* x_direct = nullptr,
+                     int x_first = 0);
 // Mid-size batches of fine-grained experts (expert_fused.cu): swap-AB CTA-pair tiles (256 weight
 // rows x <= 256 tokens, N sized to the valid rows), gate_up and down in one persistent launch.
 bool use_swap_pair(int xp_rows, int n_experts, int d, int F);

@@ -53,6 +53,8 @@ struct FusedParams {
   int32_t* progress;  // optional host-mapped per-expert progress words (signal_expert_done)
   int seq;
   int merge;  // swap-AB pair: remainder rows (<= merge) folded into an expert's last token tile
+  int x_first;  // 1-CTA kernel: experts >= x_first read their A rows straight from X (row m0 -
+                // offsets[e]; Qwen's shared sub-experts, whose queues are X's rows in order)
 };
 
 // Token rows of one 128-row A tile for the gather: lane l owns rows [4l, 4l+4) of the tile; rows
@@ -73,7 +75,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 __global__ void __launch_bounds__(kThreadsF, 1)
 ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                  const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW2,
-                 FusedParams p) {
+                 const __grid_constant__ CUtensorMap tmXd, FusedParams p) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
@@ -158,7 +160,9 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
       const bool gather = up && p.gather;
       int g[4] = {0, 0, 0, 0};
       if (gather) gather_rows4(p, m0, p.offsets[e + 1], lane, g);
-      const CUtensorMap* ta = up ? &tmX : &tmAct;
+      const bool direct = up && e >= p.x_first;  // A rows = X rows m0 - offsets[e] .. (never with gather)
+      const CUtensorMap* ta = up ? (direct ? &tmXd : &tmX) : &tmAct;
+      const int arow = direct ? m0 - p.offsets[e] : m0;
       const CUtensorMap* tb = up ? &tmW1 : &tmW2;
       // B rows: gate_up -> gate [n0, +128) over up F + [n0, +128); down -> [n0, +256)
       const int brow0 = up ? e * 2 * p.F + n0 : e * p.d + n0;
@@ -169,7 +173,7 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         uint8_t* sa = smem + stage * kStageBytesF;
         if (lane == 0) {
           ptx::mbar_arrive_expect_tx(&full_bar[stage], kStageBytesF);
-          if (!gather) ptx::tma_load_2d(ta, &full_bar[stage], sa, kb * kBKf, m0, ptx::kEvictNormal);
+          if (!gather) ptx::tma_load_2d(ta, &full_bar[stage], sa, kb * kBKf, arow, ptx::kEvictNormal);
           ptx::tma_load_2d(tb, &full_bar[stage], sa + kABytesF, kb * kBKf, brow0, ptx::kEvictNormal);
           ptx::tma_load_2d(tb, &full_bar[stage], sa + kABytesF + (kBN / 2) * 128, kb * kBKf, brow1,
                            ptx::kEvictNormal);
@@ -940,9 +944,11 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
                      const void* w1, const void* w2, int e_begin, int e_end, void* act_ws, void* y,
                      const volatile int32_t* flag, int32_t* cursor_out, FfnWorkspace* ws, int xp_rows,
                      void* const* y_peers, bool pair, const void* x, int T, int k, cudaStream_t s,
-                     int32_t* progress, int seq) {
+                     int32_t* progress, int seq, const void* x_direct, int x_first) {
   int st;
-  CUtensorMap maps[4];
+  CUtensorMap maps[5];
+  QMOE_REQUIRE(x_direct == nullptr || (!pair && x == nullptr), "qmoe_expert_ffn_xs: direct-X rows need the 1-CTA tiles");
+  if (x_direct != nullptr && (st = tc_make_map(&maps[4], x_direct, T, d, kBM))) return st;
   // A boxes: 128 token rows (each CTA of a pair loads its own 128), or single rows of X for the
   // tile::gather4 loads (x != nullptr); B boxes: 128 weight rows
   if ((st = x != nullptr ? tc_make_map(&maps[0], x, T, d, 1) : tc_make_map(&maps[0], xp, xp_rows, d, kBM)) ||
@@ -968,6 +974,8 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
   p.cursor = cursor_out;
   p.progress = progress;
   p.seq = seq;
+  p.x_first = x_direct != nullptr ? x_first : INT_MAX;
+  if (x_direct == nullptr) maps[4] = maps[0];  // unused
   static uint64_t attr_set = 0;  // devices already configured
   if (!(attr_set & current_device_bit())) {
     QMOE_CUDA_TRY(cudaFuncSetAttribute(ffn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemF));
@@ -978,7 +986,7 @@ int expert_ffn_fused(const void* xp, const int32_t* offsets, const int32_t* perm
     return launch_pdl("qmoe_expert_ffn(tcgen05 single launch, pair)", ffn_fused_pair_kernel,
                       dim3((tc_num_sms() / 2) * 2), dim3(kThreadsF), kSmemP, s, maps[0], maps[1], maps[2], maps[3], p);
   return launch_pdl("qmoe_expert_ffn(tcgen05 single launch)", ffn_fused_kernel, dim3(tc_num_sms()), dim3(kThreadsF),
-                    kSmemF, s, maps[0], maps[1], maps[2], maps[3], p);
+                    kSmemF, s, maps[0], maps[1], maps[2], maps[3], maps[4], p);
 }
 
 // Batches past the swap-AB range (checked first) of coarse experts: the swap-AB CTA-pair kernel,

@@ -65,13 +65,15 @@ __device__ __forceinline__ void copy_row(const uint8_t* __restrict__ src, uint8_
 }
 
 // Wide row gather for multi-chunk launches: Xp[r] = X[perm[r] / k], one warp per row.
+// gather_e: rows of experts >= gather_e are not gathered (their A operand is read straight from X,
+// qmoe_expert_ffn_xs: the shared sub-experts' queues are X's rows in order).
 __global__ void __launch_bounds__(256) perm_gather_kernel(const int32_t* __restrict__ perm,
-                                                          const int32_t* __restrict__ offsets, int E, int k,
+                                                          const int32_t* __restrict__ offsets, int gather_e, int k,
                                                           int max_rows, const uint8_t* __restrict__ x,
                                                           uint8_t* __restrict__ xp, size_t row_bytes) {
   pdl_wait();
   pdl_trigger();
-  const int R = offsets[E];
+  const int R = offsets[gather_e];
   const int lane = lane_id();
   for (int r = blockIdx.x * 8 + warp_id(); r < R && r < max_rows; r += gridDim.x * 8)
     copy_row(x + (size_t)(perm[r] / k) * row_bytes, xp + (size_t)r * row_bytes, row_bytes, lane);
@@ -197,11 +199,24 @@ extern "C" size_t qmoe_permute_workspace_bytes(int T, int k, int E) {
   return (size_t)((nblk < 1 ? 1 : nblk) * (E < 1 ? 1 : E)) * sizeof(int32_t);
 }
 
+extern "C" int qmoe_permute_ex(const int32_t* ids, const int32_t* cursor, int T, int k, int E, int gather_e_end,
+                               int32_t* perm_out, int32_t* offsets_out, void* workspace, size_t workspace_bytes,
+                               const void* x, void* xp, size_t row_bytes, void* stream);
+
 extern "C" int qmoe_permute(const int32_t* ids, const int32_t* cursor, int T, int k, int E,
                             int32_t* perm_out, int32_t* offsets_out, void* workspace,
                             size_t workspace_bytes, const void* x, void* xp, size_t row_bytes,
                             void* stream) {
+  return qmoe_permute_ex(ids, cursor, T, k, E, E, perm_out, offsets_out, workspace, workspace_bytes, x, xp, row_bytes,
+                         stream);
+}
+
+extern "C" int qmoe_permute_ex(const int32_t* ids, const int32_t* cursor, int T, int k, int E, int gather_e_end,
+                               int32_t* perm_out, int32_t* offsets_out, void* workspace, size_t workspace_bytes,
+                               const void* x, void* xp, size_t row_bytes, void* stream) {
   using namespace qmoe;
+  QMOE_REQUIRE(gather_e_end >= 0 && gather_e_end <= E, "qmoe_permute_ex: gather_e_end %d outside [0, %d]", gather_e_end,
+               E);
   QMOE_REQUIRE(T >= 0 && k >= 1 && E >= 1 && E <= kMaxE, "qmoe_permute: bad sizes T=%d k=%d E=%d", T, k, E);
   QMOE_REQUIRE(offsets_out != nullptr, "qmoe_permute: offsets_out is null");
   QMOE_REQUIRE((x == nullptr) == (xp == nullptr), "qmoe_permute: x and xp must both be set or both null");
@@ -234,7 +249,7 @@ extern "C" int qmoe_permute(const int32_t* ids, const int32_t* cursor, int T, in
     const int rows = (int)S;
     const int grid = rows / 8 < 148 * 16 ? (rows + 7) / 8 : 148 * 16;
     if ((st = launch_pdl("qmoe_permute(gather)", perm_gather_kernel, dim3(grid), dim3(256), 0, s, perm_out,
-                         offsets_out, E, k, rows, (const uint8_t*)x, (uint8_t*)xp, row_bytes)))
+                         offsets_out, gather_e_end, k, rows, (const uint8_t*)x, (uint8_t*)xp, row_bytes)))
       return st;
   }
   return QMOE_OK;

@@ -108,6 +108,7 @@ class ExpertParallelDecoder(DecoderMoEModel):
         super().__init__(cfg, device=device, seed=seed, dtype=dtype,
                          expert_range=(self.bounds[rank], self.bounds[rank + 1]))
         self.timeout_s = barrier_timeout_s
+        self._direct_shared = False  # the local slice of the queues reads gathered rows only
         self.flags = torch.zeros(world, dtype=torch.int32, device=self.device)
         self.error = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.epoch = 0

@@ -24,6 +24,7 @@ EXPERT_TANH_AFFINE = _lib.QMOE_EXPERT_TANH_AFFINE
 EXPERT_SWIGLU = _lib.QMOE_EXPERT_SWIGLU
 
 _workspaces: dict[tuple[int, int, str], torch.Tensor] = {}
+_SHARED_DIRECT = __import__("os").environ.get("QMOE_SHARED_DIRECT", "1") != "0"
 
 
 def _stream() -> int:
@@ -96,11 +97,12 @@ def router(x: torch.Tensor, w_router: torch.Tensor, k: int, mode: int = ROUTE_TO
 
 
 def permute(ids: torch.Tensor, num_experts: int, cursor: Optional[torch.Tensor] = None,
-            x: Optional[torch.Tensor] = None):
+            x: Optional[torch.Tensor] = None, gather_e_end: Optional[int] = None):
     """Stable expert-major order of the pending slots.
 
     Returns (perm [T*k] int32 — only the first offsets[E] entries are meaningful,
-    offsets [E+1] int32, xp [T*k, d] gathered rows or None)."""
+    offsets [E+1] int32, xp [T*k, d] gathered rows or None).  gather_e_end: gather only the rows of
+    experts below it (qmoe_permute_ex; the rest are read from x by expert_ffn(x_direct=...))."""
     _need(ids, "ids", torch.int32)
     T, k = ids.shape
     if cursor is not None:
@@ -120,8 +122,13 @@ def permute(ids: torch.Tensor, num_experts: int, cursor: Optional[torch.Tensor] 
     lib = _lib.load()
     nbytes = lib.qmoe_permute_workspace_bytes(T, k, num_experts)
     ws = workspace(nbytes, "permute", ids.device)
-    check(lib.qmoe_permute(_ptr(ids), _ptr(cursor), T, k, num_experts, _ptr(perm), _ptr(offsets), _ptr(ws), nbytes,
-                           _ptr(x), _ptr(xp), row_bytes, _stream()), "qmoe_permute")
+    if gather_e_end is None:
+        check(lib.qmoe_permute(_ptr(ids), _ptr(cursor), T, k, num_experts, _ptr(perm), _ptr(offsets), _ptr(ws),
+                               nbytes, _ptr(x), _ptr(xp), row_bytes, _stream()), "qmoe_permute")
+    else:
+        check(lib.qmoe_permute_ex(_ptr(ids), _ptr(cursor), T, k, num_experts, int(gather_e_end), _ptr(perm),
+                                  _ptr(offsets), _ptr(ws), nbytes, _ptr(x), _ptr(xp), row_bytes, _stream()),
+              "qmoe_permute_ex")
     return perm, offsets, xp
 
 
@@ -129,7 +136,7 @@ def expert_ffn(variant: int, xp: torch.Tensor, offsets: torch.Tensor, perm: torc
                w2: torch.Tensor, y: torch.Tensor, e_begin: int = 0, e_end: Optional[int] = None,
                act_ws: Optional[torch.Tensor] = None, preempt_flag: Optional[torch.Tensor] = None,
                cursor_out: Optional[torch.Tensor] = None, progress: Optional[torch.Tensor] = None,
-               progress_seq: int = 0) -> None:
+               progress_seq: int = 0, x_direct: Optional[torch.Tensor] = None, x_first: int = 0) -> None:
     """Run experts [e_begin, e_end) over their rows of xp; results land in y[perm[r]] (slot order).
 
     TANH_AFFINE: w1 = A [E, d, d], w2 = b [E, d].  SWIGLU: w1 = gate_up [E, 2F, d], w2 = down [E, d, F],
@@ -165,6 +172,15 @@ def expert_ffn(variant: int, xp: torch.Tensor, offsets: torch.Tensor, perm: torc
     lib = _lib.load()
     nbytes = lib.qmoe_expert_ffn_workspace_bytes(variant, _code(xp), d, xp.shape[0])
     ws = workspace(nbytes, "ffn", xp.device)
+    if x_direct is not None:  # experts >= x_first read token rows straight from x (qmoe_expert_ffn_xs)
+        _need(x_direct, "x_direct", xp.dtype)
+        if progress is not None and (not progress.is_pinned() or progress.dtype != torch.int32):
+            raise ValueError("progress must be a pinned host int32 tensor")
+        check(lib.qmoe_expert_ffn_xs(_ptr(xp), _ptr(offsets), _ptr(perm), E, d, F, _ptr(w1), _ptr(w2), e_begin, e_end,
+                                     xp.shape[0], _ptr(act_ws), _ptr(y), _ptr(preempt_flag), _ptr(cursor_out),
+                                     _ptr(progress), int(progress_seq), _ptr(x_direct), x_direct.shape[0],
+                                     int(x_first), _ptr(ws), nbytes, _stream()), "qmoe_expert_ffn_xs")
+        return
     if progress is None:
         check(lib.qmoe_expert_ffn(variant, _code(xp), _ptr(xp), _ptr(offsets), _ptr(perm), E, d, F, _ptr(w1),
                                   _ptr(w2), e_begin, e_end, xp.shape[0], _ptr(act_ws), _ptr(y), _ptr(preempt_flag),
@@ -521,6 +537,12 @@ def expert_ffn_peer_ex(xp: torch.Tensor, offsets: torch.Tensor, ret: torch.Tenso
 
 PATH_SWAP_AB, PATH_FUSED_1CTA, PATH_FUSED_PAIR = _lib.QMOE_PATH_SWAP_AB, _lib.QMOE_PATH_FUSED_1CTA, _lib.QMOE_PATH_FUSED_PAIR
 PATH_SWAP_PAIR = _lib.QMOE_PATH_SWAP_PAIR
+
+
+def shared_direct_ok(d: int, F: int, E: int, rows: int) -> bool:
+    """Whether the shared sub-experts may read their rows straight from X (qmoe_expert_ffn_xs): the
+    single-launch 1-CTA path only; QMOE_SHARED_DIRECT=0 turns it off (A/B, tests)."""
+    return _SHARED_DIRECT and expert_ffn_path(d, F, E, rows) == PATH_FUSED_1CTA
 
 
 def expert_ffn_path(d: int, F: int, E: int, rows: int) -> int:

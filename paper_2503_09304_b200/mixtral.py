@@ -58,6 +58,16 @@ class _Layer:
     pass
 
 
+class _DirectRows:
+    """Gathered routed rows plus the layer input x, whose rows the shared sub-experts read directly
+    (kernels.expert_ffn(x_direct=...)); opaque to the engine, which only hands it back."""
+
+    __slots__ = ("xp", "x")
+
+    def __init__(self, xp, x):
+        self.xp, self.x = xp, x
+
+
 class DecoderMoEModel:
     """Device plugin (engine.py interface) for a Mixtral/Qwen-shaped decoder."""
 
@@ -129,6 +139,7 @@ class DecoderMoEModel:
         self._stop = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._pass = None  # (members, handles, ns, decode, expected cached entries, metadata) of the pass
         self.pass_serial = 0  # bumped by the engine at every execute (new_expert_state buffers)
+        self._direct_shared = True  # shared sub-experts read x directly where the path allows it
         self._pass_bufs = None
         self.preempt_guard = None  # set by the engine per iteration (device-preempt mode)
         self._pinned_tok = None
@@ -241,18 +252,32 @@ class DecoderMoEModel:
         return y, b[2]
 
     def permute(self, ids, cursor, x):
-        return K.permute(ids, self.config.num_experts, cursor=cursor, x=x)
+        """Queues (+ gathered rows).  Qwen on the 1-CTA path: the shared sub-experts' rows are not
+        gathered; the returned rows object then carries x as well (_DirectRows), which the engine
+        passes back to run_experts unchanged (also across a queue-reusing resume)."""
+        E = self.config.num_experts
+        # only with this pass's fresh (all-zero) cursor: every token is then pending for every shared
+        # sub-expert (a merged resume group may mix cursors, and its queues are subsets of x's rows)
+        fresh = self._pass_bufs is not None and cursor is self._pass_bufs[2]
+        if self.n_shared and fresh and self._direct_shared and K.shared_direct_ok(self.cfg.hidden_dim,
+                                                                                  self.cfg.ffn_dim, E, ids.numel()):
+            perm, offsets, xp = K.permute(ids, E, cursor=cursor, x=x, gather_e_end=self.cfg.num_experts)
+            return perm, offsets, _DirectRows(xp, x)
+        return K.permute(ids, E, cursor=cursor, x=x)
 
     def run_experts(self, layer: int, xp, offsets, perm, y, e_begin: int, e_end: int, preempt_flag=None,
                     progress=None, progress_seq: int = 0, cursor_out=None):
         L = self.layers[layer]
+        x_direct = None
+        if isinstance(xp, _DirectRows):
+            xp, x_direct = xp.xp, xp.x
         rows = xp.shape[0]
         F = self.cfg.ffn_dim
         act = K.workspace(rows * F * 2, "act", self.device).view(self.dtype)[: rows * F].view(rows, F)
         stop = self._stop if cursor_out is None else cursor_out
         K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, L.gate_up, L.down, y, e_begin=e_begin, e_end=e_end,
                      act_ws=act, preempt_flag=preempt_flag, cursor_out=stop, progress=progress,
-                     progress_seq=progress_seq)
+                     progress_seq=progress_seq, x_direct=x_direct, x_first=self.cfg.num_experts)
         return stop
 
     def advance_cursor(self, cursor, stop_dev):

@@ -142,11 +142,14 @@ class SparseMoeBlock(nn.Module):
         T, k, S, d, F = x.shape[0], self.top_k, self.n_shared, self.hidden_dim, self.ffn_dim
         ids, w = K.router(x, self._w_router, k, self.route_mode, n_shared=S)
         slots, EE = k + S, self.num_experts + S
-        perm, offsets, xp = K.permute(ids, EE, x=x)
+        # the shared sub-experts' queues are x's rows in token order: on the 1-CTA path their A
+        # rows come straight from x and the permute gathers only the routed rows
+        direct = S > 0 and K.shared_direct_ok(d, F, EE, T * slots)
+        perm, offsets, xp = K.permute(ids, EE, x=x, gather_e_end=self.num_experts if direct else None)
         y = torch.empty((T * slots, d), dtype=x.dtype, device=x.device)
         act = K.workspace(T * slots * F * x.element_size(), "act", x.device).view(x.dtype)[: T * slots * F]
         K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, self._gate_up, self._down, y,
-                     act_ws=act.view(T * slots, F))
+                     act_ws=act.view(T * slots, F), x_direct=x if direct else None, x_first=self.num_experts)
         res = None if residual is None else residual.reshape(-1, d).contiguous()
         self.last_routing = (ids[:, :k], w[:, :k])
         return K.combine(y, w, res).reshape(shape)

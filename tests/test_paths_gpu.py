@@ -207,3 +207,43 @@ def test_swap_pair_wide_last_tile_is_bit_identical(cuda):
     wide = _run({**env, "QMOE_SP_MERGE": "128"}, shapes)
     narrow = _run({**env, "QMOE_SP_MERGE": "0"}, shapes)
     assert [r["sha"] for r in wide] == [r["sha"] for r in narrow]
+
+
+def test_shared_sub_experts_read_x_directly_bit_identical(cuda):
+    """Qwen-shaped block on the 1-CTA path: the shared sub-experts read their token rows straight
+    from x (qmoe_permute_ex gathers only the routed rows, qmoe_expert_ffn_xs) -- the layer output
+    is bit-identical to the fully gathered path, with and without a preemption stop and resume."""
+    from paper_2503_09304_b200.moe_block import SparseMoeBlock
+
+    d, F, E, k, Fs = 1024, 512, 30, 4, 2048
+    blk = SparseMoeBlock(d, F, E, k, route_mode=K.ROUTE_SOFTMAX_TOPK, shared_expert_intermediate_size=Fs,
+                         device=torch.device("cuda")).init_random(4)
+    S = Fs // F
+    for T in (2000, 4100):
+        x = torch.randn((T, d), device="cuda").bfloat16()
+        assert K.expert_ffn_path(d, F, E + S, T * (k + S)) == K.PATH_FUSED_1CTA
+        K._SHARED_DIRECT = True
+        direct = blk(x)
+        K._SHARED_DIRECT = False
+        try:
+            gathered = blk(x)
+        finally:
+            K._SHARED_DIRECT = True
+        assert torch.equal(direct, gathered), T
+        # preempt inside the shared sub-experts, resume from the cursor: same bits
+        ids, w = K.router(x, blk._w_router, k, K.ROUTE_SOFTMAX_TOPK, n_shared=S)
+        perm, offsets, xp = K.permute(ids, E + S, x=x, gather_e_end=E)
+        y_full = torch.zeros((T * (k + S), d), dtype=torch.bfloat16, device="cuda")
+        K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, blk._gate_up, blk._down, y_full, x_direct=x, x_first=E)
+        y = torch.zeros_like(y_full)
+        flag = torch.full((1,), E + 2, dtype=torch.int32, device="cuda")
+        cur = torch.zeros(1, dtype=torch.int32, device="cuda")
+        K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, blk._gate_up, blk._down, y, preempt_flag=flag, cursor_out=cur,
+                     x_direct=x, x_first=E)
+        stop = int(cur)
+        assert E + 2 <= stop <= E + S
+        flag.zero_()
+        K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, blk._gate_up, blk._down, y, e_begin=stop, x_direct=x,
+                     x_first=E)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_full)
