@@ -312,10 +312,14 @@ def run_qwen_layer(dev, flush, world: int) -> dict:
         y = torch.empty((T * (k + S), d), dtype=torch.bfloat16, device=dev)
         act = torch.empty((T * (k + S), F), dtype=torch.bfloat16, device=dev)
 
+        # as SparseMoeBlock: on the 1-CTA path the shared sub-experts read x directly (no gather)
+        direct = K.shared_direct_ok(d, F, E + S, T * (k + S))
+
         def layer():
             ids, w = K.router(x, wr, k, K.ROUTE_SOFTMAX_TOPK, n_shared=S)
-            perm, offsets, xp = K.permute(ids, E + S, x=x)
-            K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act)
+            perm, offsets, xp = K.permute(ids, E + S, x=x, gather_e_end=E if direct else None)
+            K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act, x_direct=x if direct else None,
+                         x_first=E)
             return K.combine(y, w, x), offsets
 
         for _ in range(3):

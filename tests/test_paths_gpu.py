@@ -213,6 +213,9 @@ def test_shared_sub_experts_read_x_directly_bit_identical(cuda):
     """Qwen-shaped block on the 1-CTA path: the shared sub-experts read their token rows straight
     from x (qmoe_permute_ex gathers only the routed rows, qmoe_expert_ffn_xs) -- the layer output
     is bit-identical to the fully gathered path, with and without a preemption stop and resume."""
+    import torch
+
+    from paper_2503_09304_b200 import kernels as K
     from paper_2503_09304_b200.moe_block import SparseMoeBlock
 
     d, F, E, k, Fs = 1024, 512, 30, 4, 2048

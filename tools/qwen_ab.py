@@ -17,16 +17,20 @@ for T in [int(t) for t in (sys.argv[1] if len(sys.argv) > 1 else "1024,2048,4096
     x = torch.randn((T, d), device="cuda", generator=g).bfloat16()
     y = torch.empty((T * (k + S), d), dtype=torch.bfloat16, device="cuda")
     act = torch.empty((T * (k + S), F), dtype=torch.bfloat16, device="cuda")
+    # the product's choice (moe_block.SparseMoeBlock): shared sub-experts read x directly on the
+    # 1-CTA path unless QMOE_SHARED_DIRECT=0
+    direct = K.shared_direct_ok(d, F, E + S, T * (k + S))
+    ge, xd = (E, x) if direct else (None, None)
     ids, w = K.router(x, wr, k, K.ROUTE_SOFTMAX_TOPK, n_shared=S)
-    perm, offsets, xp = K.permute(ids, E + S, x=x)
+    perm, offsets, xp = K.permute(ids, E + S, x=x, gather_e_end=ge)
 
     def ffn():
-        K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act)
+        K.expert_ffn(K.EXPERT_SWIGLU, xp, offsets, perm, gu, dn, y, act_ws=act, x_direct=xd, x_first=E)
 
     def layer():
         i, w_ = K.router(x, wr, k, K.ROUTE_SOFTMAX_TOPK, n_shared=S)
-        p, o, xp_ = K.permute(i, E + S, x=x)
-        K.expert_ffn(K.EXPERT_SWIGLU, xp_, o, p, gu, dn, y, act_ws=act)
+        p, o, xp_ = K.permute(i, E + S, x=x, gather_e_end=ge)
+        K.expert_ffn(K.EXPERT_SWIGLU, xp_, o, p, gu, dn, y, act_ws=act, x_direct=xd, x_first=E)
         K.combine(y, w_, x)
 
     res = {}
