@@ -9,6 +9,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace qmoe {
 namespace {
@@ -719,6 +720,137 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
   return 0;
 }
 
+// ---- bf16 decode (<= 64 tokens): one cluster of 8 CTAs for the whole batch ---------------------
+// The per-token SIMT kernel re-reads all of W_router (Qwen: 61 x 2048 bf16 = 250 KB) in every
+// token's CTA and walks d in dependent rounds (14 us for 32 Qwen tokens).  Here CTA r of an
+// 8-CTA cluster owns expert chunk r / DS (8 logit rows) over d slice r % DS (NCH x DS = 8), for
+// all tokens: its 8 warps split the slice in k, every warp runs mma.sync m16n8k16 on up to 4
+// token tiles with X and W fragments loaded straight into registers (the streamed kernel's k
+// permutation), the 8 warp partials are summed in warp order in shared memory, and after a
+// cluster barrier CTA r selects the tokens t = r (mod 8): it sums the DS slice partials of every
+// chunk in slice order through distributed shared memory and runs select_token.  One launch,
+// W_router read once per batch, deterministic.
+__device__ __forceinline__ float ld_cluster_f32(const float* p, uint32_t rank) {
+  float v;
+  asm volatile(
+      "{\n\t"
+      ".reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %1, %2;\n\t"
+      "ld.shared::cluster.f32 %0, [ra];\n\t"
+      "}"
+      : "=f"(v)
+      : "r"(ptx::smem_u32(p)), "r"(rank)
+      : "memory");
+  return v;
+}
+
+template <int NCH, int DS, int MT>
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256)
+router_decode_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr, int ntok, int d,
+                     int E, int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
+                     float* __restrict__ logits_out) {
+  static_assert(NCH * DS == 8, "8 CTAs per cluster");
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float s_part[8][16 * MT][8];   // per warp partials
+  __shared__ float s_log[16 * MT][8];       // this CTA's (chunk, slice) logits
+  __shared__ float s_full[8][kMaxE];        // per warp: one token's logits (selection)
+  __shared__ float s_score[8][kMaxE];
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int chunk = (int)rank / DS, slice = (int)rank % DS;
+  const int dq = d / DS, dw = dq / 8;          // this CTA's slice, each warp's share
+  const int k0 = slice * dq + warp * dw;
+  const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)min(8 * chunk + g, E - 1) * d + k0) + t4;
+  const uint4* xr[MT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    xr[mt][0] = reinterpret_cast<const uint4*>(x + (size_t)min(16 * mt + g, ntok - 1) * d + k0) + t4;
+    xr[mt][1] = reinterpret_cast<const uint4*>(x + (size_t)min(16 * mt + g + 8, ntok - 1) * d + k0) + t4;
+  }
+  float acc[MT][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+  for (int st = 0; st < dw / 32; ++st) {
+    const uint4 b = __ldg(wp + 4 * st);
+    uint4 a0[MT], a1[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      a0[mt] = __ldg(xr[mt][0] + 4 * st);
+      a1[mt] = __ldg(xr[mt][1] + 4 * st);
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      mma_bf16_16816(acc[mt], a0[mt].x, a1[mt].x, a0[mt].y, a1[mt].y, b.x, b.y);
+      mma_bf16_16816(acc[mt], a0[mt].z, a1[mt].z, a0[mt].w, a1[mt].w, b.z, b.w);
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int r0 = 16 * mt + g, c = 2 * t4;
+    s_part[warp][r0][c] = acc[mt][0];
+    s_part[warp][r0][c + 1] = acc[mt][1];
+    s_part[warp][r0 + 8][c] = acc[mt][2];
+    s_part[warp][r0 + 8][c + 1] = acc[mt][3];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 16 * MT * 8; i += 256) {
+    const int t = i >> 3, e = i & 7;
+    float v = s_part[0][t][e];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v += s_part[w][t][e];
+    s_log[t][e] = v;
+  }
+  ptx::cluster_sync();  // every CTA's s_log is complete and visible cluster-wide
+  // CTA r selects tokens r, r + 8, ...: warp j of it takes token r + 8 j
+  const int tok = (int)rank + 8 * warp;
+  if (tok < ntok) {
+    for (int i = lane; i < NCH * 8; i += 32) {
+      const int cc = i >> 3, e = i & 7;
+      float v = 0.f;
+#pragma unroll
+      for (int ss = 0; ss < DS; ++ss) v += ld_cluster_f32(&s_log[tok][e], (uint32_t)(cc * DS + ss));
+      s_full[warp][i] = v;
+    }
+    __syncwarp();
+    select_token<float>(s_full[warp], s_score[warp], tok, E, k, mode, lane, ids_out, w_out, logits_out);
+  }
+  ptx::cluster_sync();  // no CTA leaves while a peer may still read its s_log
+}
+
+template <int NCH, int DS>
+int launch_router_decode(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
+                         void* logits, cudaStream_t s) {
+  if (T_ <= 16)
+    return launch_pdl("qmoe_router(decode cluster)", router_decode_kernel<NCH, DS, 1>, dim3(8), dim3(256), 0, s,
+                      (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,
+                      (float*)logits);
+  if (T_ <= 32)
+    return launch_pdl("qmoe_router(decode cluster)", router_decode_kernel<NCH, DS, 2>, dim3(8), dim3(256), 0, s,
+                      (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,
+                      (float*)logits);
+  return launch_pdl("qmoe_router(decode cluster)", router_decode_kernel<NCH, DS, 4>, dim3(8), dim3(256), 0, s,
+                    (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,
+                    (float*)logits);
+}
+
+// 0 = not applicable; QMOE_ROUTER_DECODE=0 keeps the per-token SIMT kernel.
+int try_router_decode(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
+                      void* logits, cudaStream_t s, int* st) {
+  static const int env = [] {
+    const char* v = getenv("QMOE_ROUTER_DECODE");
+    return v == nullptr ? 1 : atoi(v);
+  }();
+  if (!env || T_ > 64 || T_ < 1 || reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(wr) % 16)
+    return 0;
+  if (E <= 8 && d % (8 * 8 * 32) == 0) { *st = launch_router_decode<1, 8>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
+  if (E <= 16 && d % (4 * 8 * 32) == 0) { *st = launch_router_decode<2, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
+  if (E <= 32 && d % (2 * 8 * 32) == 0) { *st = launch_router_decode<4, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
+  if (E <= 64 && d % (8 * 32) == 0) { *st = launch_router_decode<8, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
+  return 0;
+}
+
 // Few tokens (decode): one token per CTA, all 8 warps on it.  Many tokens: warps own tokens (2
 // each) when the experts fit one or two 8-expert chunks, else 4 tokens share the 8 warps.
 template <typename T>
@@ -732,6 +864,10 @@ int dispatch_router(const void* x, const void* wr, int T_, int d, int E, int k, 
       if (try_router_stream(x, wr, T_, d, E, k, mode, ids, w, logits, s, &st)) return st;
       return launch_router_mma(x, wr, T_, d, E, k, mode, ids, w, logits, s);
     }
+  }
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    int st = QMOE_OK;
+    if (try_router_decode(x, wr, T_, d, E, k, mode, ids, w, logits, s, &st)) return st;
   }
   // decode: 16 warps on one token halve the dependent load rounds over d (Qwen: 8 chunks x 2 slices)
   if (T_ < 148 * 8) return launch_router<T, 1, 1, 16>(x, wr, T_, d, E, k, mode, ids, w, logits, s);

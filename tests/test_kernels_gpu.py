@@ -70,10 +70,12 @@ def test_router_k_equals_e(cuda):
                                           (700, 2048, 60, 4, 0), (4100, 2048, 60, 4, 1), (2000, 1024, 16, 2, 0),
                                           (33, 2048, 60, 4, 1), (300, 512, 5, 2, 0),
                                           (512, 1024, 24, 3, 0), (8192, 4096, 8, 2, 0), (8192, 2048, 60, 4, 1),
-                                          (2500, 1024, 16, 2, 0), (2049, 2048, 24, 3, 0), (6150, 4096, 7, 2, 0)])
+                                          (2500, 1024, 16, 2, 0), (2049, 2048, 24, 3, 0), (6150, 4096, 7, 2, 0),
+                                          (64, 2048, 60, 4, 1), (17, 4096, 8, 2, 0), (48, 1024, 16, 2, 0),
+                                          (5, 512, 24, 3, 0)])
 def test_router_bf16_against_oracle_on_same_inputs(cuda, T, d, E, k, qwen):
-    """T >= 256 bf16 runs the tensor-core kernels (register-streamed or cp.async-staged mma.sync),
-    smaller T the SIMT one."""
+    """T <= 64 bf16 runs the decode cluster kernel (router_decode_kernel), T >= 256 the tensor-core
+    kernels (register-streamed, W-in-registers or cp.async-staged mma.sync), the rest the SIMT one."""
     g = torch.Generator().manual_seed(T)
     x = torch.randn((T, d), generator=g).bfloat16()
     wr = (torch.randn((E, d), generator=g) / d ** 0.5).bfloat16()

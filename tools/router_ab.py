@@ -2,7 +2,7 @@
 Mixtral (d=4096, E=8, k=2) and the Qwen layer (d=2048, 60 routed + shared gate, k=4+4) at several
 token counts; saves ids/weights to compare kernels across QMOE_ROUTER_STREAM settings.
     python tools/router_ab.py out.pt"""
-import json, statistics, sys
+import json, os, statistics, sys
 sys.path.insert(0, ".")
 import torch
 from paper_2503_09304_b200 import kernels as K
@@ -13,7 +13,7 @@ for name, d, E, k, S, mode in (("mixtral", 4096, 8, 2, 0, K.ROUTE_TOPK_SOFTMAX),
                                ("qwen", 2048, 60, 4, 4, K.ROUTE_SOFTMAX_TOPK)):
     g = torch.Generator(device="cuda").manual_seed(1)
     wr = (torch.randn((E + (1 if S else 0), d), device="cuda", generator=g) * d ** -0.5).bfloat16()
-    for T in (256, 1024, 2048, 4096, 8192, 16384):
+    for T in [int(t) for t in os.environ.get("ROUTER_AB_T", "256,1024,2048,4096,8192,16384").split(",")]:
         x = torch.randn((T, d), device="cuda", generator=g).bfloat16()
         for _ in range(3):
             ids, w = K.router(x, wr, k, mode, n_shared=S)
