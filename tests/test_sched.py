@@ -72,6 +72,24 @@ def test_policy_rules():
     assert never_preempt_policy(report([BE]), s.snapshot()) is CONT
 
 
+def test_arrival_policy_holds_while_admission_is_blocked():
+    """Serving variant: a fresh LS prefill preempts -- unless the KV ledger just refused a prefill
+    (the driver fell back to decode-only work): preempting then only drops the decode batch at its
+    first report and selects it again (a preemption livelock under KV saturation)."""
+    from paper_2503_09304_b200.sched import arrival_policy
+
+    s = sched(policy=arrival_policy)
+    arrive(s, 2, LS)
+    assert arrival_policy(report([BE]), s.snapshot()) is PREEMPT
+    snap = s.snapshot()
+    s.admission_blocked = True
+    assert s.snapshot() is not snap and s.snapshot().admission_blocked
+    assert arrival_policy(report([BE]), s.snapshot()) is CONT
+    s.admission_blocked = False
+    assert arrival_policy(report([BE]), s.snapshot()) is PREEMPT
+    assert qllm_policy(report([BE]), s.snapshot()) is PREEMPT  # the reference policy is unchanged
+
+
 def test_snapshot_is_rebuilt_after_mutation():
     s = sched()
     snap = s.snapshot()
