@@ -720,7 +720,7 @@ int try_router_stream(const void* x, const void* wr, int T_, int d, int E, int k
   return 0;
 }
 
-// ---- bf16 decode (<= 64 tokens): one cluster of 8 CTAs for the whole batch ---------------------
+// ---- bf16 decode (<= 32 tokens): one cluster of 8 CTAs for the whole batch ---------------------
 // The per-token SIMT kernel re-reads all of W_router (Qwen: 61 x 2048 bf16 = 250 KB) in every
 // token's CTA and walks d in dependent rounds (14 us for 32 Qwen tokens).  Here CTA r of an
 // 8-CTA cluster owns expert chunk r / DS (8 logit rows) over d slice r % DS (NCH x DS = 8), for
@@ -744,7 +744,7 @@ __device__ __forceinline__ float ld_cluster_f32(const float* p, uint32_t rank) {
   return v;
 }
 
-template <int NCH, int DS, int MT>
+template <int NCH, int DS, int MT, int U>
 __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256)
 router_decode_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr, int ntok, int d,
                      int E, int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
@@ -772,19 +772,27 @@ router_decode_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* _
   float acc[MT][4];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
-  for (int st = 0; st < dw / 32; ++st) {
-    const uint4 b = __ldg(wp + 4 * st);
-    uint4 a0[MT], a1[MT];
+  // U k32 steps of loads in flight before their MMAs (a handful of steps per warp: latency-bound;
+  // volatile loads keep the compiler from interleaving them with the MMAs); dw / 32 % U == 0
+  for (int st0 = 0; st0 < dw / 32; st0 += U) {
+    uint4 b[U], a0[U][MT], a1[U][MT];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      a0[mt] = __ldg(xr[mt][0] + 4 * st);
-      a1[mt] = __ldg(xr[mt][1] + 4 * st);
+    for (int u = 0; u < U; ++u) {
+      const int st = st0 + u;
+      b[u] = ld_stream<false>(wp + 4 * st);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        a0[u][mt] = ld_stream<false>(xr[mt][0] + 4 * st);
+        a1[u][mt] = ld_stream<false>(xr[mt][1] + 4 * st);
+      }
     }
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      mma_bf16_16816(acc[mt], a0[mt].x, a1[mt].x, a0[mt].y, a1[mt].y, b.x, b.y);
-      mma_bf16_16816(acc[mt], a0[mt].z, a1[mt].z, a0[mt].w, a1[mt].w, b.z, b.w);
-    }
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        mma_bf16_16816(acc[mt], a0[u][mt].x, a1[u][mt].x, a0[u][mt].y, a1[u][mt].y, b[u].x, b[u].y);
+        mma_bf16_16816(acc[mt], a0[u][mt].z, a1[u][mt].z, a0[u][mt].w, a1[u][mt].w, b[u].z, b[u].w);
+      }
   }
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
@@ -819,18 +827,14 @@ router_decode_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* _
   ptx::cluster_sync();  // no CTA leaves while a peer may still read its s_log
 }
 
-template <int NCH, int DS>
+template <int NCH, int DS, int U>
 int launch_router_decode(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
                          void* logits, cudaStream_t s) {
   if (T_ <= 16)
-    return launch_pdl("qmoe_router(decode cluster)", router_decode_kernel<NCH, DS, 1>, dim3(8), dim3(256), 0, s,
+    return launch_pdl("qmoe_router(decode cluster)", router_decode_kernel<NCH, DS, 1, U>, dim3(8), dim3(256), 0, s,
                       (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,
                       (float*)logits);
-  if (T_ <= 32)
-    return launch_pdl("qmoe_router(decode cluster)", router_decode_kernel<NCH, DS, 2>, dim3(8), dim3(256), 0, s,
-                      (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,
-                      (float*)logits);
-  return launch_pdl("qmoe_router(decode cluster)", router_decode_kernel<NCH, DS, 4>, dim3(8), dim3(256), 0, s,
+  return launch_pdl("qmoe_router(decode cluster)", router_decode_kernel<NCH, DS, 2, U>, dim3(8), dim3(256), 0, s,
                     (const __nv_bfloat16*)x, (const __nv_bfloat16*)wr, T_, d, E, k, mode, ids, (float*)w,
                     (float*)logits);
 }
@@ -842,12 +846,13 @@ int try_router_decode(const void* x, const void* wr, int T_, int d, int E, int k
     const char* v = getenv("QMOE_ROUTER_DECODE");
     return v == nullptr ? 1 : atoi(v);
   }();
-  if (!env || T_ > 64 || T_ < 1 || reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(wr) % 16)
+  // up to 32 tokens (64: the 8 CTAs' X reads outweigh the per-token kernel's, measured 23 vs 17 us Qwen)
+  if (!env || T_ > 32 || T_ < 1 || reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(wr) % 16)
     return 0;
-  if (E <= 8 && d % (8 * 8 * 32) == 0) { *st = launch_router_decode<1, 8>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
-  if (E <= 16 && d % (4 * 8 * 32) == 0) { *st = launch_router_decode<2, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
-  if (E <= 32 && d % (2 * 8 * 32) == 0) { *st = launch_router_decode<4, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
-  if (E <= 64 && d % (8 * 32) == 0) { *st = launch_router_decode<8, 1>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
+  if (E <= 8 && d % (8 * 8 * 32 * 2) == 0) { *st = launch_router_decode<1, 8, 2>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
+  if (E <= 16 && d % (4 * 8 * 32 * 4) == 0) { *st = launch_router_decode<2, 4, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
+  if (E <= 32 && d % (2 * 8 * 32 * 4) == 0) { *st = launch_router_decode<4, 2, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
+  if (E <= 64 && d % (8 * 32 * 4) == 0) { *st = launch_router_decode<8, 1, 4>(x, wr, T_, d, E, k, mode, ids, w, logits, s); return 1; }
   return 0;
 }
 
