@@ -12,9 +12,12 @@
 #include "tc_ptx.cuh"
 
 namespace qmoe {
+int tc_init_driver();  // expert_tc.cu: cuTensorMapEncodeTiled entry point (sm_100 check)
+int tc_make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 namespace {
 
 constexpr int kExpChunk = 8;   // experts accumulated per pass over d
+constexpr int kNoSelect = 1 << 16;  // router_tc_kernel mode bit: skip the selection (timing runs)
 constexpr int kMaxE = 64;
 
 template <typename T> struct Vec;
@@ -133,6 +136,169 @@ __device__ __noinline__ void select_token(const A* lg, A* s_score, int tok, int 
       ids_out[(size_t)tok * ko + k + s] = Er + s;
       w_out[(size_t)tok * ko + k + s] = g;
     }
+  }
+}
+
+// select_token for a group of G consecutive lanes (G | 32) instead of a warp, bit for bit: lane j of
+// the group holds the logits of select_token's "lanes" L = j + G i (i < 32 / G), i.e. logit rows L
+// and L + 32.  The maxima and the top-k winner are order-free (exact max; value desc, id asc); the
+// softmax denominator replays warp_sum's butterfly (bit 4 of L first): the bits of L above log2 G
+// are the bits of i, combined locally, then xor shuffles G/2 .. 1.  So one token costs
+// log2 G shuffle levels instead of 5, and 256 / G tokens are selected at once by a CTA.
+template <int G>
+__device__ __forceinline__ void select_group(const float (&l0)[32 / G], const float (&l1)[32 / G], bool live, int tok,
+                                             int E, int k, int mode, int j, int32_t* __restrict__ ids_out,
+                                             float* __restrict__ w_out, float* __restrict__ logits_out) {
+  constexpr int C = 32 / G;
+  const int ns = mode >> 8;
+  mode &= 0xFF;
+  const int Er = ns > 0 ? E - 1 : E;
+  const int ko = k + ns;
+  if (live && logits_out != nullptr) {
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const int L = j + G * i;
+      if (L < E) logits_out[(size_t)tok * E + L] = l0[i];
+      if (L + 32 < E) logits_out[(size_t)tok * E + L + 32] = l1[i];
+    }
+  }
+  float s0[C], s1[C];
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    const int L = j + G * i;
+    s0[i] = L < Er ? l0[i] : 0.f;
+    s1[i] = L + 32 < Er ? l1[i] : 0.f;
+  }
+  if (mode == QMOE_ROUTE_SOFTMAX_TOPK) {
+    float m = 0.f;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {  // select_token's per-lane start value, then the max
+      const int L = j + G * i;
+      float v = L < Er ? s0[i] : s1[i];
+      if (L + 32 < Er && s1[i] > v) v = s1[i];
+      m = (i == 0 || v > m) ? v : m;
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const float v = __shfl_xor_sync(0xffffffffu, m, o);
+      m = v > m ? v : m;
+    }
+    float z0[C], z1[C], t[C];
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const int L = j + G * i;
+      z0[i] = L < Er ? exp_acc(s0[i] - m) : 0.f;
+      z1[i] = L + 32 < Er ? exp_acc(s1[i] - m) : 0.f;
+      t[i] = z0[i] + z1[i];
+    }
+#pragma unroll
+    for (int h = C / 2; h > 0; h >>= 1)
+#pragma unroll
+      for (int i = 0; i < h; ++i) t[i] = t[i] + t[i + h];
+    float tot = t[0];
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      s0[i] = z0[i] / tot;
+      s1[i] = z1[i] / tot;
+    }
+  }
+  // top-k by (score desc, id asc)
+  uint32_t taken0 = 0, taken1 = 0;  // bit i: leaf i's row L (resp. L + 32) taken or not an expert
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    const int L = j + G * i;
+    if (!(L < Er)) taken0 |= 1u << i;
+    if (!(L + 32 < Er)) taken1 |= 1u << i;
+  }
+  int pick[8];
+  float pv[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    pick[q] = 0x7fffffff;
+    pv[q] = 0.f;
+    if (q < k) {
+      int bid = -1;
+      float bv = 0.f;
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const int L = j + G * i;
+        if (!(taken0 >> i & 1) && (bid < 0 || s0[i] > bv || (s0[i] == bv && L < bid))) { bid = L; bv = s0[i]; }
+        if (!(taken1 >> i & 1) && (bid < 0 || s1[i] > bv || (s1[i] == bv && L + 32 < bid))) { bid = L + 32; bv = s1[i]; }
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
+        if (oid >= 0 && (bid < 0 || ov > bv || (ov == bv && oid < bid))) { bv = ov; bid = oid; }
+      }
+      pick[q] = bid;
+      pv[q] = bv;
+      if (bid >= 0 && (bid & 31) % G == j) {
+        if (bid < 32) taken0 |= 1u << ((bid & 31) / G);
+        else taken1 |= 1u << ((bid & 31) / G);
+      }
+    }
+  }
+  // ids ascending (model.py:75 / :129): an 8-element sorting network on (id, value)
+#define QMOE_CX(a, b)                                                         \
+  if (pick[b] < pick[a]) {                                                    \
+    const int ti = pick[a]; pick[a] = pick[b]; pick[b] = ti;                  \
+    const float tv = pv[a]; pv[a] = pv[b]; pv[b] = tv;                        \
+  }
+  QMOE_CX(0, 1) QMOE_CX(2, 3) QMOE_CX(4, 5) QMOE_CX(6, 7)
+  QMOE_CX(0, 2) QMOE_CX(1, 3) QMOE_CX(4, 6) QMOE_CX(5, 7)
+  QMOE_CX(1, 2) QMOE_CX(5, 6) QMOE_CX(0, 4) QMOE_CX(3, 7)
+  QMOE_CX(1, 5) QMOE_CX(2, 6)
+  QMOE_CX(1, 4) QMOE_CX(3, 6)
+  QMOE_CX(2, 4) QMOE_CX(3, 5)
+  QMOE_CX(3, 4)
+#undef QMOE_CX
+  float gl = 0.f;  // the shared expert's gate logit (row Er), from the lane that holds it
+  if (ns > 0) {
+    const int gi = (Er & 31) / G, gj = (Er & 31) % G;
+#pragma unroll
+    for (int i = 0; i < C; ++i)
+      if (i == gi) gl = Er >= 32 ? l1[i] : l0[i];
+    gl = __shfl_sync(0xffffffffu, gl, (threadIdx.x & 31 & ~(G - 1)) + gj);
+  }
+  if (!live || j != 0) return;
+  float wv[8];
+  if (mode == QMOE_ROUTE_SOFTMAX_TOPK) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) wv[q] = pv[q];
+  } else {
+    // softmax over the picked logits, summed in ascending id order (model.py:78-80)
+    float m = pv[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (q < k) m = pv[q] > m ? pv[q] : m;
+    float tot = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < k) {
+        wv[q] = exp_acc(pv[q] - m);
+        tot += wv[q];
+      }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < k) wv[q] = wv[q] / tot;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (q < k) {
+      ids_out[(size_t)tok * ko + q] = pick[q];
+      w_out[(size_t)tok * ko + q] = wv[q];
+    }
+  if (ns > 0) {
+    const float g = 1.f / (1.f + exp_acc(-gl));
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < ns) {
+        ids_out[(size_t)tok * ko + k + q] = Er + q;
+        w_out[(size_t)tok * ko + k + q] = g;
+      }
   }
 }
 
@@ -856,6 +1022,235 @@ int try_router_decode(const void* x, const void* wr, int T_, int d, int E, int k
   return 0;
 }
 
+// ---- bf16, large batches: tcgen05 logits, d split over a cluster --------------------------------
+// The mma.sync kernels above pay for W_router in every 16/32-token tile (re-read from L2: Qwen's
+// 61 x 2048 logit rows are 250 KB, 4x the X bytes of a 32-token tile) and move every operand
+// through registers.  Here the logits are a skinny GEMM on the 5th-gen tensor core: a tile is
+// 128 tokens x NB logit rows (experts padded to 16), K = d split into S slices, one CTA per
+// (tile, slice), the S CTAs of a tile forming a cluster.  Warp 0 streams X (128 x 64, evict-first)
+// and W_router (NB x 64, evict-last) into a STAGES-deep 128B-swizzled ring with TMA; one thread of
+// warp 1 issues tcgen05.mma (M=128, N=NB, K=16) into an NB-column fp32 TMEM accumulator.  Warps
+// 4-7 read the accumulator (thread = token row) into shared memory; after a cluster barrier CTA r
+// sums the S slice partials of tokens [r 128/S, (r+1) 128/S) in slice order through distributed
+// shared memory (deterministic) and its 8 warps run select_token.  X rows beyond T are zero-filled
+// by TMA and never selected.  W_router is read from L2 once per 128 tokens.
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t"
+      "}"
+      : "=r"(ok)
+      : "r"(ptx::smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+template <int NB, int S, int STAGES, int MINB>
+__global__ void __cluster_dims__(S, 1, 1) __launch_bounds__(256, MINB)
+router_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int ntok, int d,
+                 int E, int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
+                 float* __restrict__ logits_out) {
+  constexpr int kXBytes = 128 * 64 * 2, kWBytes = NB * 64 * 2, kStage = kXBytes + kWBytes;
+  constexpr uint32_t kCols = NB <= 32 ? 32 : (NB <= 64 ? 64 : 128);
+  constexpr int kRows = 128 / S;   // tokens this CTA selects
+  constexpr int kLdP = NB + 4;     // padded partial row (float4 stores conflict-free)
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(128, NB);
+  static_assert(kStage % 1024 == 0, "stages keep the 1024-byte swizzle-atom alignment");
+  static_assert(128 * kLdP * 4 <= STAGES * kStage, "the partial tile aliases the ring");
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], done_bar;
+  __shared__ uint32_t tmem_base_smem;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = S > 1 ? ptx::cluster_ctarank() : 0;
+  const int tile = blockIdx.x / S;
+  const int nkb = d / (64 * S), kb0 = (int)rank * nkb;  // this CTA's 64-wide K blocks
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    ptx::mbar_init(&done_bar, 1);
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&tmX);
+    ptx::tma_prefetch_desc(&tmW);
+  }
+  if (warp == 1) ptx::tmem_alloc<kCols>(&tmem_base_smem);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tmem_base_smem;
+  pdl_wait();  // X is the predecessor's output
+  pdl_trigger();
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sx = smem + stage * kStage;
+        ptx::mbar_arrive_expect_tx(&full_bar[stage], kStage);
+        ptx::tma_load_2d(&tmX, &full_bar[stage], sx, (kb0 + kb) * 64, tile * 128, ptx::kEvictFirst);
+        ptx::tma_load_2d(&tmW, &full_bar[stage], sx + kXBytes, (kb0 + kb) * 64, 0, ptx::kEvictLast);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait(&full_bar[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t a = ptx::smem_u32(smem + stage * kStage), b = a + kXBytes;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          ptx::tc_mma_bf16(tmem, ptx::sw128_kmajor_desc(a + kk * 32), ptx::sw128_kmajor_desc(b + kk * 32), kIdesc,
+                           (kb > 0 || kk > 0) ? 1u : 0u);
+        ptx::tc_commit(&empty_bar[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      ptx::tc_commit(&done_bar);  // accumulator complete
+    }
+    __syncwarp();
+  }
+  float* s_p = reinterpret_cast<float*>(smem);  // [128][kLdP] this CTA's slice partials (ring reused)
+  if (warp >= 4) {
+    // every MMA retired (the ring is free).  One polling lane per warp, backing off: 128 threads
+    // spinning on try_wait compete with the ring's barriers and the TMA completions.
+    if (lane == 0) {
+      while (!mbar_try_wait(&done_bar, 0)) __nanosleep(256);
+    }
+    __syncwarp();
+    ptx::tc_fence_after();
+    const int row = (warp - 4) * 32 + lane;
+    const uint32_t t_row = tmem + ((uint32_t)((warp - 4) * 32) << 16);
+#pragma unroll
+    for (int c0 = 0; c0 < NB; c0 += 32) {
+      uint32_t v[32];
+      ptx::tmem_ld32(t_row + c0, v);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 32 && c0 + c < NB; c += 4)
+        *reinterpret_cast<float4*>(s_p + row * kLdP + c0 + c) =
+            make_float4(__uint_as_float(v[c]), __uint_as_float(v[c + 1]), __uint_as_float(v[c + 2]),
+                        __uint_as_float(v[c + 3]));
+    }
+  }
+  ptx::tc_fence_before();
+  if constexpr (S > 1) ptx::cluster_sync(); else __syncthreads();
+  // token r of this CTA's kRows is selected by the G = 256 / kRows consecutive threads r G .. r G +
+  // G - 1; thread j of the group sums the slice partials (slice order) of logit rows L, L + 32 for
+  // L = j + G i straight into registers
+  constexpr int G = 256 / kRows, C = 32 / G;
+  const int r = threadIdx.x / G, j = threadIdx.x % G;
+  const int tok = tile * 128 + (int)rank * kRows + r;
+  float l0[C], l1[C];
+  {
+    const float* p = s_p + ((int)rank * kRows + r) * kLdP;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const int L = j + G * i;
+      float a = 0.f, b = 0.f;
+      if (L < E) {
+        a = S > 1 ? ld_cluster_f32(p + L, 0) : p[L];
+#pragma unroll
+        for (int sl = 1; sl < S; ++sl) a += ld_cluster_f32(p + L, (uint32_t)sl);
+      }
+      if (L + 32 < E && L + 32 < NB) {
+        b = S > 1 ? ld_cluster_f32(p + L + 32, 0) : p[L + 32];
+#pragma unroll
+        for (int sl = 1; sl < S; ++sl) b += ld_cluster_f32(p + L + 32, (uint32_t)sl);
+      }
+      l0[i] = a;
+      l1[i] = b;
+    }
+  }
+  if constexpr (S > 1) ptx::cluster_sync(); else __syncthreads();  // peers done reading s_p
+  if (!(mode & kNoSelect))
+    select_group<G>(l0, l1, tok < ntok, tok, E, k, mode, j, ids_out, w_out, logits_out);
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<kCols>(tmem);
+  }
+}
+
+template <int NB, int S, int STAGES, int MINB>
+int launch_router_tc(const CUtensorMap& mx, const CUtensorMap& mw, int T_, int d, int E, int k, int mode,
+                     int32_t* ids, void* w, void* logits, cudaStream_t s) {
+  constexpr int smem = STAGES * (128 * 64 * 2 + NB * 64 * 2) + 1024;
+  static uint64_t attr_set = 0;  // devices already configured
+  if (!(attr_set & current_device_bit())) {
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(router_tc_kernel<NB, S, STAGES, MINB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set |= current_device_bit();
+  }
+  const int ntiles = (T_ + 127) / 128;
+  return launch_pdl("qmoe_router(tcgen05)", router_tc_kernel<NB, S, STAGES, MINB>, dim3(ntiles * S), dim3(256), smem,
+                    s, mx, mw, T_, d, E, k, mode, ids, (float*)w, (float*)logits);
+}
+
+// 0 = not applicable.  QMOE_ROUTER_TC=0 disables it, QMOE_ROUTER_TC_MIN sets the token threshold,
+// QMOE_ROUTER_TC_S forces the d split (1, 2, 4; default: enough CTAs for one wave, see below).
+int try_router_tc(const void* x, const void* wr, int T_, int d, int E, int k, int mode, int32_t* ids, void* w,
+                  void* logits, cudaStream_t s, int* st) {
+  static const int env = [] {
+    const char* v = getenv("QMOE_ROUTER_TC");
+    return v == nullptr ? 1 : atoi(v);
+  }();
+  static const int tmin_env = [] {
+    const char* v = getenv("QMOE_ROUTER_TC_MIN");
+    return v == nullptr ? 0 : atoi(v);
+  }();
+  // measured crossover against the mma.sync kernels (tools/router_ab.py, L2 flushed): Mixtral
+  // 4096 tokens 18.4 vs 18.5 us, Qwen (61 logit rows) 2048 tokens 16.8 vs 17.1, 4096 28.6 vs 18.8
+  const int tmin = tmin_env ? tmin_env : (E > 16 ? 3072 : 4096);
+  static const int s_env = [] {
+    const char* v = getenv("QMOE_ROUTER_TC_S");
+    return v == nullptr ? 0 : atoi(v);
+  }();
+  static const int nosel = [] {  // timing only: logits streamed, no selection (ids/w not written)
+    const char* v = getenv("QMOE_ROUTER_TC_NOSEL");
+    return v != nullptr && atoi(v) != 0;
+  }();
+  static const int deep = [] {  // QMOE_ROUTER_TC_DEEP=1: deeper ring, 1 CTA per SM
+    const char* v = getenv("QMOE_ROUTER_TC_DEEP");
+    return v != nullptr && atoi(v) != 0;
+  }();
+  if (nosel) mode |= kNoSelect;
+  if (!env || T_ < tmin || E > 64 || d % 64 != 0) return 0;
+  if (tc_init_driver() != QMOE_OK) return 0;
+  // d split: the smallest S that puts >= 128 CTAs on the GPU, slices of >= 512 columns (Qwen
+  // 4k / 8k / 16k tokens: S = 4 / 2 / 1 -> 18.8 / 22.5 / 28.7 us; Mixtral 8k / 16k: S = 2 / 1)
+  const int ntiles = (T_ + 127) / 128;
+  int S = 1;
+  while (S < 4 && ntiles * S < 128 && d / (2 * S) >= 512 && d % (128 * S) == 0) S *= 2;
+  if (s_env == 1 || s_env == 2 || s_env == 4) S = s_env;
+  if (d % (64 * S) != 0) return 0;
+  const int NB = E <= 16 ? 16 : (E <= 32 ? 32 : 64);
+  CUtensorMap mx, mw;
+  if (tc_make_map(&mx, x, (uint64_t)T_, (uint64_t)d, 128) != QMOE_OK) return 0;
+  if (tc_make_map(&mw, wr, (uint64_t)E, (uint64_t)d, (uint32_t)NB) != QMOE_OK) return 0;
+#define QMOE_RTC(NB_, S_, ST_, MB_)                                                                   \
+  if (NB == NB_ && S == S_) {                                                                         \
+    *st = launch_router_tc<NB_, S_, ST_, MB_>(mx, mw, T_, d, E, k, mode, ids, w, logits, s);          \
+    return 1;                                                                                         \
+  }
+  if (deep) {
+    QMOE_RTC(16, 1, 12, 1) QMOE_RTC(16, 2, 12, 1) QMOE_RTC(16, 4, 12, 1)
+    QMOE_RTC(64, 1, 8, 1) QMOE_RTC(64, 2, 8, 1) QMOE_RTC(64, 4, 8, 1)
+  }
+  QMOE_RTC(16, 1, 6, 2) QMOE_RTC(16, 2, 6, 2) QMOE_RTC(16, 4, 6, 2)
+  QMOE_RTC(32, 1, 5, 2) QMOE_RTC(32, 2, 5, 2) QMOE_RTC(32, 4, 5, 2)
+  QMOE_RTC(64, 1, 5, 1) QMOE_RTC(64, 2, 4, 2) QMOE_RTC(64, 4, 4, 2)
+#undef QMOE_RTC
+  return 0;
+}
+
 // Few tokens (decode): one token per CTA, all 8 warps on it.  Many tokens: warps own tokens (2
 // each) when the experts fit one or two 8-expert chunks, else 4 tokens share the 8 warps.
 template <typename T>
@@ -866,6 +1261,7 @@ int dispatch_router(const void* x, const void* wr, int T_, int d, int E, int k, 
     if (T_ >= 256 && d % kMmaK == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
         reinterpret_cast<uintptr_t>(wr) % 16 == 0) {
       int st = QMOE_OK;
+      if (try_router_tc(x, wr, T_, d, E, k, mode, ids, w, logits, s, &st)) return st;
       if (try_router_stream(x, wr, T_, d, E, k, mode, ids, w, logits, s, &st)) return st;
       return launch_router_mma(x, wr, T_, d, E, k, mode, ids, w, logits, s);
     }

@@ -72,10 +72,12 @@ def test_router_k_equals_e(cuda):
                                           (512, 1024, 24, 3, 0), (8192, 4096, 8, 2, 0), (8192, 2048, 60, 4, 1),
                                           (2500, 1024, 16, 2, 0), (2049, 2048, 24, 3, 0), (6150, 4096, 7, 2, 0),
                                           (64, 2048, 60, 4, 1), (17, 4096, 8, 2, 0), (48, 1024, 16, 2, 0),
-                                          (5, 512, 24, 3, 0)])
+                                          (5, 512, 24, 3, 0), (4500, 1024, 24, 3, 0), (4097, 3072, 40, 4, 1),
+                                          (16384, 4096, 8, 2, 0)])
 def test_router_bf16_against_oracle_on_same_inputs(cuda, T, d, E, k, qwen):
-    """T <= 64 bf16 runs the decode cluster kernel (router_decode_kernel), T >= 256 the tensor-core
-    kernels (register-streamed, W-in-registers or cp.async-staged mma.sync), the rest the SIMT one."""
+    """T <= 64 bf16 runs the decode cluster kernel (router_decode_kernel), T >= 4096 the tcgen05
+    kernel (router_tc_kernel, d split over a cluster), 256 <= T < 4096 the mma.sync kernels
+    (register-streamed or cp.async-staged), the rest the SIMT one."""
     g = torch.Generator().manual_seed(T)
     x = torch.randn((T, d), generator=g).bfloat16()
     wr = (torch.randn((E, d), generator=g) / d ** 0.5).bfloat16()
@@ -102,6 +104,27 @@ def test_router_bf16_against_oracle_on_same_inputs(cuda, T, d, E, k, qwen):
     chosen = np.take_along_axis(ref_logits.numpy(), got.astype(np.int64), 1)
     assert np.all(chosen[~safe] >= kth[~safe, None] - band)
     assert np.all(np.diff(got, axis=1) > 0)
+
+
+@pytest.mark.parametrize("T,d,E,k,qwen,ns", [(8192, 4096, 8, 2, 0, 0), (8192, 2048, 60, 4, 1, 4), (4500, 1024, 24, 3, 0, 0),
+                                             (5000, 2048, 60, 4, 1, 0), (4097, 4096, 7, 2, 0, 0),
+                                             (6000, 2048, 16, 2, 1, 2)])
+def test_router_group_selection_is_select_token_bit_for_bit(cuda, T, d, E, k, qwen, ns):
+    """The tcgen05 router's selection (select_group: G lanes per token) against the per-warp
+    select_token of the f32 SIMT router run on the very same logits (x = the tcgen05 kernel's fp32
+    logits, W_router = identity, so every f32 logit is exact): ids and weights bit-identical, the
+    shared gate slots included."""
+    g = torch.Generator().manual_seed(T + E)
+    rows = E + (1 if ns else 0)
+    x = torch.randn((T, d), generator=g).bfloat16().cuda()
+    wr = (torch.randn((rows, d), generator=g) / d ** 0.5).bfloat16().cuda()
+    mode = K.ROUTE_SOFTMAX_TOPK if qwen else K.ROUTE_TOPK_SOFTMAX
+    ids, w, logits = K.router(x, wr, k, mode, want_logits=True, n_shared=ns)
+    eye = torch.eye(rows, dtype=torch.float32, device="cuda")
+    ids2, w2, logits2 = K.router(logits.contiguous(), eye, k, mode, want_logits=True, n_shared=ns)
+    assert torch.equal(logits2, logits)
+    assert torch.equal(ids, ids2)
+    assert torch.equal(w, w2)
 
 
 def test_router_qwen_softmax_topk_mode(cuda):
