@@ -302,6 +302,26 @@ __device__ __forceinline__ void select_group(const float (&l0)[32 / G], const fl
   }
 }
 
+// Selection of a 16-token tile whose logits sit in shared memory (row stride kMaxE): the block's
+// NT threads form 16 groups of G = NT / 16 lanes, one token each (select_group, bit-identical to
+// select_token), instead of kWarps warps walking the 16 tokens in turn.
+template <int NT>
+__device__ __forceinline__ void select_tile16(const float* s_logit, int tok0, int ntok, int E, int k, int mode,
+                                              int32_t* __restrict__ ids_out, float* __restrict__ w_out,
+                                              float* __restrict__ logits_out) {
+  constexpr int G = NT / 16, C = 32 / G;
+  static_assert(G >= 1 && G <= 32 && 32 % G == 0, "16 groups of a power-of-two size");
+  const int r = threadIdx.x / G, j = threadIdx.x % G;
+  float l0[C], l1[C];
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    const int L = j + G * i;
+    l0[i] = L < E ? s_logit[r * kMaxE + L] : 0.f;
+    l1[i] = L + 32 < E ? s_logit[r * kMaxE + L + 32] : 0.f;
+  }
+  select_group<G>(l0, l1, tok0 + r < ntok, tok0 + r, E, k, mode, j, ids_out, w_out, logits_out);
+}
+
 // One CTA owns TPC tokens, split into TPC/TPW groups of TPW tokens; each group gets kWarps/groups
 // warps laid out as (d slice) x (8-expert chunk).  Decode (TPC = 1): with few experts (Mixtral's 8)
 // all 8 warps split d, with many (Qwen's 60) each warp owns one chunk over the whole of d, so a
@@ -651,7 +671,6 @@ router_stream_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* _
   constexpr int kCols = 8 * NTW * NQ;  // experts covered (padded)
   __shared__ float s_part[DS][16][kCols];
   __shared__ float s_logit[16][kMaxE];
-  __shared__ float s_score[16][kMaxE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int slice = warp / NQ, grp = warp % NQ;
@@ -716,12 +735,7 @@ router_stream_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* _
     s_logit[t][e] = v;
   }
   __syncthreads();
-#pragma unroll 1
-  for (int ti = warp; ti < 16; ti += kWarps) {
-    const int tok = tok0 + ti;
-    if (tok >= ntok) break;
-    select_token<float>(s_logit[ti], s_score[ti], tok, E, k, mode, lane, ids_out, w_out, logits_out);
-  }
+  select_tile16<kWarps * 32>(&s_logit[0][0], tok0, ntok, E, k, mode, ids_out, w_out, logits_out);
 }
 
 template <int DS, int NQ, int NTW, int U, int MINB = 1>
@@ -749,7 +763,6 @@ router_wreg_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __r
   constexpr int DS = 8;
   __shared__ float s_part[DS][16][8];
   __shared__ float s_logit[16][kMaxE];
-  __shared__ float s_score[16][kMaxE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int k0 = warp * KS * 32;  // this warp's d slice: KS k32 steps
@@ -802,12 +815,7 @@ router_wreg_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __r
       s_logit[t][e] = v;
     }
     __syncthreads();
-#pragma unroll 1
-    for (int ti = warp; ti < 16; ti += 8) {
-      const int tok = tok0 + ti;
-      if (tok >= ntok) break;
-      select_token<float>(s_logit[ti], s_score[ti], tok, E, k, mode, lane, ids_out, w_out, logits_out);
-    }
+    select_tile16<256>(&s_logit[0][0], tok0, ntok, E, k, mode, ids_out, w_out, logits_out);
     __syncthreads();  // s_part / s_logit are rewritten by the next tile
   }
 }
@@ -1206,9 +1214,10 @@ int try_router_tc(const void* x, const void* wr, int T_, int d, int E, int k, in
     const char* v = getenv("QMOE_ROUTER_TC_MIN");
     return v == nullptr ? 0 : atoi(v);
   }();
-  // measured crossover against the mma.sync kernels (tools/router_ab.py, L2 flushed): Mixtral
-  // 4096 tokens 18.4 vs 18.5 us, Qwen (61 logit rows) 2048 tokens 16.8 vs 17.1, 4096 28.6 vs 18.8
-  const int tmin = tmin_env ? tmin_env : (E > 16 ? 3072 : 4096);
+  // measured crossover against the mma.sync kernels (tools/router_ab.py, L2 flushed, CUDA events):
+  // Mixtral 2048 / 3072 / 4096 tokens 16.4 / 16.8 / 18.4 us vs 14.3 / 21.2 / 17.3; Qwen (61 logit
+  // rows) 16.4 / 18.4 / 18.4 vs 16.4 / 26.6 / 28.7
+  const int tmin = tmin_env ? tmin_env : 3072;
   static const int s_env = [] {
     const char* v = getenv("QMOE_ROUTER_TC_S");
     return v == nullptr ? 0 : atoi(v);

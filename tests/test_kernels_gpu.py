@@ -108,10 +108,13 @@ def test_router_bf16_against_oracle_on_same_inputs(cuda, T, d, E, k, qwen):
 
 @pytest.mark.parametrize("T,d,E,k,qwen,ns", [(8192, 4096, 8, 2, 0, 0), (8192, 2048, 60, 4, 1, 4), (4500, 1024, 24, 3, 0, 0),
                                              (5000, 2048, 60, 4, 1, 0), (4097, 4096, 7, 2, 0, 0),
-                                             (6000, 2048, 16, 2, 1, 2)])
+                                             (6000, 2048, 16, 2, 1, 2), (300, 4096, 8, 2, 0, 0),
+                                             (2000, 2048, 60, 4, 1, 4), (2500, 1024, 16, 2, 0, 0),
+                                             (2049, 2048, 24, 3, 1, 0), (1000, 4096, 8, 2, 0, 0)])
 def test_router_group_selection_is_select_token_bit_for_bit(cuda, T, d, E, k, qwen, ns):
-    """The tcgen05 router's selection (select_group: G lanes per token) against the per-warp
-    select_token of the f32 SIMT router run on the very same logits (x = the tcgen05 kernel's fp32
+    """The bf16 prefill routers' selection (select_group: G lanes per token, in the tcgen05 kernel
+    from 3-4k tokens and the register-streamed mma.sync kernels below) against the per-warp
+    select_token of the f32 SIMT router run on the very same logits (x = the bf16 kernel's fp32
     logits, W_router = identity, so every f32 logit is exact): ids and weights bit-identical, the
     shared gate slots included."""
     g = torch.Generator().manual_seed(T + E)
