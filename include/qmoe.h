@@ -411,6 +411,19 @@ QMOE_API int qmoe_paged_decode_attention(const void* q, int q_stride, const void
                                          const int32_t* seq_lens, int B, int H, int KV, int head_dim, int page_size,
                                          int max_pages, int max_len, float scale, void* out, void* workspace,
                                          size_t workspace_bytes, void* stream);
+/*
+ * Causal varlen GQA prefill attention (the decoders' attention stage on prefill passes; reference
+ * counterpart: _prefill_attention, engine.py:252-301 / attend, model.py:58-68, a toy single-head
+ * attention; replaces flash-attn's varlen kernel).  Sequence b owns rows [cu_seqlens[b],
+ * cu_seqlens[b+1]) of q / k / v (bf16; rows q_stride / kv_stride elements apart, heads dense:
+ * e.g. views into a packed qkv projection); query i of a sequence attends its keys 0..i.  max_len
+ * >= the longest sequence (host-known).  out: [rows, out_stride] bf16, head h at columns
+ * h*head_dim.  fp32 scores, online softmax and accumulation (P rounded to bf16 for P.V).  head_dim
+ * 64 or 128, H a multiple of KV; q / k / v 16-byte aligned.
+ */
+QMOE_API int qmoe_prefill_attention(const void* q, const void* k, const void* v, int q_stride, int kv_stride,
+                                    const int32_t* cu_seqlens, int B, int max_len, int H, int KV, int head_dim,
+                                    float scale, void* out, int out_stride, void* stream);
 QMOE_API size_t qmoe_lm_head_argmax_workspace_bytes(void);
 QMOE_API int qmoe_lm_head_argmax(const void* h, const void* w_out, int T, int d, int V, int32_t* tokens_out,
                                  void* workspace, size_t workspace_bytes, void* stream);

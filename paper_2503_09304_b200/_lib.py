@@ -75,6 +75,8 @@ SIGNATURES = {
     "qmoe_paged_decode_attention_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int]),
     "qmoe_paged_decode_attention": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int,
                                              _c_int, _c_int, ctypes.c_float, _vp, _vp, _c_size, _vp]),
+    "qmoe_prefill_attention": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                        ctypes.c_float, _vp, _c_int, _vp]),
     "qmoe_lm_head_argmax_workspace_bytes": (_c_size, []),
     "qmoe_lm_head_argmax": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_size, _vp]),
     "qmoe_expert_ffn_gather": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int,

@@ -21,7 +21,7 @@ STAMP = PKG / ".libqmoe.stamp"
 
 SOURCES = ["router.cu", "permute.cu", "combine.cu", "expert.cu", "expert_simt.cu", "expert_tc.cu", "expert_swap.cu",
            "decoder.cu", "ep.cu", "expert_fused.cu", "lm_head.cu",
-           "attention.cu"]
+           "attention.cu", "attention_prefill.cu"]
 HEADERS = ["common.cuh", "expert_common.cuh", "tc_ptx.cuh"]
 
 NVCC_FLAGS = [

@@ -272,6 +272,29 @@ def paged_decode_attention(q: torch.Tensor, pool: torch.Tensor, block_table: tor
     return out
 
 
+def prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, cu_seqlens: torch.Tensor, max_len: int,
+                      scale: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Causal varlen GQA attention of packed sequences: q [T, H, hd], k / v [T, KV, hd] bf16 (rows
+    may be strided views into a packed qkv projection; heads and features dense), cu_seqlens
+    [B + 1] int32 -> out [T, H, hd] bf16 (flash_attn_varlen_func(..., causal=True) semantics)."""
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if not t.is_cuda or t.dtype != torch.bfloat16 or t.dim() != 3 or t.stride(2) != 1 or t.stride(1) != t.shape[2]:
+            raise ValueError(f"{name} must be a CUDA bf16 [T, heads, head_dim] tensor with dense heads")
+    if k.stride(0) != v.stride(0) or k.shape != v.shape:
+        raise ValueError("k and v must share shape and row stride")
+    _need(cu_seqlens, "cu_seqlens", torch.int32)
+    T, H, hd = q.shape
+    KV = k.shape[1]
+    B = cu_seqlens.shape[0] - 1
+    if out is None:
+        out = torch.empty((T, H, hd), dtype=q.dtype, device=q.device)
+    lib = _lib.load()
+    check(lib.qmoe_prefill_attention(_ptr(q), _ptr(k), _ptr(v), q.stride(0), k.stride(0), _ptr(cu_seqlens), B,
+                                     int(max_len), H, KV, hd, float(scale), _ptr(out), out.stride(0), _stream()),
+          "qmoe_prefill_attention")
+    return out
+
+
 def lm_head_argmax(h: torch.Tensor, w_out: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Greedy tokens [T] int32 on the device: argmax_v(w_out[v] . h[t]), lowest id on ties."""
     _need(h, "h", torch.bfloat16)

@@ -4,8 +4,9 @@ Random-init bf16 weights of the real architectures (no checkpoints exist offline
 GQA attention with RoPE over the device paged KV cache, a sparse MoE block per layer, final
 norm + LM head with greedy (lowest-id-on-tie) emission.  The MoE block is the hot path and runs
 entirely on libqmoe (router, permute, tcgen05 grouped SwiGLU experts, combine with the residual
-fused); attention is outside the north-star path and uses flash-attn's paged kernels (library
-code, like cuBLAS) on the engine-owned page pool.
+fused); attention runs on libqmoe too: the paged GQA decode kernel over
+the engine-owned page pool and the causal varlen prefill kernel (flash-attn's kernels only for
+A/B runs: QMOE_FA_DECODE=1 / QMOE_FA_PREFILL=1).
 
 Layer semantics = HF MixtralDecoderLayer / Qwen2MoeDecoderLayer:
   h2 = h + o_proj(attn(rope(q), rope(k), v))          (ATTENTION stage: returns x=norm2(h2), res=h2)
@@ -91,9 +92,6 @@ class DecoderMoEModel:
         if not 0 <= lo < hi <= cfg.num_experts + S:
             raise ValueError(f"bad expert range [{lo}, {hi}) of {cfg.num_experts + S}")
         self.e_lo, self.e_hi = lo, hi
-        from flash_attn import flash_attn_varlen_func, flash_attn_with_kvcache
-
-        self._fa_varlen, self._fa_kvcache = flash_attn_varlen_func, flash_attn_with_kvcache
         g = torch.Generator(device=self.device).manual_seed(seed)
         d, F, E, hd = cfg.hidden_dim, cfg.ffn_dim, cfg.num_experts, cfg.head_dim
         H, KV = cfg.n_heads, cfg.n_kv_heads
@@ -147,6 +145,11 @@ class DecoderMoEModel:
         import os
 
         self._fa_decode = os.environ.get("QMOE_FA_DECODE", "0") == "1"
+        self._fa_prefill = os.environ.get("QMOE_FA_PREFILL", "0") == "1"  # flash-attn varlen prefill (A/B)
+        if self._fa_decode or self._fa_prefill:  # library kernels only for A/B runs
+            from flash_attn import flash_attn_varlen_func, flash_attn_with_kvcache
+
+            self._fa_varlen, self._fa_kvcache = flash_attn_varlen_func, flash_attn_with_kvcache
 
     # ------------------------------------------------------------------ cache geometry
     def kv_row_shape(self):
@@ -229,6 +232,9 @@ class DecoderMoEModel:
             pool = cache.pool(layer)
             attn = self._fa_kvcache(q.view(T, 1, H, hd), pool[:, :, 0], pool[:, :, 1], cache_seqlens=meta["lens"],
                                     block_table=meta["bt"], causal=True).view(T, H * hd)
+        elif not self._fa_prefill:
+            # hand-written causal varlen GQA prefill attention (csrc/attention_prefill.cu)
+            attn = K.prefill_attention(q, k, v, meta["cu"], meta["max"], hd ** -0.5).view(T, H * hd)
         else:
             attn = self._fa_varlen(q, k, v, meta["cu"], meta["cu"], meta["max"], meta["max"],
                                    causal=True).reshape(T, H * hd)

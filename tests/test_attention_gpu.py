@@ -81,3 +81,69 @@ def test_paged_decode_matches_flash_attn(cuda):
     ref = fa.flash_attn_with_kvcache(q.view(32, 1, 32, 128), pool[:, :, 0], pool[:, :, 1], cache_seqlens=ln,
                                      block_table=bt, causal=True).view(32, 32, 128)
     assert (got.float() - ref.float()).abs().max().item() < 2e-2
+
+
+# ------------------------------------------------------------------------- prefill (varlen, causal)
+
+def _prefill_case(H, KV, lens, hd=128, seed=0):
+    """q / k / v as strided views into one packed [T, (H + 2 KV) hd] projection, as the decoders
+    hold them."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    T = sum(lens)
+    qkv = torch.randn((T, (H + 2 * KV) * hd), device="cuda", generator=g).bfloat16()
+    q = qkv[:, : H * hd].view(T, H, hd)
+    k = qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd)
+    v = qkv[:, (H + KV) * hd:].view(T, KV, hd)
+    cu = [0]
+    for n in lens:
+        cu.append(cu[-1] + n)
+    return q, k, v, torch.tensor(cu, dtype=torch.int32, device="cuda")
+
+
+def _prefill_ref(q, k, v, cu, scale):
+    T, H, hd = q.shape
+    KV = k.shape[1]
+    out = torch.empty((T, H, hd), dtype=torch.float32, device="cuda")
+    c = cu.tolist()
+    for b in range(len(c) - 1):
+        s, e = c[b], c[b + 1]
+        n = e - s
+        mask = torch.ones((n, n), dtype=torch.bool, device="cuda").tril()
+        for h in range(H):
+            gq = h // (H // KV)
+            sc = (q[s:e, h].float() @ k[s:e, gq].float().T) * scale
+            p = torch.softmax(sc.masked_fill(~mask, float("-inf")), -1)
+            out[s:e, h] = p @ v[s:e, gq].float()
+    return out
+
+
+@pytest.mark.parametrize("H,KV", [(32, 8), (16, 16), (8, 2)])
+@pytest.mark.parametrize("lens", [[1], [64], [65, 3, 200], [513, 17, 64, 1000, 2]])
+def test_prefill_attention_matches_torch(cuda, H, KV, lens):
+    q, k, v, cu = _prefill_case(H, KV, lens)
+    scale = 128 ** -0.5
+    got = K.prefill_attention(q, k, v, cu, max(lens), scale)
+    ref = _prefill_ref(q, k, v, cu, scale)
+    err = (got.float() - ref).abs().max().item()
+    assert err < 2e-2, err
+    assert torch.equal(K.prefill_attention(q, k, v, cu, max(lens), scale), got)  # deterministic
+
+
+@pytest.mark.parametrize("H,KV", [(8, 2), (4, 4)])
+def test_prefill_attention_head_dim_64(cuda, H, KV):
+    lens = [1, 64, 300, 129]
+    q, k, v, cu = _prefill_case(H, KV, lens, hd=64, seed=5)
+    got = K.prefill_attention(q, k, v, cu, max(lens), 64 ** -0.5)
+    ref = _prefill_ref(q, k, v, cu, 64 ** -0.5)
+    assert (got.float() - ref).abs().max().item() < 2e-2
+
+
+def test_prefill_attention_matches_flash_attn(cuda):
+    """Against the library kernel it replaces (flash_attn_varlen_func, causal), Mixtral heads."""
+    flash_attn = pytest.importorskip("flash_attn")
+    lens = [700, 1, 256, 31, 2048]
+    q, k, v, cu = _prefill_case(32, 8, lens, seed=3)
+    got = K.prefill_attention(q, k, v, cu, max(lens), 128 ** -0.5)
+    fa = flash_attn.flash_attn_varlen_func(q, k, v, cu, cu, max(lens), max(lens), causal=True)
+    err = (got.float() - fa.float()).abs().max().item()
+    assert err < 1e-2, err
