@@ -8,18 +8,19 @@
 // attends the keys of its own sequence at positions <= its own (the prompt's K/V; a prefill pass
 // starts from an empty cache, so these are exactly the entries the pass appends to the page pool).
 //
-// Flash-attention forward on mma.sync m16n8k16 (bf16 in, fp32 accumulate): CTA = (64-query block,
-// head, sequence), 4 warps x 16 query rows.  Q is staged once and held as A fragments; 64-key
+// Flash-attention forward on mma.sync m16n8k16 (bf16 in, fp32 accumulate): CTA = (16 W-query
+// block, head, sequence), W = 4 or 8 warps x 16 query rows.  Q is staged once and held as A fragments; 64-key
 // blocks of K and V stream through a 2-stage cp.async ring (padded rows, ldmatrix / ldmatrix.trans);
 // S = Q K^T stays in registers, online softmax in the exp2 domain with quad shuffles, P is re-packed
 // from the S accumulators straight into A fragments for O += P V.  Keys beyond the query (causal)
 // or beyond the sequence are masked; the last key block is the diagonal one.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace qmoe {
 namespace {
 
-constexpr int kQB = 64;  // query rows per CTA (16 per warp)
 constexpr int kKB = 64;  // keys per block
 
 __device__ __forceinline__ void ldsm_x4(const void* p, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
@@ -51,13 +52,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
-template <int HD>
-__global__ void __launch_bounds__(128)
+template <int HD, int W>  // W warps x 16 query rows per CTA
+__global__ void __launch_bounds__(W * 32)
 prefill_attn_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
                     const __nv_bfloat16* __restrict__ v, int q_stride, int kv_stride, const int32_t* __restrict__ cu,
                     int H, int KV, float scale_log2, __nv_bfloat16* __restrict__ out, int out_stride) {
   pdl_wait();
   pdl_trigger();
+  constexpr int kQB = 16 * W;  // query rows per CTA
+  constexpr int kThreads = W * 32;
   constexpr int LD = HD + 8;  // padded smem row (bf16): ldmatrix rows 16 B apart mod 128 B
   constexpr int NT = HD / 8;  // n8 tiles of the output
   constexpr int KS = HD / 16; // k16 steps of Q K^T
@@ -74,7 +77,7 @@ prefill_attn_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int kPieces = HD / 8;  // 16-byte pieces per row
   // Q tile
-  for (int i = tid; i < kQB * kPieces; i += 128) {
+  for (int i = tid; i < kQB * kPieces; i += kThreads) {
     const int r = i / kPieces, c = (i % kPieces) * 8;
     const int t = q0 + r;
     cp16(sQ + r * LD + c, q + (size_t)(start + min(t, len - 1)) * q_stride + h * HD + c, t < len);
@@ -83,7 +86,7 @@ prefill_attn_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
     const int k0 = kb * kKB;
     __nv_bfloat16* dk = sK + st * kKB * LD;
     __nv_bfloat16* dv = sV + st * kKB * LD;
-    for (int i = tid; i < kKB * kPieces; i += 128) {
+    for (int i = tid; i < kKB * kPieces; i += kThreads) {
       const int r = i / kPieces, c = (i % kPieces) * 8;
       const int t = k0 + r;
       const size_t row = (size_t)(start + min(t, len - 1)) * kv_stride + g * HD + c;
@@ -209,19 +212,33 @@ prefill_attn_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
   }
 }
 
-template <int HD>
+template <int HD, int W>
 int launch_prefill(const void* q, const void* k, const void* v, int q_stride, int kv_stride, const int32_t* cu, int B,
                    int max_len, int H, int KV, float scale, void* out, int out_stride, cudaStream_t s) {
-  constexpr int smem = (kQB + 4 * kKB) * (HD + 8) * 2;
+  constexpr int smem = (16 * W + 4 * kKB) * (HD + 8) * 2;
   static uint64_t attr_set = 0;  // devices already configured
   if (!(attr_set & current_device_bit())) {
-    QMOE_CUDA_TRY(cudaFuncSetAttribute(prefill_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    QMOE_CUDA_TRY(cudaFuncSetAttribute(prefill_attn_kernel<HD, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set |= current_device_bit();
   }
-  const dim3 grid((max_len + kQB - 1) / kQB, H, B);
-  return launch_pdl("qmoe_prefill_attention", prefill_attn_kernel<HD>, grid, dim3(128), smem, s,
+  const dim3 grid((max_len + 16 * W - 1) / (16 * W), H, B);
+  return launch_pdl("qmoe_prefill_attention", prefill_attn_kernel<HD, W>, grid, dim3(W * 32), smem, s,
                     (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, q_stride, kv_stride, cu,
                     H, KV, scale * 1.4426950408889634f, (__nv_bfloat16*)out, out_stride);
+}
+
+// 128-query CTAs (8 warps) halve the K/V tile loads per query row; 64-query CTAs keep short
+// prompts spread over more CTAs.  QMOE_PREFILL_W=4/8 forces one.
+template <int HD>
+int dispatch_prefill(const void* q, const void* k, const void* v, int q_stride, int kv_stride, const int32_t* cu,
+                     int B, int max_len, int H, int KV, float scale, void* out, int out_stride, cudaStream_t s) {
+  static const int w_env = [] {
+    const char* e = getenv("QMOE_PREFILL_W");
+    return e == nullptr ? 0 : atoi(e);
+  }();
+  const bool wide = w_env ? w_env == 8 : max_len >= 1024;
+  return wide ? launch_prefill<HD, 8>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s)
+              : launch_prefill<HD, 4>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s);
 }
 
 }  // namespace
@@ -244,8 +261,8 @@ extern "C" int qmoe_prefill_attention(const void* q, const void* k, const void* 
                "qmoe_prefill_attention: q / k / v must be 16-byte aligned");
   QMOE_REQUIRE(B <= 65535 && H <= 65535, "qmoe_prefill_attention: B=%d H=%d exceed the grid", B, H);
   cudaStream_t s = as_stream(stream);
-  return head_dim == 128 ? launch_prefill<128>(q, k, v, q_stride, kv_stride, cu_seqlens, B, max_len, H, KV, scale, out,
+  return head_dim == 128 ? dispatch_prefill<128>(q, k, v, q_stride, kv_stride, cu_seqlens, B, max_len, H, KV, scale, out,
                                                out_stride, s)
-                         : launch_prefill<64>(q, k, v, q_stride, kv_stride, cu_seqlens, B, max_len, H, KV, scale, out,
+                         : dispatch_prefill<64>(q, k, v, q_stride, kv_stride, cu_seqlens, B, max_len, H, KV, scale, out,
                                               out_stride, s);
 }

@@ -118,7 +118,7 @@ def _prefill_ref(q, k, v, cu, scale):
 
 
 @pytest.mark.parametrize("H,KV", [(32, 8), (16, 16), (8, 2)])
-@pytest.mark.parametrize("lens", [[1], [64], [65, 3, 200], [513, 17, 64, 1000, 2]])
+@pytest.mark.parametrize("lens", [[1], [64], [65, 3, 200], [513, 17, 64, 1000, 2], [1100, 5, 130]])
 def test_prefill_attention_matches_torch(cuda, H, KV, lens):
     q, k, v, cu = _prefill_case(H, KV, lens)
     scale = 128 ** -0.5
