@@ -212,6 +212,210 @@ prefill_attn_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __
   }
 }
 
+// The same computation with two 16-row m tiles per warp (4 warps x 32 query rows = 128-query CTAs):
+// every K / V fragment loaded from shared memory feeds both m tiles, halving the ldmatrix traffic
+// per MMA; Q is re-read from shared memory per k step instead of held in registers.  Per query row
+// the arithmetic (MMA order, masking, softmax updates, P.V order) is exactly prefill_attn_kernel's,
+// so the two kernels return the same bits.
+template <int HD>
+__global__ void __launch_bounds__(128, 1)
+prefill_attn_wide_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+                         const __nv_bfloat16* __restrict__ v, int q_stride, int kv_stride,
+                         const int32_t* __restrict__ cu, int H, int KV, float scale_log2,
+                         __nv_bfloat16* __restrict__ out, int out_stride) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int kQB = 128, kThreads = 128, MT = 2;
+  constexpr int LD = HD + 8;
+  constexpr int NT = HD / 8;
+  constexpr int KS = HD / 16;
+  extern __shared__ __align__(16) __nv_bfloat16 smem[];
+  __nv_bfloat16* sQ = smem;
+  __nv_bfloat16* sK = sQ + kQB * LD;
+  __nv_bfloat16* sV = sK + 2 * kKB * LD;
+  const int b = blockIdx.z, h = blockIdx.y, qb = gridDim.x - 1 - blockIdx.x;
+  const int start = cu[b], len = cu[b + 1] - start;
+  const int q0 = qb * kQB;
+  if (q0 >= len) return;
+  const int g = h / (H / KV);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kPieces = HD / 8;
+  for (int i = tid; i < kQB * kPieces; i += kThreads) {
+    const int r = i / kPieces, c = (i % kPieces) * 8;
+    const int t = q0 + r;
+    cp16(sQ + r * LD + c, q + (size_t)(start + min(t, len - 1)) * q_stride + h * HD + c, t < len);
+  }
+  auto load_kv = [&](int kb, int st) {
+    const int k0 = kb * kKB;
+    __nv_bfloat16* dk = sK + st * kKB * LD;
+    __nv_bfloat16* dv = sV + st * kKB * LD;
+    for (int i = tid; i < kKB * kPieces; i += kThreads) {
+      const int r = i / kPieces, c = (i % kPieces) * 8;
+      const int t = k0 + r;
+      const size_t row = (size_t)(start + min(t, len - 1)) * kv_stride + g * HD + c;
+      cp16(dk + r * LD + c, k + row, t < len);
+      cp16(dv + r * LD + c, v + row, t < len);
+    }
+  };
+  const int nkb = min((len + kKB - 1) / kKB, (q0 + kQB - 1) / kKB + 1);
+  load_kv(0, 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  const int qr0 = warp * 32;  // m tile mt: rows qr0 + 16 mt .. + 15
+  int row_a[MT], row_b[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    row_a[mt] = q0 + qr0 + 16 * mt + (lane >> 2);
+    row_b[mt] = row_a[mt] + 8;
+  }
+  float o[MT][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[mt][n][0] = o[mt][n][1] = o[mt][n][2] = o[mt][n][3] = 0.f;
+  float m_a[MT], m_b[MT], l_a[MT], l_b[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    m_a[mt] = m_b[mt] = -INFINITY;
+    l_a[mt] = l_b[mt] = 0.f;
+  }
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int st = kb & 1;
+    if (kb + 1 < nkb) load_kv(kb + 1, st ^ 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const __nv_bfloat16* bk = sK + st * kKB * LD;
+    const __nv_bfloat16* bv = sV + st * kKB * LD;
+    float s[MT][kKB / 8][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int n = 0; n < kKB / 8; ++n) s[mt][n][0] = s[mt][n][1] = s[mt][n][2] = s[mt][n][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t qa[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+        ldsm_x4(sQ + (qr0 + 16 * mt + (lane & 15)) * LD + ks * 16 + (lane >> 4) * 8, qa[mt][0], qa[mt][1], qa[mt][2],
+                qa[mt][3]);
+#pragma unroll
+      for (int np = 0; np < kKB / 16; ++np) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(bk + (16 * np + (lane >> 4) * 8 + (lane & 7)) * LD + ks * 16 + ((lane >> 3) & 1) * 8, b0, b1, b2, b3);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          mma16816(s[mt][2 * np], qa[mt][0], qa[mt][1], qa[mt][2], qa[mt][3], b0, b1);
+          mma16816(s[mt][2 * np + 1], qa[mt][0], qa[mt][1], qa[mt][2], qa[mt][3], b2, b3);
+        }
+      }
+    }
+    const int k0 = kb * kKB;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      float mx_a = m_a[mt], mx_b = m_b[mt];
+#pragma unroll
+      for (int n = 0; n < kKB / 8; ++n) {
+        const int key = k0 + 8 * n + 2 * (lane & 3);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int kk = key + c;
+          s[mt][n][c] = (kk <= row_a[mt] && kk < len) ? s[mt][n][c] * scale_log2 : -INFINITY;
+          s[mt][n][2 + c] = (kk <= row_b[mt] && kk < len) ? s[mt][n][2 + c] * scale_log2 : -INFINITY;
+          mx_a = fmaxf(mx_a, s[mt][n][c]);
+          mx_b = fmaxf(mx_b, s[mt][n][2 + c]);
+        }
+      }
+#pragma unroll
+      for (int off = 1; off < 4; off <<= 1) {
+        mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, off));
+        mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, off));
+      }
+      const float base_a = mx_a == -INFINITY ? 0.f : mx_a, base_b = mx_b == -INFINITY ? 0.f : mx_b;
+      const float corr_a = exp2f(m_a[mt] - base_a), corr_b = exp2f(m_b[mt] - base_b);
+      m_a[mt] = mx_a;
+      m_b[mt] = mx_b;
+      float sum_a = 0.f, sum_b = 0.f;
+#pragma unroll
+      for (int n = 0; n < kKB / 8; ++n) {
+        s[mt][n][0] = exp2f(s[mt][n][0] - base_a);
+        s[mt][n][1] = exp2f(s[mt][n][1] - base_a);
+        s[mt][n][2] = exp2f(s[mt][n][2] - base_b);
+        s[mt][n][3] = exp2f(s[mt][n][3] - base_b);
+        sum_a += s[mt][n][0] + s[mt][n][1];
+        sum_b += s[mt][n][2] + s[mt][n][3];
+      }
+      l_a[mt] = l_a[mt] * corr_a + sum_a;
+      l_b[mt] = l_b[mt] * corr_b + sum_b;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        o[mt][n][0] *= corr_a;
+        o[mt][n][1] *= corr_a;
+        o[mt][n][2] *= corr_b;
+        o[mt][n][3] *= corr_b;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < kKB / 16; ++kk) {
+      uint32_t pa[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        pa[mt][0] = pack_bf16(s[mt][2 * kk][0], s[mt][2 * kk][1]);
+        pa[mt][1] = pack_bf16(s[mt][2 * kk][2], s[mt][2 * kk][3]);
+        pa[mt][2] = pack_bf16(s[mt][2 * kk + 1][0], s[mt][2 * kk + 1][1]);
+        pa[mt][3] = pack_bf16(s[mt][2 * kk + 1][2], s[mt][2 * kk + 1][3]);
+      }
+#pragma unroll
+      for (int np = 0; np < NT / 2; ++np) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(bv + (16 * kk + (lane & 15)) * LD + 16 * np + (lane >> 4) * 8, b0, b1, b2, b3);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          mma16816(o[mt][2 * np], pa[mt][0], pa[mt][1], pa[mt][2], pa[mt][3], b0, b1);
+          mma16816(o[mt][2 * np + 1], pa[mt][0], pa[mt][1], pa[mt][2], pa[mt][3], b2, b3);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    float la = l_a[mt], lb = l_b[mt];
+#pragma unroll
+    for (int off = 1; off < 4; off <<= 1) {
+      la += __shfl_xor_sync(0xffffffffu, la, off);
+      lb += __shfl_xor_sync(0xffffffffu, lb, off);
+    }
+    const float inv_a = la > 0.f ? 1.f / la : 0.f, inv_b = lb > 0.f ? 1.f / lb : 0.f;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int c = h * HD + 8 * n + 2 * (lane & 3);
+      if (row_a[mt] < len)
+        *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(start + row_a[mt]) * out_stride + c) =
+            __floats2bfloat162_rn(o[mt][n][0] * inv_a, o[mt][n][1] * inv_a);
+      if (row_b[mt] < len)
+        *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(start + row_b[mt]) * out_stride + c) =
+            __floats2bfloat162_rn(o[mt][n][2] * inv_b, o[mt][n][3] * inv_b);
+    }
+  }
+}
+
+template <int HD>
+int launch_prefill_wide(const void* q, const void* k, const void* v, int q_stride, int kv_stride, const int32_t* cu,
+                        int B, int max_len, int H, int KV, float scale, void* out, int out_stride, cudaStream_t s) {
+  constexpr int smem = (128 + 4 * kKB) * (HD + 8) * 2;
+  static uint64_t attr_set = 0;  // devices already configured
+  if (!(attr_set & current_device_bit())) {
+    QMOE_CUDA_TRY(
+        cudaFuncSetAttribute(prefill_attn_wide_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set |= current_device_bit();
+  }
+  const dim3 grid((max_len + 127) / 128, H, B);
+  return launch_pdl("qmoe_prefill_attention(wide)", prefill_attn_wide_kernel<HD>, grid, dim3(128), smem, s,
+                    (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, q_stride, kv_stride, cu,
+                    H, KV, scale * 1.4426950408889634f, (__nv_bfloat16*)out, out_stride);
+}
+
 template <int HD, int W>
 int launch_prefill(const void* q, const void* k, const void* v, int q_stride, int kv_stride, const int32_t* cu, int B,
                    int max_len, int H, int KV, float scale, void* out, int out_stride, cudaStream_t s) {
@@ -227,8 +431,9 @@ int launch_prefill(const void* q, const void* k, const void* v, int q_stride, in
                     H, KV, scale * 1.4426950408889634f, (__nv_bfloat16*)out, out_stride);
 }
 
-// 128-query CTAs (8 warps) halve the K/V tile loads per query row; 64-query CTAs keep short
-// prompts spread over more CTAs.  QMOE_PREFILL_W=4/8 forces one.
+// 128-query CTAs halve the K/V tile loads per query row; 64-query CTAs keep short prompts spread
+// over more CTAs.  QMOE_PREFILL_W forces one: 4 / 8 = prefill_attn_kernel with 4 / 8 warps of 16
+// rows, 2 = prefill_attn_wide_kernel (4 warps of 32 rows).
 template <int HD>
 int dispatch_prefill(const void* q, const void* k, const void* v, int q_stride, int kv_stride, const int32_t* cu,
                      int B, int max_len, int H, int KV, float scale, void* out, int out_stride, cudaStream_t s) {
@@ -236,9 +441,10 @@ int dispatch_prefill(const void* q, const void* k, const void* v, int q_stride, 
     const char* e = getenv("QMOE_PREFILL_W");
     return e == nullptr ? 0 : atoi(e);
   }();
-  const bool wide = w_env ? w_env == 8 : max_len >= 1024;
-  return wide ? launch_prefill<HD, 8>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s)
-              : launch_prefill<HD, 4>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s);
+  if (w_env == 2 || (w_env == 0 && max_len >= 1024))  // 4 warps x 32 rows
+    return launch_prefill_wide<HD>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s);
+  return w_env == 8 ? launch_prefill<HD, 8>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s)
+                    : launch_prefill<HD, 4>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s);
 }
 
 }  // namespace

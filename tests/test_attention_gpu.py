@@ -147,3 +147,15 @@ def test_prefill_attention_matches_flash_attn(cuda):
     fa = flash_attn.flash_attn_varlen_func(q, k, v, cu, cu, max(lens), max(lens), causal=True)
     err = (got.float() - fa.float()).abs().max().item()
     assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("H,KV,hd", [(32, 8, 128), (16, 16, 128), (8, 2, 64)])
+def test_prefill_attention_kernels_agree_bit_for_bit(cuda, H, KV, hd):
+    """max_len is only a host-side bound (it sizes the grid): a bound >= 1024 selects the
+    128-query kernel with 32 rows per warp, a tight bound of short prompts the 64-query kernel.
+    Per query row both run the same arithmetic, so the outputs are identical."""
+    lens = [700, 1, 64, 129, 333]
+    q, k, v, cu = _prefill_case(H, KV, lens, hd=hd, seed=11)
+    narrow = K.prefill_attention(q, k, v, cu, max(lens), hd ** -0.5)
+    wide = K.prefill_attention(q, k, v, cu, 2048, hd ** -0.5)
+    assert torch.equal(narrow, wide)
