@@ -431,8 +431,8 @@ int launch_prefill(const void* q, const void* k, const void* v, int q_stride, in
                     H, KV, scale * 1.4426950408889634f, (__nv_bfloat16*)out, out_stride);
 }
 
-// 128-query CTAs halve the K/V tile loads per query row; 64-query CTAs keep short prompts spread
-// over more CTAs.  QMOE_PREFILL_W forces one: 4 / 8 = prefill_attn_kernel with 4 / 8 warps of 16
+// 128-query CTAs halve the K/V tile loads per query row (and the 32-row warps halve the ldmatrix
+// traffic per MMA); 64-query CTAs keep short prompts spread over more CTAs.  QMOE_PREFILL_W forces one: 4 / 8 = prefill_attn_kernel with 4 / 8 warps of 16
 // rows, 2 = prefill_attn_wide_kernel (4 warps of 32 rows).
 template <int HD>
 int dispatch_prefill(const void* q, const void* k, const void* v, int q_stride, int kv_stride, const int32_t* cu,
@@ -441,7 +441,9 @@ int dispatch_prefill(const void* q, const void* k, const void* v, int q_stride, 
     const char* e = getenv("QMOE_PREFILL_W");
     return e == nullptr ? 0 : atoi(e);
   }();
-  if (w_env == 2 || (w_env == 0 && max_len >= 1024))  // 4 warps x 32 rows
+  // measured (tools/prefill_attn_ab.py): the 32-row kernel wins from 256-token prompts (Mixtral heads
+  // 8 x 256: 0.051 vs 0.058 ms; 1 x 4096: 0.553 vs 0.680), the 64-query one for 16 x 64 (0.030 vs 0.033)
+  if (w_env == 2 || (w_env == 0 && max_len >= 256))  // 4 warps x 32 rows
     return launch_prefill_wide<HD>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s);
   return w_env == 8 ? launch_prefill<HD, 8>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s)
                     : launch_prefill<HD, 4>(q, k, v, q_stride, kv_stride, cu, B, max_len, H, KV, scale, out, out_stride, s);
