@@ -211,6 +211,9 @@ extern "C" int qmoe_combine(int dtype, const void* y, const void* w, const void*
       if (k == 4)
         return launch_pdl("qmoe_combine", combine_bf16_kernel<4>, g2, block, 0, s, yb, (const float*)w, rb, T, k, d,
                           parts, ob);
+      if (k == 8)  // Qwen: 4 routed + 4 shared sub-expert slots (generic k: 79 us at 8k tokens, 4.2 TB/s)
+        return launch_pdl("qmoe_combine", combine_bf16_kernel<8>, g2, block, 0, s, yb, (const float*)w, rb, T, k, d,
+                          parts, ob);
       return launch_pdl("qmoe_combine", combine_bf16_kernel<0>, g2, block, 0, s, yb, (const float*)w, rb, T, k, d,
                         parts, ob);
     }
