@@ -61,6 +61,8 @@ struct SwapParams {
   int32_t* cursor;     // optional cursor_out (written by the last CTA out, ffn_exit)
   int32_t* progress;   // optional host-mapped per-expert progress words (signal_expert_done)
   int seq;
+  const __nv_bfloat16* w1;  // gate_up weights [E, 2F, d] (L2 prefetch ahead of griddepcontrol.wait)
+  int prefetch_bytes;       // per CTA; 0 = none
 };
 
 template <int NT>
@@ -82,6 +84,29 @@ template <int NT>
 __global__ void __launch_bounds__(kThreadsS, 1)
 ffn_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                 const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW2, SwapParams p) {
+  if (threadIdx.x == 0 && p.prefetch_bytes > 0) {
+    // The weights are not produced by the kernels this launch depends on, so before
+    // griddepcontrol.wait -- while the router and the permute of this layer still run (they
+    // trigger their dependents at entry) -- each CTA pulls into L2 the first rows of the gate and
+    // up halves of the unit it will most likely claim first (unit = CTA index: expert e_begin +
+    // b / nt1, 128-column block b % nt1, one token tile per expert at decode sizes).
+    const int nt1 = (p.F + kWRows - 1) / kWRows;
+    const int e = p.e_begin + (int)blockIdx.x / nt1, fb = (int)blockIdx.x % nt1;
+    if (e < p.e_end) {
+      const size_t row_bytes = (size_t)p.d * 2;
+      const int rows = min(kWRows, p.F - fb * kWRows);
+      const uint32_t half = (uint32_t)min((size_t)p.prefetch_bytes / 2, (size_t)rows * row_bytes) & ~15u;
+      const __nv_bfloat16* g = p.w1 + ((size_t)e * 2 * p.F + (size_t)fb * kWRows) * p.d;
+      const __nv_bfloat16* u = g + (size_t)p.F * p.d;
+      for (uint32_t off = 0; off < half; off += 65536) {
+        const uint32_t n = min(65536u, half - off);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(g) + off),
+                     "r"(n) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(u) + off),
+                     "r"(n) : "memory");
+      }
+    }
+  }
   pdl_wait();
   pdl_trigger();
   using C = SwapCfg<NT>;
@@ -457,6 +482,19 @@ int expert_ffn_swap(const void* xp, const int32_t* offsets, const int32_t* perm,
   p.cursor = cursor_out;
   p.progress = progress;
   p.seq = seq;
+  p.w1 = (const __nv_bfloat16*)w1;
+  {
+    // L2 prefetch of the first wave's gate_up rows ahead of the dependency wait
+    // (QMOE_SWAP_PREFETCH_KB = bytes per CTA / 1024).  Off by default: measured on the Qwen decode
+    // layer (tools/qwen_layer_timeline.py 32, CUPTI) with 553 KB per CTA (~80 MB) the layer span
+    // stays at 185-187 us while the router it overlaps slows from 10.8 to 12.9 us; the early
+    // trigger of the router / permute kernels alone took the span from ~190 to ~186 us.
+    static const int kb_env = [] {
+      const char* v = getenv("QMOE_SWAP_PREFETCH_KB");
+      return v == nullptr ? 0 : atoi(v);
+    }();
+    p.prefetch_bytes = kb_env > 0 ? kb_env * 1024 : 0;
+  }
   const int nkb2 = (F + kBK - 1) / kBK;
   const int want = xp_rows <= kSwapRowsMax ? swap_splits(F) : 1;  // partials sized for <= 512 rows
   p.kb_per_split = (nkb2 + want - 1) / want;

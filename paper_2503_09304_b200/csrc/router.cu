@@ -924,8 +924,8 @@ router_decode_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* _
                      int E, int k, int mode, int32_t* __restrict__ ids_out, float* __restrict__ w_out,
                      float* __restrict__ logits_out) {
   static_assert(NCH * DS == 8, "8 CTAs per cluster");
+  pdl_trigger();  // at entry: the permute and the expert launch behind it may be scheduled now
   pdl_wait();
-  pdl_trigger();
   __shared__ float s_part[8][16 * MT][8];   // per warp partials
   __shared__ float s_log[16 * MT][8];       // this CTA's (chunk, slice) logits
   __shared__ float s_full[8][kMaxE];        // per warp: one token's logits (selection)
