@@ -1233,11 +1233,11 @@ int try_router_tc(const void* x, const void* wr, int T_, int d, int E, int k, in
   if (nosel) mode |= kNoSelect;
   if (!env || T_ < tmin || E > 64 || d % 64 != 0) return 0;
   if (tc_init_driver() != QMOE_OK) return 0;
-  // d split: the smallest S that puts >= 128 CTAs on the GPU, slices of >= 512 columns (Qwen
+  // d split: the smallest S that puts >= 128 CTAs on the GPU, slices of >= 256 columns (Qwen
   // 4k / 8k / 16k tokens: S = 4 / 2 / 1 -> 18.8 / 22.5 / 28.7 us; Mixtral 8k / 16k: S = 2 / 1)
   const int ntiles = (T_ + 127) / 128;
   int S = 1;
-  while (S < 4 && ntiles * S < 128 && d / (2 * S) >= 512 && d % (128 * S) == 0) S *= 2;
+  while (S < 4 && ntiles * S < 128 && d / (2 * S) >= 256 && d % (128 * S) == 0) S *= 2;
   if (s_env == 1 || s_env == 2 || s_env == 4) S = s_env;
   if (d % (64 * S) != 0) return 0;
   const int NB = E <= 16 ? 16 : (E <= 32 ? 32 : 64);

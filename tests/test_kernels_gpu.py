@@ -374,3 +374,43 @@ def test_cursor_advance(cuda):
     stop = torch.tensor([5], dtype=torch.int32, device="cuda")
     K.cursor_advance(cur, stop)
     assert cur.cpu().tolist() == [5, 5, 6, 8]
+
+
+_SPLIT_PROBE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2503_09304_b200 import kernels as K
+from oracle import moe_oracle as om
+bad = 0
+for T, d, E, k, qwen in ((700, 1024, 8, 2, 0), (1000, 2048, 61, 4, 1), (513, 4096, 24, 3, 0)):
+    g = torch.Generator().manual_seed(T)
+    x = torch.randn((T, d), generator=g).bfloat16()
+    wr = (torch.randn((E, d), generator=g) / d ** 0.5).bfloat16()
+    mode = K.ROUTE_SOFTMAX_TOPK if qwen else K.ROUTE_TOPK_SOFTMAX
+    ids, w, lg = K.router(x.cuda(), wr.cuda(), k, mode, want_logits=True)
+    ref = x.double() @ wr.double().T
+    err = float((lg.cpu().double() - ref).abs().max())
+    oi, ow = (om.route_many_qwen if qwen else om.route_many)(wr.double().numpy(), x.double().numpy(), k)
+    srt = np.sort(ref.numpy(), axis=1)[:, ::-1]
+    safe = (srt[:, k - 1] - srt[:, k]) > 1e-3
+    bad += int(err > 2e-4) + int(not np.array_equal(ids.cpu().numpy()[safe], oi[safe]))
+print("BAD", bad)
+"""
+
+
+@pytest.mark.parametrize("split", [1, 2, 4])
+def test_router_tcgen05_every_d_split(cuda, split):
+    """Every d split of the tcgen05 router (QMOE_ROUTER_TC_S, read once per process, so each runs in
+    a fresh interpreter) at every logit-row padding (16 / 32 / 64): fp32 logits within 2e-4 of fp64
+    and ids equal to the oracle's outside the tie band."""
+    import os
+    import pathlib
+    import subprocess
+    import sys
+
+    root = str(pathlib.Path(__file__).resolve().parents[1])
+    env = dict(os.environ, QMOE_ROUTER_TC_MIN="256", QMOE_ROUTER_TC_S=str(split))
+    out = subprocess.run([sys.executable, "-c", _SPLIT_PROBE.format(root=root)], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "BAD 0" in out.stdout, out.stdout + out.stderr[-2000:]
