@@ -32,8 +32,8 @@ __device__ __forceinline__ int slot_expert(const int32_t* ids, const int32_t* cu
 __global__ void __launch_bounds__(256) perm_count_kernel(const int32_t* __restrict__ ids,
                                                          const int32_t* __restrict__ cursor, int S,
                                                          int k, int E, int32_t* __restrict__ hist) {
-  pdl_trigger();  // at entry: lets the expert launch start its weight prefetch early (see expert_swap.cu)
   pdl_wait();
+  pdl_trigger();
   __shared__ int h[kMaxE];
   for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = 0;
   __syncthreads();
@@ -71,8 +71,13 @@ __global__ void __launch_bounds__(256) perm_gather_kernel(const int32_t* __restr
                                                           const int32_t* __restrict__ offsets, int gather_e, int k,
                                                           int max_rows, const uint8_t* __restrict__ x,
                                                           uint8_t* __restrict__ xp, size_t row_bytes) {
-  pdl_trigger();  // at entry: lets the expert launch start its weight prefetch early (see expert_swap.cu)
+  // Decode-sized launches trigger their dependents at entry, so the expert launch is resident
+  // before the permute finishes (Qwen decode layer ~190 -> ~186 us, CUPTI); large ones after the
+  // wait (at 8192 Qwen tokens the entry trigger cost the grouped GEMM ~25 us).
+  const bool early = max_rows <= kChunk;
+  if (early) pdl_trigger();
   pdl_wait();
+  if (!early) pdl_trigger();
   const int R = offsets[gather_e];
   const int lane = lane_id();
   for (int r = blockIdx.x * 8 + warp_id(); r < R && r < max_rows; r += gridDim.x * 8)
@@ -84,8 +89,9 @@ perm_scatter_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__
                     int E, int nblk, int32_t* __restrict__ hist, int32_t* __restrict__ perm,
                     int32_t* __restrict__ offsets, const uint8_t* __restrict__ x, uint8_t* __restrict__ xp,
                     size_t row_bytes) {
-  pdl_trigger();  // at entry: lets the expert launch start its weight prefetch early (see expert_swap.cu)
+  if (nblk == 1) pdl_trigger();  // decode-sized: at entry (see perm_gather_kernel)
   pdl_wait();
+  if (nblk > 1) pdl_trigger();
   __shared__ int base[kMaxE];
   __shared__ int warp_cnt[kWarpsPer][kMaxE];
   __shared__ int pass_tot[kMaxE];
